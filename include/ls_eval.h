@@ -1,0 +1,199 @@
+/*
+ * ls_eval.h — C ABI of the B200 batched strategy evaluator (libls_eval.so).
+ *
+ * Drop-in boundary for the Learn-to-Shard cost model. The reference has no
+ * native code and no batched API: every caller scores one candidate at a
+ * time through
+ *
+ *     SearchEnv.evaluate_raw(strategy) -> SimResult
+ *         pkg/src/shardsearch/env.py:140-150   (the seam, called from step :152-180)
+ *     simulate(SimRequest) -> SimResult
+ *         pkg/src/shardsearch/simulator.py:239-341
+ *
+ * This header is what a binding for that seam links against (ctypes stub in
+ * INTEGRATION.md). Everything is POD: plain pointers, sizes and status codes;
+ * no C++ exceptions or torch types cross it. Device buffers are owned by the
+ * caller; a context owns only its per-workload tables. All device entry points
+ * are stream-ordered and asynchronous; a context is immutable after creation,
+ * so concurrent calls on distinct streams are safe.
+ *
+ * Candidate wire format: the reference's flat index vector
+ * (strategy.py:220-263, encode_strategy / decode_strategy), stored
+ * struct-of-arrays: head h of candidate i is planes[h * plane_stride + i]
+ * (one uint8 per head). Heads 0..3 index the tp/ep/pp/batch domains, heads
+ * 4.. are per-operator axis choices (AxisChoice, strategy.py:17-28).
+ */
+#ifndef LS_EVAL_H
+#define LS_EVAL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LS_ABI_VERSION 1u
+#define LS_MAX_DOMAIN 64 /* entries per tp/ep/pp/batch domain */
+#define LS_MAX_HEADS 64  /* max vector length A */
+#define LS_NUM_OPS 12    /* canonical fused operators, strategy.py:65-78 */
+
+/* Status codes returned by every entry point. */
+enum {
+  LS_OK = 0,
+  LS_ERR_INVALID_ARGUMENT = 1,
+  LS_ERR_CUDA = 2,
+  LS_ERR_OUT_OF_MEMORY = 3,
+  LS_ERR_UNSUPPORTED = 4
+};
+
+/* Verdict codes, in InvalidReason declaration order (simulator.py:48-53).
+ * LS_REASON_DECODE_ERROR marks a vector decode_strategy would reject with
+ * DecodingError (strategy.py:245-254); the Python facade raises it. */
+enum {
+  LS_REASON_NONE = 0,
+  LS_REASON_OVER_DEVICE_BUDGET = 1,
+  LS_REASON_LAYOUT_ERROR = 2,
+  LS_REASON_OOM = 3,
+  LS_REASON_SLO_VIOLATION = 4,
+  LS_REASON_DECODE_ERROR = 255
+};
+
+/* Canonical fused operators, in _CANONICAL_OPS order (strategy.py:65-78). */
+enum {
+  LS_OP_EMBEDDING = 0,
+  LS_OP_QKV_PROJ = 1,
+  LS_OP_KV_CACHE_IO = 2,
+  LS_OP_ATTN_CORE = 3,
+  LS_OP_ATTN_OUT_PROJ = 4,
+  LS_OP_ROUTER_GATE = 5,
+  LS_OP_EXPERT_FFN1 = 6,
+  LS_OP_EXPERT_FFN2 = 7,
+  LS_OP_SHARED_FFN1 = 8,
+  LS_OP_SHARED_FFN2 = 9,
+  LS_OP_FINAL_NORM = 10,
+  LS_OP_LM_HEAD = 11
+};
+
+/* Float summation order of _plan_times (simulator.py:232-235): Python's
+ * builtin sum() is a naive left fold up to 3.11 and Neumaier-compensated
+ * from 3.12 on. The evaluator reproduces whichever the caller names. */
+enum { LS_SUM_NAIVE = 0, LS_SUM_NEUMAIER = 1 };
+
+/* Top-k keys. */
+enum {
+  LS_KEY_RAW = 0,   /* raw throughput of valid candidates (build_report by_raw, ppo.py:441-447) */
+  LS_KEY_REWARD = 1 /* shaped reward of valid candidates (EliteBuffer.offer, policy.py:86-102) */
+};
+
+/* One workload: ModelSpec + HardwareSpec + SimRequest knobs + ActionSpaceSpec. */
+typedef struct ls_workload_desc {
+  uint32_t abi_version; /* = LS_ABI_VERSION */
+  uint32_t sum_mode;    /* LS_SUM_NAIVE / LS_SUM_NEUMAIER */
+  /* ModelSpec, model.py:13-36 */
+  int64_t num_layers, hidden_dim, num_heads, head_dim, num_kv_heads, ffn_dim;
+  int64_t num_experts, experts_per_token, vocab_size, dtype_bytes;
+  int32_t has_shared_expert;
+  int32_t reserved0;
+  /* HardwareSpec, model.py:74-93 */
+  double peak_flops, hbm_bandwidth, hbm_capacity, intra_node_bw, inter_node_bw;
+  int64_t node_size, device_budget;
+  double kernel_overhead, per_collective_latency;
+  /* SimRequest, simulator.py:56-73 */
+  int64_t context_len;
+  double slo_tpot;
+  /* ActionSpaceSpec, strategy.py:106-175: domains in head order tp, ep, pp, batch */
+  int32_t domain_len[4];
+  int64_t domain[4][LS_MAX_DOMAIN];
+  int32_t vector_length; /* A = 4 + len(op_names) */
+  /* Axis source per canonical op (Strategy.axis_of, strategy.py:209-214):
+   * op_head[k] >= 4 is the head index that controls op k; -1 means the op
+   * is not controlled and takes op_pinned[k] (pins, default UNSHARDED). */
+  int8_t op_head[LS_NUM_OPS];
+  int8_t op_pinned[LS_NUM_OPS];
+} ls_workload_desc;
+
+/* Per-candidate results, struct-of-arrays. reason is required; any other
+ * pointer may be NULL to skip that field. Field conventions follow SimResult
+ * (simulator.py:89-97, :246-255): over-budget / layout-error / decode-error
+ * leave every number 0; OOM sets only memory_bytes; SLO sets tpot, memory and
+ * the breakdown with throughput 0. */
+typedef struct ls_result_soa {
+  uint8_t* reason;
+  double* throughput; /* tokens/s/chip, the raw objective */
+  double* tpot_s;
+  double* memory_bytes;
+  double* compute_s;
+  double* comm_s;
+  double* pipeline_s;
+} ls_result_soa;
+
+/* One elite / top-k record. code is the candidate's mixed-radix rank over the
+ * head sizes (head 0 most significant), i.e. its index in
+ * itertools.product(*map(range, head_sizes)) order; index is the candidate's
+ * global position in the evaluated stream. */
+typedef struct ls_elite_rec {
+  double key;    /* raw or reward, per key kind */
+  double raw;    /* raw throughput */
+  int64_t index; /* global candidate index (ties: smaller wins) */
+  uint64_t code; /* mixed-radix vector code (dedupe + decode) */
+} ls_elite_rec;
+
+typedef struct ls_ctx ls_ctx;
+
+/* Last error message of the calling thread ("" when none). */
+const char* ls_last_error(void);
+uint32_t ls_abi_version(void);
+
+/* Validate the workload, build its per-workload tables on `device`. */
+int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out);
+int ls_ctx_destroy(ls_ctx* ctx);
+/* Size of the encodable space (product of head sizes); 0 if it overflows. */
+uint64_t ls_space_size(const ls_ctx* ctx);
+
+/* Score n candidates already resident on the device (SoA planes). */
+int ls_evaluate(ls_ctx* ctx, const uint8_t* planes, int64_t n, int64_t plane_stride,
+                const ls_result_soa* out, void* stream);
+
+/* Same, from and to HOST memory: chunked H2D copy -> evaluate -> D2H copy,
+ * double-buffered across two internal streams; returns when results are in
+ * host memory. Host buffers should be pinned (ls_host_alloc) for full speed. */
+int ls_evaluate_host(ls_ctx* ctx, const uint8_t* host_planes, int64_t n, int64_t plane_stride,
+                     const ls_result_soa* host_out);
+
+/* Pinned host memory helpers for ls_evaluate_host callers. */
+int ls_host_alloc(size_t bytes, void** out);
+int ls_host_free(void* ptr);
+
+/* Reward shaping of SearchEnv.step (env.py:159-164, :178-179) over a batch:
+ *   b_i = max(b0, max{raw_j : j < i, valid_j})     (exclusive running best)
+ *   reward_i = alpha*raw_i + beta*(raw_i - b_i)  if valid_i else penalty
+ * raw_i is throughput for valid candidates and 0 otherwise. best_out (device,
+ * optional) receives max(b0, all valid raw), the env's best_raw afterwards.
+ * scratch must hold ls_scan_scratch_bytes(n) bytes of device memory. */
+size_t ls_scan_scratch_bytes(int64_t n);
+int ls_reward_scan(ls_ctx* ctx, const uint8_t* reason, const double* throughput, int64_t n,
+                   double b0, double alpha, double beta, double penalty, double* reward_out,
+                   double* best_out, void* scratch, void* stream);
+
+/* Top-k of valid candidates by (key desc, index asc) over DISTINCT vectors
+ * (first occurrence kept), written best first to out[0..k) on the device;
+ * count_out (device int32) receives the number of records filled (<= k).
+ * key is `throughput` for LS_KEY_RAW or the reward array for LS_KEY_REWARD.
+ * index_base is added to local positions (global stream offset). planes are
+ * the candidate vectors (for the dedupe code). scratch must hold
+ * ls_topk_scratch_bytes(n, k) bytes. k <= 64. */
+size_t ls_topk_scratch_bytes(int64_t n, int k);
+int ls_topk(ls_ctx* ctx, const uint8_t* planes, int64_t plane_stride, const uint8_t* reason,
+            const double* throughput, const double* key, int64_t n, int k, int64_t index_base,
+            ls_elite_rec* out, int32_t* count_out, void* scratch, void* stream);
+
+/* Merge m device-resident record lists (e.g. the all-gathered per-rank top-k)
+ * into the global top-k with the same ordering and dedupe rule. */
+int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
+                  ls_elite_rec* out, int32_t* count_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LS_EVAL_H */
