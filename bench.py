@@ -1,0 +1,345 @@
+"""Benchmark: batched strategy evaluation (evals/s) on B200, 1..8 GPUs.
+
+Metric (BASELINE.json): strategy evaluations per second, whole job.
+Workload: BASELINE config 4 — the 1.6T-parameter MoE on 2048 simulated H100s
+(packaged config ``moe_1p6t_h100x2048``), candidates i.i.d. uniform over every
+head (baselines.uniform_vector semantics, reference baselines.py:50-54),
+generated on each GPU from a per-rank seed. Weak scaling: each rank scores
+its own batch of ``--n`` candidates per step (contiguous global index range),
+so inputs (16 B/candidate, ~2 GB) dwarf the 126 MB L2 — no flush needed.
+
+One step = the hot path over one batch:
+  evaluate (reason + raw throughput per candidate, HBM SoA in/out)
+  -> device top-k by raw over distinct vectors (elite of the batch)
+  -> (N > 1) NCCL all-gather of the per-rank top-k + device merge.
+
+Also reported: ``e2e`` — the same metric through the public API with HOST
+buffers (Evaluator.evaluate_host -> ls_evaluate_host: pinned H2D of the
+planes, kernels, D2H of reason + raw, inside the timed region);
+``roofline`` of the evaluate kernel (25 algorithmic bytes per candidate ÷
+its CUDA-event time vs the measured HBM copy peak); ``cpu_baseline`` — the
+C restatement of the reference cost model (oracle/, a "port") on this
+host's cores over a bounded sample.
+
+``--impl reference`` times that CPU port alone (the reference is pure
+Python with no native path to build).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "strategy evals/sec"
+UNIT = "evals/s"
+CONFIG = "moe_1p6t_h100x2048"
+ALGO_BYTES = 16 + 1 + 8  # per candidate: 16 head bytes in, reason u8 + raw f64 out
+ELITE_K = 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--n", type=int, default=1 << 27, help="candidates per GPU per step")
+    ap.add_argument("--e2e-n", type=int, default=1 << 26, help="candidates per GPU per e2e step")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def uniform_planes_np(head_sizes, n, seed):
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.integers(0, k, size=n, dtype=np.uint8) for k in head_sizes])
+
+
+# ----------------------------------------------------------------- CPU side
+
+
+def cpu_rate(workload, seconds, seed=0, sample=1 << 23):
+    """Oracle C port over all host cores: evals/s on a bounded uniform sample."""
+    from oracle.cost_model import simulate_planes
+
+    threads = os.cpu_count() or 1
+    planes = uniform_planes_np(workload.space.head_sizes, sample, seed)
+    desc = workload.desc()
+    simulate_planes(desc, planes[:, : 1 << 16], threads=threads)  # warm
+    done, t0 = 0, time.perf_counter()
+    while True:
+        simulate_planes(desc, planes, threads=threads)
+        done += sample
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return done / el, threads, done
+
+
+def run_reference(args, rank):
+    from paper_2509_00217_b200.config import load_workload
+    from oracle.cost_model import simulate_planes
+
+    if rank != 0:
+        return
+    wl = load_workload(args.config)
+    threads = os.cpu_count() or 1
+    sample = 1 << 22
+    planes = uniform_planes_np(wl.space.head_sizes, sample, 0)
+    desc = wl.desc()
+    for _ in range(args.warmup):
+        simulate_planes(desc, planes, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        simulate_planes(desc, planes, threads=threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: uniform candidates (baselines.uniform_vector), {sample} per step",
+                   "candidates_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} uniform candidates x {args.steps} steps, oracle/shardsim_oracle.c "
+                                   f"(C restatement of simulator.py:239-341), {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU side
+
+
+class Clocks:
+    """nvidia-smi sampler running across the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_00217_b200.config import load_workload
+    from paper_2509_00217_b200.evaluator import BatchResult, Evaluator
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    wl = load_workload(args.config)
+    ev = Evaluator(wl, device=local_rank)
+    sizes = ev.head_sizes
+    n = args.n
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    planes = torch.empty((len(sizes), n), dtype=torch.uint8, device=dev)
+    for h, k in enumerate(sizes):
+        planes[h] = torch.randint(0, k, (n,), generator=gen, device=dev, dtype=torch.uint8)
+    out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=dev),
+                      throughput=torch.empty(n, dtype=torch.float64, device=dev))
+    base = rank * n  # contiguous global index range per rank
+    rec_bytes = 32
+    gathered = torch.empty((world * ELITE_K, rec_bytes), dtype=torch.uint8, device=dev) if world > 1 else None
+    gcounts = torch.empty(world, dtype=torch.int32, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+    ev_start, ev_end = [], []
+
+    def step(timed):
+        if timed:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        ev.evaluate(planes, out=out)
+        if timed:
+            b.record(stream)
+            ev_start.append(a)
+            ev_end.append(b)
+        recs, count = ev.topk_records(planes, out.reason, out.throughput, k=ELITE_K, index_base=base)
+        launches = 3
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, recs)
+            dist.all_gather_into_tensor(gcounts, count)
+            recs, count = ev.merge_records(gathered, gcounts, ELITE_K, ELITE_K)
+            launches += 1
+        return recs, count, launches
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_start.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        recs, count, nl = step(True)
+        launches += nl
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kern_ms = [s.elapsed_time(e) for s, e in zip(ev_start, ev_end)]
+    elite = ev.decode_records(recs, count)
+
+    # max over ranks of the device time
+    if world > 1:
+        t = torch.tensor([elapsed_ms, statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, kern_avg = float(t[0]), float(t[1])
+    else:
+        kern_avg = statistics.mean(kern_ms)
+
+    # end-to-end through the public host API: pinned host planes in, host verdicts out
+    e2e_n = min(args.e2e_n, n)
+    host_planes = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
+    host_planes.copy_(planes[:, :e2e_n].cpu())
+    hp = host_planes.numpy()
+    e2e_steps = max(3, min(args.steps, 10))
+    ev.evaluate_host(hp)  # warm: allocates the pipeline buffers
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = ev.evaluate_host(hp)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e_value = world * e2e_n * e2e_steps / e2e_s
+    del res
+
+    if rank != 0:
+        return
+    value = world * n * args.steps / (elapsed_ms / 1e3)
+    pk, pk_kind = peaks()
+    achieved_gbs = ALGO_BYTES * n / (kern_avg / 1e3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "roofline_traffic.json"
+    if tfile.exists():
+        try:
+            tj = json.loads(tfile.read_text())
+            if tj.get("config") == args.config and tj.get("n") == n:
+                traffic = tj.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: uniform candidates (baselines.uniform_vector), "
+                               f"{n} per GPU per step, SoA uint8 planes in HBM",
+                   "candidates_per_gpu": n, "elite_k": ELITE_K, "parallelism": f"dp{world} (index-range shards)",
+                   "l2": "inputs 16 B x n per GPU >> 126 MB L2; no flush"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * len(sizes),
+                "d2h_bytes_per_step": world * e2e_n * 9, "candidates_per_gpu": e2e_n,
+                "api": "Evaluator.evaluate_host -> ls_evaluate_host"},
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                     "frac": achieved_gbs / pk.get("hbm_gbs"), "traffic": traffic,
+                     "kernel": "eval_vec4_kernel", "algorithmic_bytes_per_candidate": ALGO_BYTES,
+                     "kernel_ms_avg": kern_avg, "peak_source": f"{pk_kind} hbm_gbs (MEASURED_PEAKS.json)"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "elite_best": {"vector": list(elite[0].vector), "raw": elite[0].raw, "index": elite[0].index} if elite else None,
+    }
+    if not args.no_cpu:
+        rate, cores, done = cpu_rate(wl, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"{done} uniform candidates of {args.config} through oracle/shardsim_oracle.c"
+                                          f" (C restatement of the reference cost model), {cores} threads"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

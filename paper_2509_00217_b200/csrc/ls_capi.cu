@@ -1,0 +1,376 @@
+// ls_capi.cu — the C ABI of libls_eval.so (declared in include/ls_eval.h).
+//
+// Owns per-workload contexts (validated descriptor, device tables, launch
+// plan) and the host<->device pipeline of ls_evaluate_host. No exception
+// crosses the ABI; every entry returns a status and records a message
+// retrievable with ls_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ls_eval.h"
+#include "ls_kernels.h"
+
+using namespace ls;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(LS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+constexpr int kHostChunk = 1 << 22;  // candidates per pipelined host chunk
+constexpr size_t kSmemTableLimit = 200 * 1024;
+
+}  // namespace
+
+struct ls_ctx {
+  ls_workload_desc desc;
+  TabLayout L;
+  EvalMeta M;
+  TopkMeta TM;
+  int device = 0;
+  int num_sms = 148;
+  uint64_t* d_tab = nullptr;
+  bool smem_tables = false;
+  int64_t blocks_vec4 = 0, blocks_generic = 0;
+  uint64_t space_size = 0;
+  // host pipeline
+  std::mutex host_mu;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  uint8_t* h_planes[2] = {nullptr, nullptr};
+  uint8_t* h_reason[2] = {nullptr, nullptr};
+  double* h_f[2][6] = {};
+};
+
+namespace {
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0; }
+
+int validate(const ls_workload_desc& d) {
+  if (d.abi_version != LS_ABI_VERSION) return fail(LS_ERR_INVALID_ARGUMENT, "abi_version mismatch");
+  if (d.sum_mode > 1) return fail(LS_ERR_INVALID_ARGUMENT, "sum_mode must be 0 (naive) or 1 (neumaier)");
+  const int64_t ints[] = {d.num_layers,  d.hidden_dim,        d.num_heads,  d.head_dim,   d.num_kv_heads,
+                          d.ffn_dim,     d.num_experts,       d.experts_per_token, d.vocab_size, d.dtype_bytes,
+                          d.node_size,   d.device_budget,     d.context_len};
+  for (int64_t v : ints)
+    if (v < 1 || v > (int64_t(1) << 40)) return fail(LS_ERR_INVALID_ARGUMENT, "model/hardware integers must be in [1, 2^40]");
+  if (d.num_heads * d.head_dim != d.hidden_dim)
+    return fail(LS_ERR_INVALID_ARGUMENT, "model.num_heads * model.head_dim must equal model.hidden_dim");
+  if (d.num_heads % d.num_kv_heads) return fail(LS_ERR_INVALID_ARGUMENT, "model.num_kv_heads must divide model.num_heads");
+  if (d.experts_per_token > d.num_experts)
+    return fail(LS_ERR_INVALID_ARGUMENT, "model.experts_per_token must not exceed model.num_experts");
+  if (!finite_pos(d.peak_flops) || !finite_pos(d.hbm_bandwidth) || !finite_pos(d.hbm_capacity) ||
+      !finite_pos(d.intra_node_bw) || !finite_pos(d.inter_node_bw))
+    return fail(LS_ERR_INVALID_ARGUMENT, "hardware rates must be positive and finite");
+  if (!(std::isfinite(d.kernel_overhead) && d.kernel_overhead >= 0) ||
+      !(std::isfinite(d.per_collective_latency) && d.per_collective_latency >= 0))
+    return fail(LS_ERR_INVALID_ARGUMENT, "hardware overheads must be non-negative and finite");
+  if (!finite_pos(d.slo_tpot)) return fail(LS_ERR_INVALID_ARGUMENT, "slo_tpot must be positive");
+  for (int h = 0; h < 4; ++h) {
+    if (d.domain_len[h] < 1 || d.domain_len[h] > LS_MAX_DOMAIN)
+      return fail(LS_ERR_INVALID_ARGUMENT, "domain lengths must be in [1, 64]");
+    for (int j = 0; j < d.domain_len[h]; ++j)
+      if (d.domain[h][j] < 1 || d.domain[h][j] > (1 << 20))
+        return fail(LS_ERR_INVALID_ARGUMENT, "domain values must be in [1, 2^20]");
+  }
+  if (d.vector_length < 4 || d.vector_length > LS_MAX_HEADS)
+    return fail(LS_ERR_INVALID_ARGUMENT, "vector_length must be in [4, 64]");
+  bool used[LS_MAX_HEADS] = {};
+  for (int k = 0; k < LS_NUM_OPS; ++k) {
+    const int h = d.op_head[k];
+    if (h == -1) {
+      if (d.op_pinned[k] < 0 || d.op_pinned[k] > 2) return fail(LS_ERR_INVALID_ARGUMENT, "op_pinned must be 0..2");
+      continue;
+    }
+    if (h < 4 || h >= d.vector_length || used[h])
+      return fail(LS_ERR_INVALID_ARGUMENT, "op_head entries must be distinct heads in [4, vector_length)");
+    used[h] = true;
+  }
+  // exact int->double conversions (< 2^53) for every product the model forms
+  const double lim = 9007199254740992.0;
+  const double h = (double)d.hidden_dim;
+  const double qkv = (double)((d.num_heads + 2 * d.num_kv_heads) * d.head_dim);
+  const double dense = 2.0 * d.vocab_size * h + d.num_layers * (h * qkv + h * h + h * d.num_experts + 4 * h) +
+                       (d.has_shared_expert ? d.num_layers * 2.0 * h * d.ffn_dim : 0.0) + h;
+  const double routed = (double)d.num_layers * d.num_experts * 2.0 * h * d.ffn_dim;
+  int64_t bmax = 0;
+  for (int j = 0; j < d.domain_len[3]; ++j) bmax = std::max<int64_t>(bmax, d.domain[3][j]);
+  const double widest = std::max({h, qkv, (double)d.ffn_dim, (double)d.vocab_size});
+  if (dense * d.dtype_bytes >= lim || routed * d.dtype_bytes >= lim ||
+      (double)bmax * d.experts_per_token * widest * d.dtype_bytes >= lim)
+    return fail(LS_ERR_UNSUPPORTED, "workload integers exceed 2^53: exact float64 parity is not guaranteed");
+  return LS_OK;
+}
+
+void build_meta(ls_ctx* c) {
+  const ls_workload_desc& d = c->desc;
+  EvalMeta& M = c->M;
+  std::memset(&M, 0, sizeof(M));
+  M.A = d.vector_length;
+  for (int h = 0; h < LS_MAX_HEADS; ++h) {
+    M.head_size[h] = h < 4 ? (uint8_t)d.domain_len[h] : 3;
+    M.head_op[h] = -1;
+  }
+  M.pinned_axes = 0;
+  for (int k = 0; k < LS_NUM_OPS; ++k) {
+    if (d.op_head[k] >= 0) M.head_op[d.op_head[k]] = (int8_t)k;
+    else M.pinned_axes |= (uint32_t)d.op_pinned[k] << (2 * k);
+  }
+  for (int p = 0; p < d.domain_len[2]; ++p)
+    if (d.num_layers % d.domain[2][p]) M.pp_bad |= 1ull << p;
+  for (int e = 0; e < d.domain_len[1]; ++e) {
+    const int64_t ep = d.domain[1][e];
+    if (ep > d.num_experts || d.num_experts % ep) M.ep_bad |= 1ull << e;
+  }
+  M.device_budget = d.device_budget;
+  M.node_size = d.node_size;
+  M.num_layers_d = (double)d.num_layers;
+  M.slo_tpot = d.slo_tpot;
+  M.hbm_capacity = d.hbm_capacity;
+  // mixed-radix place values, head 0 most significant
+  unsigned __int128 stride = 1;
+  bool overflow = false;
+  for (int h = d.vector_length - 1; h >= 0; --h) {
+    M.code_stride[h] = (int64_t)stride;
+    stride *= M.head_size[h];
+    if (stride >= ((unsigned __int128)1 << 63)) overflow = true;
+  }
+  c->space_size = overflow ? 0 : (uint64_t)stride;
+  c->TM.A = M.A;
+  for (int h = 0; h < LS_MAX_HEADS; ++h) c->TM.code_stride[h] = M.code_stride[h];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ls_last_error(void) { return g_err.c_str(); }
+uint32_t ls_abi_version(void) { return LS_ABI_VERSION; }
+
+int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
+  g_err.clear();
+  if (!desc || !out) return fail(LS_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  int rc = validate(*desc);
+  if (rc) return rc;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return fail(LS_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev) return fail(LS_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(LS_ERR_CUDA, "cudaSetDevice failed");
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) return fail(LS_ERR_UNSUPPORTED, "libls_eval.so is built for sm_100a (B200)");
+  ls_ctx* c = new ls_ctx();
+  c->desc = *desc;
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->L = make_layout(c->desc);
+  build_meta(c);
+  const size_t tab_bytes = (size_t)c->L.words * 8;
+  if ((e = cudaMalloc(&c->d_tab, tab_bytes)) != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(tables)");
+  }
+  if ((e = build_tables(c->desc, c->L, c->d_tab, 0)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    cudaFree(c->d_tab);
+    delete c;
+    return cuda_fail(e, "build_tables");
+  }
+  c->smem_tables = tab_bytes <= kSmemTableLimit && tab_bytes <= (size_t)prop.sharedMemPerBlockOptin;
+  const size_t smem = c->smem_tables ? tab_bytes : 0;
+  if (c->smem_tables) prepare_eval_kernels(smem);
+  const int occ4 = std::max(1, occupancy_blocks_per_sm(true, c->smem_tables, smem));
+  const int occg = std::max(1, occupancy_blocks_per_sm(false, c->smem_tables, smem));
+  c->blocks_vec4 = (int64_t)c->num_sms * occ4;
+  c->blocks_generic = (int64_t)c->num_sms * occg;
+  if ((e = cudaGetLastError()) != cudaSuccess) {
+    cudaFree(c->d_tab);
+    delete c;
+    return cuda_fail(e, "kernel setup");
+  }
+  *out = c;
+  return LS_OK;
+}
+
+int ls_ctx_destroy(ls_ctx* c) {
+  if (!c) return LS_OK;
+  DeviceGuard g(c->device);
+  for (int s = 0; s < 2; ++s) {
+    if (c->hs[s]) cudaStreamDestroy(c->hs[s]);
+    cudaFree(c->h_planes[s]);
+    cudaFree(c->h_reason[s]);
+    for (int f = 0; f < 6; ++f) cudaFree(c->h_f[s][f]);
+  }
+  cudaFree(c->d_tab);
+  delete c;
+  return LS_OK;
+}
+
+uint64_t ls_space_size(const ls_ctx* c) { return c ? c->space_size : 0; }
+
+static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stride, const ls_result_soa* out,
+                       cudaStream_t s) {
+  if (n < 0 || !out || !out->reason || (n > 0 && !planes)) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate arguments");
+  if (stride < n) return fail(LS_ERR_INVALID_ARGUMENT, "plane_stride must be >= n");
+  if (n == 0) return LS_OK;
+  EvalArgs a;
+  a.planes = planes;
+  a.n = n;
+  a.stride = stride;
+  a.reason = out->reason;
+  a.thr = out->throughput;
+  a.tpot = out->tpot_s;
+  a.mem = out->memory_bytes;
+  a.comp = out->compute_s;
+  a.comm = out->comm_s;
+  a.pipe = out->pipeline_s;
+  bool vec4 = c->M.A <= 16 && aligned(planes, 4) && stride % 4 == 0 && aligned(a.reason, 4);
+  const double* fs[6] = {a.thr, a.tpot, a.mem, a.comp, a.comm, a.pipe};
+  for (const double* f : fs) vec4 = vec4 && aligned(f, 16);
+  LaunchPlan lp;
+  lp.vec4 = vec4;
+  lp.max_blocks = vec4 ? c->blocks_vec4 : c->blocks_generic;
+  cudaError_t e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->smem_tables, c->d_tab, c->L, c->M, a, s);
+  if (e != cudaSuccess) return cuda_fail(e, "evaluate launch");
+  return LS_OK;
+}
+
+int ls_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_stride, const ls_result_soa* out,
+                void* stream) {
+  g_err.clear();
+  if (!c) return fail(LS_ERR_INVALID_ARGUMENT, "null context");
+  DeviceGuard g(c->device);
+  return do_evaluate(c, planes, n, plane_stride, out, static_cast<cudaStream_t>(stream));
+}
+
+int ls_evaluate_host(ls_ctx* c, const uint8_t* host_planes, int64_t n, int64_t plane_stride,
+                     const ls_result_soa* host_out) {
+  g_err.clear();
+  if (!c || !host_out || !host_out->reason || (n > 0 && !host_planes) || n < 0 || plane_stride < n)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host arguments");
+  if (n == 0) return LS_OK;
+  std::lock_guard<std::mutex> lock(c->host_mu);
+  DeviceGuard g(c->device);
+  const int A = c->desc.vector_length;
+  double* hf[6] = {host_out->throughput, host_out->tpot_s, host_out->memory_bytes,
+                   host_out->compute_s,  host_out->comm_s, host_out->pipeline_s};
+  cudaError_t e;
+  for (int s = 0; s < 2; ++s) {
+    if (!c->hs[s] && (e = cudaStreamCreateWithFlags(&c->hs[s], cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream create");
+    if (!c->h_planes[s]) {
+      if ((e = cudaMalloc(&c->h_planes[s], (size_t)LS_MAX_HEADS * kHostChunk)) != cudaSuccess ||
+          (e = cudaMalloc(&c->h_reason[s], kHostChunk)) != cudaSuccess)
+        return cuda_fail(e, "pipeline buffers");
+    }
+    for (int f = 0; f < 6; ++f)
+      if (hf[f] && !c->h_f[s][f] && (e = cudaMalloc(&c->h_f[s][f], sizeof(double) * kHostChunk)) != cudaSuccess)
+        return cuda_fail(e, "pipeline buffers");
+  }
+  int64_t chunk = 0;
+  for (int64_t off = 0; off < n; off += kHostChunk, ++chunk) {
+    const int s = (int)(chunk & 1);
+    const int64_t cnt = std::min<int64_t>(kHostChunk, n - off);
+    cudaStream_t st = c->hs[s];
+    if ((e = cudaMemcpy2DAsync(c->h_planes[s], (size_t)cnt, host_planes + off, (size_t)plane_stride, (size_t)cnt, A,
+                               cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "H2D planes");
+    ls_result_soa dev;
+    dev.reason = c->h_reason[s];
+    double** dv[6] = {&dev.throughput, &dev.tpot_s, &dev.memory_bytes, &dev.compute_s, &dev.comm_s, &dev.pipeline_s};
+    for (int f = 0; f < 6; ++f) *dv[f] = hf[f] ? c->h_f[s][f] : nullptr;
+    int rc = do_evaluate(c, c->h_planes[s], cnt, cnt, &dev, st);
+    if (rc) return rc;
+    if ((e = cudaMemcpyAsync(host_out->reason + off, dev.reason, (size_t)cnt, cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+      return cuda_fail(e, "D2H reason");
+    for (int f = 0; f < 6; ++f)
+      if (hf[f] && (e = cudaMemcpyAsync(hf[f] + off, *dv[f], sizeof(double) * cnt, cudaMemcpyDeviceToHost, st)) !=
+                       cudaSuccess)
+        return cuda_fail(e, "D2H field");
+  }
+  for (int s = 0; s < 2; ++s)
+    if ((e = cudaStreamSynchronize(c->hs[s])) != cudaSuccess) return cuda_fail(e, "pipeline sync");
+  return LS_OK;
+}
+
+int ls_host_alloc(size_t bytes, void** out) {
+  g_err.clear();
+  if (!out) return fail(LS_ERR_INVALID_ARGUMENT, "null out");
+  cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "cudaHostAlloc");
+}
+
+int ls_host_free(void* p) {
+  cudaError_t e = cudaFreeHost(p);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "cudaFreeHost");
+}
+
+size_t ls_scan_scratch_bytes(int64_t n) { return scan_scratch_bytes(n); }
+
+int ls_reward_scan(ls_ctx* c, const uint8_t* reason, const double* throughput, int64_t n, double b0, double alpha,
+                   double beta, double penalty, double* reward_out, double* best_out, void* scratch, void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || (n > 0 && (!reason || !throughput || !reward_out || !scratch)))
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad reward_scan arguments");
+  DeviceGuard g(c->device);
+  cudaError_t e = launch_reward_scan(reason, throughput, n, b0, alpha, beta, penalty, reward_out, best_out, scratch,
+                                     c->num_sms, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "reward_scan launch");
+}
+
+size_t ls_topk_scratch_bytes(int64_t n, int k) { return topk_scratch_bytes(n, k < 1 ? 1 : k, 0); }
+
+int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_t* reason, const double* throughput,
+            const double* key, int64_t n, int k, int64_t index_base, ls_elite_rec* out, int32_t* count_out,
+            void* scratch, void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || k < 1 || k > 64 || !out || !count_out || !scratch ||
+      (n > 0 && (!planes || !reason || !throughput || !key)) || plane_stride < n)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad topk arguments (k must be in [1, 64])");
+  if (c->space_size == 0) return fail(LS_ERR_UNSUPPORTED, "vector codes overflow 63 bits for this action space");
+  DeviceGuard g(c->device);
+  cudaError_t e = launch_topk(c->TM, planes, plane_stride, reason, throughput, key, n, k, index_base, out, count_out,
+                              scratch, c->num_sms, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
+}
+
+int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k, ls_elite_rec* out,
+                  int32_t* count_out, void* stream) {
+  g_err.clear();
+  if (!recs || !counts || m < 1 || k_in < 1 || k_in > 64 || k < 1 || k > 64 || !out || !count_out)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad topk_merge arguments");
+  cudaError_t e = launch_topk_merge(recs, counts, m, k_in, k, out, count_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge launch");
+}
+
+}  // extern "C"

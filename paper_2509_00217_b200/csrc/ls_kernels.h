@@ -1,0 +1,49 @@
+// ls_kernels.h — internal launch interface between the C ABI (ls_capi.cu)
+// and the kernels. Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ls_tables.cuh"
+
+namespace ls {
+
+struct EvalArgs {
+  const uint8_t* planes;
+  int64_t n;
+  int64_t stride;
+  uint8_t* reason;
+  double *thr, *tpot, *mem, *comp, *comm, *pipe;
+};
+
+struct LaunchPlan {
+  bool vec4;
+  int64_t max_blocks;
+};
+
+cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
+
+cudaError_t prepare_eval_kernels(size_t smem_bytes);
+int occupancy_blocks_per_sm(bool vec4, bool smem_tables, size_t smem);
+cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, bool smem_tables, const uint64_t* tab,
+                            const TabLayout& L, const EvalMeta& M, const EvalArgs& a, cudaStream_t s);
+
+// Reward scan (ls_select.cu)
+size_t scan_scratch_bytes(int64_t n);
+cudaError_t launch_reward_scan(const uint8_t* reason, const double* thr, int64_t n, double b0, double alpha,
+                               double beta, double penalty, double* reward, double* best_out, void* scratch,
+                               int num_sms, cudaStream_t s);
+
+// Top-k (ls_select.cu)
+struct TopkMeta {
+  int A;
+  int64_t code_stride[LS_MAX_HEADS];
+};
+size_t topk_scratch_bytes(int64_t n, int k, int num_sms);
+cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t stride, const uint8_t* reason,
+                        const double* thr, const double* key, int64_t n, int k, int64_t index_base,
+                        ls_elite_rec* out, int32_t* count_out, void* scratch, int num_sms, cudaStream_t s);
+cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
+                              ls_elite_rec* out, int32_t* count_out, cudaStream_t s);
+
+}  // namespace ls

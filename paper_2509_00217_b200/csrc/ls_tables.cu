@@ -1,0 +1,164 @@
+// ls_tables.cu — device-side construction of the per-workload tables.
+//
+// One thread per table word. Each word is the reference's own expression for
+// that (op, axis, tp, batch[, ep][, attn axis]) tuple (ls_formulas.cuh), so
+// the evaluate kernel only has to gather and sum. Runs once per context.
+#include "ls_formulas.cuh"
+#include "ls_tables.cuh"
+
+namespace ls {
+
+namespace {
+
+__device__ inline uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
+
+
+// Decompose a flat row-major index over dims (d0..d3) into 4 coordinates.
+__device__ inline void unflat(int i, int d1, int d2, int d3, int* c0, int* c1, int* c2, int* c3) {
+  *c3 = i % d3;
+  i /= d3;
+  *c2 = i % d2;
+  i /= d2;
+  *c1 = i % d1;
+  *c0 = i / d1;
+}
+
+__device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, int w) {
+  const int nt = L.nt, ne = L.ne, np = L.np, nb = L.nb;
+  const int64_t* TP = d.domain[0];
+  const int64_t* EP = d.domain[1];
+  const int64_t* PP = d.domain[2];
+  const int64_t* B = d.domain[3];
+  int c0, c1, c2, c3;
+  // [axis][t][b] op-time segments of the batch-token walkers
+  const struct {
+    int off, op;
+  } dense3[] = {{L.opt_emb, LS_OP_EMBEDDING}, {L.opt_qkv, LS_OP_QKV_PROJ}, {L.opt_out, LS_OP_ATTN_OUT_PROJ},
+                {L.opt_sh1, LS_OP_SHARED_FFN1}, {L.opt_sh2, LS_OP_SHARED_FFN2}, {L.opt_lmh, LS_OP_LM_HEAD}};
+  for (int k = 0; k < 6; ++k) {
+    const int off = dense3[k].off, op = dense3[k].op;
+    if ((op == LS_OP_SHARED_FFN1 || op == LS_OP_SHARED_FFN2) && !L.has_shared) continue;
+    if (w >= off && w < off + 3 * nt * nb) {
+      const int i = w - off, b = i % nb, t = (i / nb) % nt, a = i / (nb * nt);
+      return dbits(op_cost_time(d, op, a, (double)B[b], TP[t], 1, false));
+    }
+  }
+  // kv_cache_io / attn_core: [attn_dim1][t][b]
+  if (w >= L.opt_kv && w < L.opt_kv + 2 * nt * nb) {
+    const int i = w - L.opt_kv, b = i % nb, t = (i / nb) % nt, a2 = i / (nb * nt);
+    return dbits(op_cost_time(d, LS_OP_KV_CACHE_IO, 0, (double)B[b], TP[t], 1, a2 != 0));
+  }
+  if (w >= L.opt_attn && w < L.opt_attn + 2 * nt * nb) {
+    const int i = w - L.opt_attn, b = i % nb, t = (i / nb) % nt, a2 = i / (nb * nt);
+    return dbits(op_cost_time(d, LS_OP_ATTN_CORE, a2 ? 2 : 0, (double)B[b], TP[t], 1, a2 != 0));
+  }
+  if (w >= L.opt_router && w < L.opt_router + nb)
+    return dbits(op_cost_time(d, LS_OP_ROUTER_GATE, 0, (double)B[w - L.opt_router], 1, 1, false));
+  if (w >= L.opt_norm && w < L.opt_norm + nb)
+    return dbits(op_cost_time(d, LS_OP_FINAL_NORM, 0, (double)B[w - L.opt_norm], 1, 1, false));
+  // expert ops: [axis][t][e][b], tokens = routed tokens
+  for (int k = 0; k < 2; ++k) {
+    const int off = k ? L.opt_ffn2 : L.opt_ffn1;
+    if (w >= off && w < off + 3 * nt * ne * nb) {
+      unflat(w - off, nt, ne, nb, &c0, &c1, &c2, &c3);
+      const double rt = routed_tokens(d, B[c3], EP[c2]);
+      return dbits(op_cost_time(d, k ? LS_OP_EXPERT_FFN2 : LS_OP_EXPERT_FFN1, c0, rt, TP[c1], EP[c2], false));
+    }
+  }
+  // TP-group collectives: [cls][fam][t][b], tokens = batch
+  if (w >= L.coll && w < L.coll + 8 * nt * nb) {
+    unflat(w - L.coll, 2, nt, nb, &c0, &c1, &c2, &c3);
+    const int64_t feats[4] = {qkv_out_dim(d), d.hidden_dim, d.ffn_dim, d.vocab_size};
+    const double payload = ((double)B[c3] * (double)feats[c0]) * (double)d.dtype_bytes;
+    return dbits(coll_time(d, c1 == 0, TP[c2], payload, TP[c2] <= d.node_size));
+  }
+  // routed ffn1->ffn2 reconcile: [fam][t][e][b], tokens = routed tokens
+  if (w >= L.rtf && w < L.rtf + 2 * nt * ne * nb) {
+    unflat(w - L.rtf, nt, ne, nb, &c0, &c1, &c2, &c3);
+    const double payload = (routed_tokens(d, B[c3], EP[c2]) * (double)d.ffn_dim) * (double)d.dtype_bytes;
+    return dbits(coll_time(d, c0 == 0, TP[c1], payload, TP[c1] <= d.node_size));
+  }
+  // expert dispatch / combine all_to_all: [t][e][b] over the EP group
+  if (w >= L.a2a && w < L.a2a + nt * ne * nb) {
+    unflat(w - L.a2a, 1, nt, ne * nb, &c0, &c1, &c2, &c3);
+    const int t = c2, e = c3 / nb, b = c3 % nb;
+    const double payload = (routed_tokens(d, B[b], EP[e]) * (double)d.hidden_dim) * (double)d.dtype_bytes;
+    return dbits(coll_time(d, false, EP[e], payload, TP[t] * EP[e] <= d.node_size));
+  }
+  // weights per device: [t][e][p]
+  if (w >= L.mem_w && w < L.mem_w + nt * ne * np) {
+    unflat(w - L.mem_w, 1, nt, ne * np, &c0, &c1, &c2, &c3);
+    const int t = c2, e = c3 / np, p = c3 % np;
+    int64_t dense, routed;
+    param_counts(d, &dense, &routed);
+    return dbits(((double)(dense * d.dtype_bytes) / (double)TP[t]) / (double)PP[p] +
+                 ((double)(routed * d.dtype_bytes) / (double)(EP[e] * TP[t])) / (double)PP[p]);
+  }
+  // KV cache per device: [attn_dim1][t][p][b]
+  if (w >= L.mem_kv && w < L.mem_kv + 2 * nt * np * nb) {
+    unflat(w - L.mem_kv, nt, np, nb, &c0, &c1, &c2, &c3);
+    const int64_t share = kv_share(d, TP[c1], c0 != 0);
+    return dbits(((((2.0 * ((double)d.num_layers / (double)PP[c2])) *
+                    ((double)(d.num_kv_heads * d.head_dim) / (double)share)) *
+                   (double)d.context_len) *
+                  (double)B[c3]) *
+                 (double)d.dtype_bytes);
+  }
+  if (w >= L.mem_ws && w < L.mem_ws + nb) {
+    const int b = w - L.mem_ws;
+    return dbits(((2.0 * (double)B[b]) * (double)(d.hidden_dim + d.ffn_dim)) * (double)d.dtype_bytes);
+  }
+  // stage handoff hop: [intra][b]
+  if (w >= L.hop && w < L.hop + 2 * nb) {
+    const int i = w - L.hop, b = i % nb;
+    return dbits(p2p_time(d, (double)(B[b] * d.hidden_dim * d.dtype_bytes), i / nb != 0));
+  }
+  if (w >= L.batch_d && w < L.batch_d + nb) return dbits((double)B[w - L.batch_d]);
+  if (w >= L.lps_d && w < L.lps_d + np) return dbits((double)(d.num_layers / PP[w - L.lps_d]));
+  if (w >= L.ppm1_d && w < L.ppm1_d + np) return dbits((double)(PP[w - L.ppm1_d] - 1));
+  if (w >= L.tpv && w < L.tpv + nt) return (uint64_t)TP[w - L.tpv];
+  if (w >= L.epv && w < L.epv + ne) return (uint64_t)EP[w - L.epv];
+  if (w >= L.ppv && w < L.ppv + np) return (uint64_t)PP[w - L.ppv];
+  // layout-error masks per (axis, tp): bit 2k when op k under that axis is
+  // inadmissible or its sharded extent does not divide tp (layout.py:214-221)
+  if (w >= L.bad && w < L.bad + 3 * nt) {
+    const int i = w - L.bad, t = i % nt, a = i / nt;
+    uint64_t m = 0;
+    for (int op = 0; op < LS_NUM_OPS; ++op) {
+      if ((op == LS_OP_SHARED_FFN1 || op == LS_OP_SHARED_FFN2) && !d.has_shared_expert) continue;
+      bool bad = !((admits_mask(op) >> a) & 1);
+      if (!bad && a != 0 && TP[t] > 1) {
+        const int64_t ext = shard_extent(d, op, a);
+        bad = ext < 0 || ext % TP[t] != 0;
+      }
+      if (bad) m |= 1ull << (2 * op);
+    }
+    return m;
+  }
+  // over device budget: [t][e] -> bit p
+  if (w >= L.ovb && w < L.ovb + nt * ne) {
+    const int i = w - L.ovb, t = i / ne, e = i % ne;
+    uint64_t m = 0;
+    for (int p = 0; p < np; ++p)
+      if (TP[t] * EP[e] * PP[p] > d.device_budget) m |= 1ull << p;
+    return m;
+  }
+  return 0;  // padding
+}
+
+__global__ void build_tables_kernel(const ls_workload_desc d, const TabLayout L, uint64_t* out) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < L.words; w += gridDim.x * blockDim.x)
+    out[w] = table_word(d, L, w);
+}
+
+}  // namespace
+
+cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream) {
+  const int threads = 256;
+  int blocks = (L.words + threads - 1) / threads;
+  if (blocks < 1) blocks = 1;
+  build_tables_kernel<<<blocks, threads, 0, stream>>>(d, L, out);
+  return cudaGetLastError();
+}
+
+}  // namespace ls

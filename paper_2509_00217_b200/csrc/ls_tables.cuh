@@ -1,0 +1,114 @@
+// ls_tables.cuh — per-workload lookup tables of the B200 evaluator.
+//
+// The reference recomputes every operator cost and collective cost from
+// scratch for every candidate (simulator.py:163-236, layout.py:347-456).
+// Each of those quantities is a pure function of a few domain indices —
+// (op, axis, tp, batch[, ep][, attention axis]) — so a workload compiles
+// into a few thousand float64 words computed ONCE per context by
+// ls_build_tables (ls_tables.cu) with exactly the reference's expression
+// order. The evaluate kernel stages the whole table into shared memory with
+// one bulk (TMA) copy per CTA and only gathers + sums per candidate, which
+// removes ~66 IEEE divisions per full-path candidate while staying
+// bit-identical (each entry is the value the reference computes).
+//
+// All words are 8 bytes: doubles, or int64/uint64 bit patterns.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/ls_eval.h"
+
+namespace ls {
+
+// Layout states of an activation over the TP group (layout.py:34-37). The
+// code equals the producing matmul's axis: UNSHARDED->R, DIM0->P, DIM1->S.
+enum : int { ST_R = 0, ST_P = 1, ST_S = 2 };
+// Collective families: AR pays 2(n-1)/n, the rest (AG, RS, A2A) (n-1)/n
+// (simulator.py:116-119).
+enum : int { FAM_NONE = 0, FAM_AR = 1, FAM_ONCE = 2 };
+// Payload classes of TP-group collectives: tokens x features x dtype.
+enum : int { CLS_QKV = 0, CLS_H = 1, CLS_F = 2, CLS_V = 3 };
+
+// Offsets (in 8-byte words) of every table segment inside one buffer.
+struct TabLayout {
+  int nt, ne, np, nb;  // tp / ep / pp / batch domain sizes
+  int has_shared;
+  // op-time segments
+  int opt_emb, opt_qkv, opt_kv, opt_attn, opt_out, opt_router, opt_ffn1, opt_ffn2;
+  int opt_sh1, opt_sh2, opt_norm, opt_lmh;
+  // collective-time segments
+  int coll, rtf, a2a;
+  // memory segments
+  int mem_w, mem_kv, mem_ws;
+  // pipeline hop, per-index doubles
+  int hop, batch_d, lps_d, ppm1_d;
+  // integer segments
+  int tpv, epv, ppv, bad, ovb;
+  int words;  // total, padded to a multiple of 2 (16 bytes)
+};
+
+// Warp-uniform per-workload scalars, passed by value as a kernel parameter.
+struct EvalMeta {
+  int A;                              // vector length
+  int pad_;
+  uint8_t head_size[LS_MAX_HEADS];    // domain size per head
+  int8_t head_op[LS_MAX_HEADS];       // canonical op controlled by head, -1 none
+  uint32_t pinned_axes;               // 2 bits per canonical op (pins / UNSHARDED)
+  uint32_t pad2_;
+  uint64_t pp_bad;                    // bit p: num_layers % pp != 0 (simulator.py:268)
+  uint64_t ep_bad;                    // bit e: ep > num_experts or ne % ep (layout.py:371-374)
+  int64_t device_budget;
+  int64_t node_size;
+  double num_layers_d;
+  double slo_tpot;
+  double hbm_capacity;
+  int64_t code_stride[LS_MAX_HEADS];  // mixed-radix place value per head
+};
+
+__host__ __device__ inline int round2(int w) { return (w + 1) & ~1; }
+
+inline TabLayout make_layout(const ls_workload_desc& d) {
+  TabLayout L{};
+  L.nt = d.domain_len[0];
+  L.ne = d.domain_len[1];
+  L.np = d.domain_len[2];
+  L.nb = d.domain_len[3];
+  L.has_shared = d.has_shared_expert ? 1 : 0;
+  const int nt = L.nt, ne = L.ne, np = L.np, nb = L.nb;
+  int w = 0;
+  auto seg = [&](int words) {
+    int at = w;
+    w += round2(words);
+    return at;
+  };
+  L.opt_emb = seg(3 * nt * nb);
+  L.opt_qkv = seg(3 * nt * nb);
+  L.opt_kv = seg(2 * nt * nb);
+  L.opt_attn = seg(2 * nt * nb);
+  L.opt_out = seg(3 * nt * nb);
+  L.opt_router = seg(nb);
+  L.opt_ffn1 = seg(3 * nt * ne * nb);
+  L.opt_ffn2 = seg(3 * nt * ne * nb);
+  L.opt_sh1 = seg(L.has_shared ? 3 * nt * nb : 0);
+  L.opt_sh2 = seg(L.has_shared ? 3 * nt * nb : 0);
+  L.opt_norm = seg(nb);
+  L.opt_lmh = seg(3 * nt * nb);
+  L.coll = seg(4 * 2 * nt * nb);
+  L.rtf = seg(2 * nt * ne * nb);
+  L.a2a = seg(nt * ne * nb);
+  L.mem_w = seg(nt * ne * np);
+  L.mem_kv = seg(2 * nt * np * nb);
+  L.mem_ws = seg(nb);
+  L.hop = seg(2 * nb);
+  L.batch_d = seg(nb);
+  L.lps_d = seg(np);
+  L.ppm1_d = seg(np);
+  L.tpv = seg(nt);
+  L.epv = seg(ne);
+  L.ppv = seg(np);
+  L.bad = seg(3 * nt);
+  L.ovb = seg(nt * ne);
+  L.words = round2(w);
+  return L;
+}
+
+}  // namespace ls

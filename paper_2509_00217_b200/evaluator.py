@@ -1,0 +1,238 @@
+"""Batched GPU evaluator: the drop-in for the reference's per-candidate path.
+
+``Evaluator`` owns one libls_eval context (one workload on one device) and
+exposes the batched API of SURVEY.md §8(b):
+
+* ``evaluate(planes)``      — score [A, N] uint8 SoA candidates resident on the
+  GPU; every element equals ``simulate(SimRequest(decode_strategy(v)))``
+  (reference simulator.py:239-341) bit for bit.
+* ``evaluate_host(planes)`` — the same from/to host memory (pipelined copies).
+* ``reward_scan(...)``      — Eq.-1 rewards with the exclusive running best
+  of ``SearchEnv.step`` (env.py:159-164, :178-179).
+* ``topk(...)``             — elite top-k over distinct vectors
+  (EliteBuffer.offer, policy.py:86-102; build_report(by_raw), ppo.py:441-447).
+
+Tensors are torch CUDA tensors; calls are enqueued on torch's current stream
+of the evaluator's device, so they order naturally with surrounding torch work.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import EliteRec, NativeUnavailable, ResultSoA, check
+from .strategy import codes_to_vectors
+from .workload import Workload
+
+__all__ = ["Evaluator", "BatchResult", "Elite", "FIELDS", "REASON_NAMES", "NativeUnavailable"]
+
+FIELDS = ("throughput", "tpot_s", "memory_bytes", "compute_s", "comm_s", "pipeline_s")
+REASON_NAMES = {0: "none", 1: "over_device_budget", 2: "layout_error", 3: "oom", 4: "slo_violation",
+                255: "decode_error"}
+_REC_BYTES = ctypes.sizeof(EliteRec)
+
+
+@dataclass
+class BatchResult:
+    """Per-candidate verdicts (struct of arrays); absent fields are None."""
+
+    reason: torch.Tensor
+    throughput: torch.Tensor | None = None
+    tpot_s: torch.Tensor | None = None
+    memory_bytes: torch.Tensor | None = None
+    compute_s: torch.Tensor | None = None
+    comm_s: torch.Tensor | None = None
+    pipeline_s: torch.Tensor | None = None
+
+    @property
+    def valid(self) -> torch.Tensor:
+        return self.reason == 0
+
+    def numpy(self) -> dict:
+        out = {"reason": self.reason.cpu().numpy()}
+        for f in FIELDS:
+            t = getattr(self, f)
+            if t is not None:
+                out[f] = t.cpu().numpy()
+        return out
+
+
+@dataclass(frozen=True)
+class Elite:
+    """One top-k record: the vector, its key (raw or reward), raw, global index."""
+
+    vector: tuple[int, ...]
+    key: float
+    raw: float
+    index: int
+
+
+def _cuda_device(device) -> torch.device:
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    if isinstance(device, int):
+        return torch.device("cuda", device)
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"the evaluator runs on CUDA devices only, got {dev}")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class Evaluator:
+    """One workload compiled onto one CUDA device."""
+
+    def __init__(self, workload: Workload, device=None):
+        self._lib = _native.lib(require_gpu=True)
+        self.workload = workload
+        self.space = workload.space
+        self.device = _cuda_device(device)
+        self.desc = workload.desc()
+        handle = ctypes.c_void_p()
+        check(self._lib.ls_ctx_create(ctypes.byref(self.desc), self.device.index, ctypes.byref(handle)))
+        self._ctx = handle
+        self.vector_length = self.desc.vector_length
+        self.head_sizes = tuple(int(self.desc.domain_len[h]) if h < 4 else 3 for h in range(self.vector_length))
+        self.space_size = int(self._lib.ls_space_size(self._ctx))
+
+    # -- lifecycle ----------------------------------------------------------
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            self._lib.ls_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _check_planes(self, planes: torch.Tensor):
+        if planes.dtype != torch.uint8 or planes.dim() != 2:
+            raise TypeError("planes must be a 2-D uint8 tensor [A, N]")
+        if planes.shape[0] != self.vector_length:
+            raise ValueError(f"planes have {planes.shape[0]} heads, the action space has {self.vector_length}")
+        if planes.shape[1] > 0 and planes.stride(1) != 1:
+            raise ValueError("planes must be contiguous along candidates (stride(1) == 1)")
+        n = planes.shape[1]
+        stride = planes.stride(0) if planes.shape[0] > 1 else max(n, 1)
+        return n, max(stride, n)
+
+    # -- evaluation ---------------------------------------------------------
+
+    def evaluate(self, planes: torch.Tensor, fields=("throughput",), out: BatchResult | None = None) -> BatchResult:
+        """Score candidates resident on the device. ``fields``: subset of FIELDS or "all"."""
+        if planes.device != self.device:
+            raise ValueError(f"planes live on {planes.device}, evaluator on {self.device}")
+        n, stride = self._check_planes(planes)
+        if fields == "all":
+            fields = FIELDS
+        if out is None:
+            out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=self.device))
+            for f in fields:
+                setattr(out, f, torch.empty(n, dtype=torch.float64, device=self.device))
+        soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS))
+        check(self._lib.ls_evaluate(self._ctx, ctypes.c_void_p(planes.data_ptr()), n, stride, ctypes.byref(soa),
+                                    self._stream()))
+        return out
+
+    def evaluate_host(self, planes: np.ndarray | torch.Tensor, fields=("throughput",)) -> dict:
+        """Score host-resident [A, N] planes; results come back as numpy arrays.
+
+        Copies are pipelined with the kernels inside the library; pass pinned
+        memory (``pinned_planes``) for full PCIe bandwidth.
+        """
+        if isinstance(planes, torch.Tensor):
+            if planes.is_cuda:
+                raise ValueError("evaluate_host takes host memory; use evaluate() for device tensors")
+            arr = planes.numpy()
+        else:
+            arr = np.asarray(planes)
+        if arr.dtype != np.uint8 or arr.ndim != 2 or arr.shape[0] != self.vector_length:
+            raise ValueError(f"expected uint8 planes of shape [{self.vector_length}, N]")
+        if arr.shape[1] and arr.strides[1] != 1:
+            arr = np.ascontiguousarray(arr)
+        n = arr.shape[1]
+        stride = arr.strides[0] if arr.shape[0] > 1 else max(n, 1)
+        if fields == "all":
+            fields = FIELDS
+        out = {"reason": np.empty(n, dtype=np.uint8)}
+        for f in fields:
+            out[f] = np.empty(n, dtype=np.float64)
+        soa = ResultSoA(ctypes.c_void_p(out["reason"].ctypes.data),
+                        *(ctypes.c_void_p(out[f].ctypes.data) if f in out else None for f in FIELDS))
+        check(self._lib.ls_evaluate_host(self._ctx, ctypes.c_void_p(arr.ctypes.data), n, max(stride, n),
+                                         ctypes.byref(soa)))
+        return out
+
+    # -- reward shaping + elites -------------------------------------------
+
+    def reward_scan(self, reason: torch.Tensor, throughput: torch.Tensor, b0: float = 0.0, alpha: float = 1.0,
+                    beta: float = 1.0, penalty: float = -10.0):
+        """Per-candidate Eq.-1 rewards and the running best after the batch."""
+        n = reason.shape[0]
+        reward = torch.empty(n, dtype=torch.float64, device=self.device)
+        best = torch.empty(1, dtype=torch.float64, device=self.device)
+        scratch = torch.empty(int(self._lib.ls_scan_scratch_bytes(n)), dtype=torch.uint8, device=self.device)
+        check(self._lib.ls_reward_scan(self._ctx, _ptr(reason), _ptr(throughput), n, float(b0), float(alpha),
+                                       float(beta), float(penalty), _ptr(reward), _ptr(best), _ptr(scratch),
+                                       self._stream()))
+        return reward, best
+
+    def topk_records(self, planes: torch.Tensor, reason: torch.Tensor, throughput: torch.Tensor,
+                     key: torch.Tensor | None = None, k: int = 3, index_base: int = 0):
+        """Device top-k: returns (records uint8 tensor [k, 32], count int32 tensor [1])."""
+        n, stride = self._check_planes(planes)
+        if key is None:
+            key = throughput
+        recs = torch.zeros((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        scratch = torch.empty(int(self._lib.ls_topk_scratch_bytes(n, k)), dtype=torch.uint8, device=self.device)
+        check(self._lib.ls_topk(self._ctx, _ptr(planes), stride, _ptr(reason), _ptr(throughput), _ptr(key), n, int(k),
+                                int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), self._stream()))
+        return recs, count
+
+    def topk(self, planes, reason, throughput, key=None, k: int = 3, index_base: int = 0) -> list[Elite]:
+        """Top-k valid candidates over distinct vectors, best first."""
+        recs, count = self.topk_records(planes, reason, throughput, key, k, index_base)
+        return self.decode_records(recs, count)
+
+    def decode_records(self, recs: torch.Tensor, count: torch.Tensor) -> list[Elite]:
+        n = int(count.item())
+        raw = recs[:n].cpu().numpy().view(np.dtype([("key", "<f8"), ("raw", "<f8"), ("index", "<i8"), ("code", "<u8")]))
+        raw = raw.reshape(-1)
+        vecs = codes_to_vectors(raw["code"], self.space) if n else np.zeros((0, self.vector_length), np.int64)
+        return [Elite(tuple(int(x) for x in vecs[i]), float(raw["key"][i]), float(raw["raw"][i]), int(raw["index"][i]))
+                for i in range(n)]
+
+    def merge_records(self, recs: torch.Tensor, counts: torch.Tensor, k_in: int, k: int):
+        """Merge m stacked record lists ([m*k_in, 32] bytes, counts [m]) into one top-k."""
+        m = counts.shape[0]
+        out = torch.zeros((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        check(self._lib.ls_topk_merge(_ptr(recs), _ptr(counts), m, int(k_in), int(k), _ptr(out), _ptr(count),
+                                      self._stream()))
+        return out, count
+
+
+def pinned_planes(a: int, n: int) -> torch.Tensor:
+    """Page-locked [A, N] uint8 host buffer for evaluate_host."""
+    return torch.empty((a, n), dtype=torch.uint8).pin_memory()
