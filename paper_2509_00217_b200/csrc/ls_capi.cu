@@ -44,7 +44,6 @@ struct DeviceGuard {
 };
 
 constexpr int kHostChunk = 1 << 22;  // candidates per pipelined host chunk
-constexpr size_t kSmemTableLimit = 200 * 1024;
 
 }  // namespace
 
@@ -56,8 +55,8 @@ struct ls_ctx {
   int device = 0;
   int num_sms = 148;
   uint64_t* d_tab = nullptr;
-  bool smem_tables = false;
-  int64_t blocks_vec4 = 0, blocks_generic = 0;
+  bool smem_gate = false;
+  int64_t blocks_tma = 0, blocks_generic = 0;
   uint64_t space_size = 0;
   // host pipeline
   std::mutex host_mu;
@@ -203,13 +202,15 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
     delete c;
     return cuda_fail(e, "build_tables");
   }
-  c->smem_tables = tab_bytes <= kSmemTableLimit && tab_bytes <= (size_t)prop.sharedMemPerBlockOptin;
-  const size_t smem = c->smem_tables ? tab_bytes : 0;
-  if (c->smem_tables) prepare_eval_kernels(smem);
-  const int occ4 = std::max(1, occupancy_blocks_per_sm(true, c->smem_tables, smem));
-  const int occg = std::max(1, occupancy_blocks_per_sm(false, c->smem_tables, smem));
-  c->blocks_vec4 = (int64_t)c->num_sms * occ4;
-  c->blocks_generic = (int64_t)c->num_sms * occg;
+  // gate tables go to shared memory when the whole TMA footprint still
+  // allows two CTAs per SM; otherwise they are read through L1.
+  const size_t two_cta = (size_t)prop.sharedMemPerMultiprocessor / 2 - 2048;
+  c->smem_gate = tma_smem_bytes(c->L, c->desc.vector_length, true) <= two_cta;
+  if (c->desc.vector_length <= 16) {
+    prepare_eval_kernels(c->L, c->desc.vector_length, c->smem_gate);
+    c->blocks_tma = (int64_t)c->num_sms * std::max(1, tma_blocks_per_sm(c->L, c->desc.vector_length, c->smem_gate));
+  }
+  c->blocks_generic = (int64_t)c->num_sms * std::max(1, generic_blocks_per_sm());
   if ((e = cudaGetLastError()) != cudaSuccess) {
     cudaFree(c->d_tab);
     delete c;
@@ -235,13 +236,13 @@ int ls_ctx_destroy(ls_ctx* c) {
 
 uint64_t ls_space_size(const ls_ctx* c) { return c ? c->space_size : 0; }
 
-static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
 static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stride, const ls_result_soa* out,
                        cudaStream_t s) {
-  if (n < 0 || !out || !out->reason || (n > 0 && !planes)) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate arguments");
-  if (stride < n) return fail(LS_ERR_INVALID_ARGUMENT, "plane_stride must be >= n");
+  if (n < 0 || !out) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate arguments");
   if (n == 0) return LS_OK;
+  if (!out->reason || !planes) return fail(LS_ERR_INVALID_ARGUMENT, "null planes or reason buffer");
+  if (stride < n) return fail(LS_ERR_INVALID_ARGUMENT, "plane_stride must be >= n");
   EvalArgs a;
   a.planes = planes;
   a.n = n;
@@ -253,13 +254,11 @@ static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stri
   a.comp = out->compute_s;
   a.comm = out->comm_s;
   a.pipe = out->pipeline_s;
-  bool vec4 = c->M.A <= 16 && aligned(planes, 4) && stride % 4 == 0 && aligned(a.reason, 4);
-  const double* fs[6] = {a.thr, a.tpot, a.mem, a.comp, a.comm, a.pipe};
-  for (const double* f : fs) vec4 = vec4 && aligned(f, 16);
   LaunchPlan lp;
-  lp.vec4 = vec4;
-  lp.max_blocks = vec4 ? c->blocks_vec4 : c->blocks_generic;
-  cudaError_t e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->smem_tables, c->d_tab, c->L, c->M, a, s);
+  lp.tma = tma_eligible(a, c->M.A) && c->blocks_tma > 0;
+  lp.smem_gate = c->smem_gate;
+  lp.max_blocks = lp.tma ? c->blocks_tma : c->blocks_generic;
+  cudaError_t e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, s);
   if (e != cudaSuccess) return cuda_fail(e, "evaluate launch");
   return LS_OK;
 }
@@ -275,9 +274,10 @@ int ls_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_strid
 int ls_evaluate_host(ls_ctx* c, const uint8_t* host_planes, int64_t n, int64_t plane_stride,
                      const ls_result_soa* host_out) {
   g_err.clear();
-  if (!c || !host_out || !host_out->reason || (n > 0 && !host_planes) || n < 0 || plane_stride < n)
-    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host arguments");
+  if (!c || !host_out || n < 0) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host arguments");
   if (n == 0) return LS_OK;
+  if (!host_out->reason || !host_planes || plane_stride < n)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host arguments");
   std::lock_guard<std::mutex> lock(c->host_mu);
   DeviceGuard g(c->device);
   const int A = c->desc.vector_length;

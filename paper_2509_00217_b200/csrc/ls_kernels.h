@@ -17,16 +17,20 @@ struct EvalArgs {
 };
 
 struct LaunchPlan {
-  bool vec4;
+  bool tma;        // TMA-ring two-pass kernel (aligned planes, A <= 16)
+  bool smem_gate;  // gate tables staged into shared memory
   int64_t max_blocks;
 };
 
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
 
-cudaError_t prepare_eval_kernels(size_t smem_bytes);
-int occupancy_blocks_per_sm(bool vec4, bool smem_tables, size_t smem);
-cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, bool smem_tables, const uint64_t* tab,
-                            const TabLayout& L, const EvalMeta& M, const EvalArgs& a, cudaStream_t s);
+bool tma_eligible(const EvalArgs& a, int A);
+cudaError_t prepare_eval_kernels(const TabLayout& L, int A, bool smem_gate);
+int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate);
+int generic_blocks_per_sm();
+size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate);
+cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
+                            const EvalMeta& M, const EvalArgs& a, cudaStream_t s);
 
 // Reward scan (ls_select.cu)
 size_t scan_scratch_bytes(int64_t n);

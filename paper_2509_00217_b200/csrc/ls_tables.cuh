@@ -6,10 +6,14 @@
 // (op, axis, tp, batch[, ep][, attention axis]) — so a workload compiles
 // into a few thousand float64 words computed ONCE per context by
 // ls_build_tables (ls_tables.cu) with exactly the reference's expression
-// order. The evaluate kernel stages the whole table into shared memory with
-// one bulk (TMA) copy per CTA and only gathers + sums per candidate, which
-// removes ~66 IEEE divisions per full-path candidate while staying
-// bit-identical (each entry is the value the reference computes).
+// order. Kernels then only gather and sum per candidate, which removes ~66
+// IEEE divisions per full-path candidate while staying bit-identical (each
+// entry IS the value the reference computes).
+//
+// The buffer starts with the GATE segment (everything the cheap first pass
+// needs: budget / layout masks and the memory terms); the evaluate kernel
+// bulk-copies just that prefix into shared memory. The op/collective time
+// segments behind it are read through L1 by the compacted fp64 pass.
 //
 // All words are 8 bytes: doubles, or int64/uint64 bit patterns.
 #pragma once
@@ -32,18 +36,19 @@ enum : int { CLS_QKV = 0, CLS_H = 1, CLS_F = 2, CLS_V = 3 };
 struct TabLayout {
   int nt, ne, np, nb;  // tp / ep / pp / batch domain sizes
   int has_shared;
+  // gate segment (staged to shared memory)
+  int ovb, bad, mem_w, mem_kv, mem_ws;
+  int gate_words;  // words of the gate segment, even
   // op-time segments
   int opt_emb, opt_qkv, opt_kv, opt_attn, opt_out, opt_router, opt_ffn1, opt_ffn2;
   int opt_sh1, opt_sh2, opt_norm, opt_lmh;
   // collective-time segments
   int coll, rtf, a2a;
-  // memory segments
-  int mem_w, mem_kv, mem_ws;
   // pipeline hop, per-index doubles
   int hop, batch_d, lps_d, ppm1_d;
   // integer segments
-  int tpv, epv, ppv, bad, ovb;
-  int words;  // total, padded to a multiple of 2 (16 bytes)
+  int tpv, epv, ppv;
+  int words;  // total, even (16-byte multiple)
 };
 
 // Warp-uniform per-workload scalars, passed by value as a kernel parameter.
@@ -80,6 +85,12 @@ inline TabLayout make_layout(const ls_workload_desc& d) {
     w += round2(words);
     return at;
   };
+  L.ovb = seg(nt * ne);
+  L.bad = seg(3 * nt);
+  L.mem_w = seg(nt * ne * np);
+  L.mem_kv = seg(2 * nt * np * nb);
+  L.mem_ws = seg(nb);
+  L.gate_words = w;
   L.opt_emb = seg(3 * nt * nb);
   L.opt_qkv = seg(3 * nt * nb);
   L.opt_kv = seg(2 * nt * nb);
@@ -95,9 +106,6 @@ inline TabLayout make_layout(const ls_workload_desc& d) {
   L.coll = seg(4 * 2 * nt * nb);
   L.rtf = seg(2 * nt * ne * nb);
   L.a2a = seg(nt * ne * nb);
-  L.mem_w = seg(nt * ne * np);
-  L.mem_kv = seg(2 * nt * np * nb);
-  L.mem_ws = seg(nb);
   L.hop = seg(2 * nb);
   L.batch_d = seg(nb);
   L.lps_d = seg(np);
@@ -105,8 +113,6 @@ inline TabLayout make_layout(const ls_workload_desc& d) {
   L.tpv = seg(nt);
   L.epv = seg(ne);
   L.ppv = seg(np);
-  L.bad = seg(3 * nt);
-  L.ovb = seg(nt * ne);
   L.words = round2(w);
   return L;
 }

@@ -130,7 +130,7 @@ class Evaluator:
             raise TypeError("planes must be a 2-D uint8 tensor [A, N]")
         if planes.shape[0] != self.vector_length:
             raise ValueError(f"planes have {planes.shape[0]} heads, the action space has {self.vector_length}")
-        if planes.shape[1] > 0 and planes.stride(1) != 1:
+        if planes.shape[1] > 1 and planes.stride(1) != 1:
             raise ValueError("planes must be contiguous along candidates (stride(1) == 1)")
         n = planes.shape[1]
         stride = planes.stride(0) if planes.shape[0] > 1 else max(n, 1)
@@ -154,7 +154,7 @@ class Evaluator:
                                     self._stream()))
         return out
 
-    def evaluate_host(self, planes: np.ndarray | torch.Tensor, fields=("throughput",)) -> dict:
+    def evaluate_host(self, planes: np.ndarray | torch.Tensor, fields=("throughput",), out: dict | None = None) -> dict:
         """Score host-resident [A, N] planes; results come back as numpy arrays.
 
         Copies are pipelined with the kernels inside the library; pass pinned
@@ -174,9 +174,12 @@ class Evaluator:
         stride = arr.strides[0] if arr.shape[0] > 1 else max(n, 1)
         if fields == "all":
             fields = FIELDS
-        out = {"reason": np.empty(n, dtype=np.uint8)}
-        for f in fields:
-            out[f] = np.empty(n, dtype=np.float64)
+        if out is None:
+            out = {"reason": np.empty(n, dtype=np.uint8)}
+            for f in fields:
+                out[f] = np.empty(n, dtype=np.float64)
+        elif any(len(v) < n for v in out.values()):
+            raise ValueError("out arrays are shorter than the batch")
         soa = ResultSoA(ctypes.c_void_p(out["reason"].ctypes.data),
                         *(ctypes.c_void_p(out[f].ctypes.data) if f in out else None for f in FIELDS))
         check(self._lib.ls_evaluate_host(self._ctx, ctypes.c_void_p(arr.ctypes.data), n, max(stride, n),
@@ -236,3 +239,13 @@ class Evaluator:
 def pinned_planes(a: int, n: int) -> torch.Tensor:
     """Page-locked [A, N] uint8 host buffer for evaluate_host."""
     return torch.empty((a, n), dtype=torch.uint8).pin_memory()
+
+
+def pinned_results(n: int, fields=("throughput",)) -> dict:
+    """Page-locked numpy result arrays for evaluate_host(out=...)."""
+    if fields == "all":
+        fields = FIELDS
+    out = {"reason": torch.empty(n, dtype=torch.uint8).pin_memory().numpy()}
+    for f in fields:
+        out[f] = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    return out
