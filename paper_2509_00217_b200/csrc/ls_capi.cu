@@ -131,22 +131,19 @@ void build_meta(ls_ctx* c) {
   EvalMeta& M = c->M;
   std::memset(&M, 0, sizeof(M));
   M.A = d.vector_length;
+  int slot[LS_MAX_HEADS];
+  head_slots(d, slot);
   for (int h = 0; h < LS_MAX_HEADS; ++h) {
     M.head_size[h] = h < 4 ? (uint8_t)d.domain_len[h] : 3;
-    M.head_op[h] = -1;
+    M.head_slot[h] = (int8_t)slot[h];
   }
-  M.pinned_axes = 0;
   for (int k = 0; k < LS_NUM_OPS; ++k) {
-    if (d.op_head[k] >= 0) M.head_op[d.op_head[k]] = (int8_t)k;
-    else M.pinned_axes |= (uint32_t)d.op_pinned[k] << (2 * k);
+    const int h = d.op_head[k];
+    M.op_src[k] = (int8_t)(h >= 0 ? 2 * slot[h] : -1);
+    M.op_pin[k] = (int8_t)(h >= 0 ? 0 : d.op_pinned[k]);
   }
-  for (int p = 0; p < d.domain_len[2]; ++p)
-    if (d.num_layers % d.domain[2][p]) M.pp_bad |= 1ull << p;
-  for (int e = 0; e < d.domain_len[1]; ++e) {
-    const int64_t ep = d.domain[1][e];
-    if (ep > d.num_experts || d.num_experts % ep) M.ep_bad |= 1ull << e;
-  }
-  M.device_budget = d.device_budget;
+  M.attn_src = M.op_src[LS_OP_ATTN_CORE];
+  M.attn_pin = M.op_pin[LS_OP_ATTN_CORE];
   M.node_size = d.node_size;
   M.num_layers_d = (double)d.num_layers;
   M.slo_tpot = d.slo_tpot;

@@ -1,18 +1,21 @@
 // ls_evaluate.cu — the batched strategy-evaluation kernels.
 //
-// eval_tma_kernel (the hot path; 16-byte aligned SoA planes, A <= 16):
-//   persistent CTAs walk 1024-candidate tiles. Per CTA:
-//   * one thread bulk-copies (TMA, cp.async.bulk + mbarrier) the workload's
-//     gate tables into shared memory, then keeps a 3-stage ring of candidate
-//     tiles in flight (A plane slices of 1 KB per tile), so HBM latency is
-//     hidden by the copy engine instead of by registers;
-//   * pass A: each thread pulls its 4 candidates (one 32-bit shared load per
-//     head plane), decodes them and runs the integer/bitmask gates and the
-//     memory model (gate()); the ~98% of candidates a uniform batch gates out
-//     are finished here with coalesced 32-bit / 128-bit stores;
-//   * survivors (fit in memory) are compacted into a shared-memory queue with
-//     warp-aggregated atomics; when half full, all 256 threads drain it
-//     through the fp64 cost model (full_path()) — dense warps, no divergence
+// eval_ws_kernel — the hot path (16-byte aligned SoA planes, A <= 16).
+// Persistent, warp-specialized CTAs (1 producer warp + 8 consumer warps):
+//   * the producer warp's elected lane bulk-copies (TMA, cp.async.bulk) the
+//     workload's gate tables into shared memory once, then keeps a 4-stage
+//     ring of 1024-candidate tiles in flight (one 1 KB slice per head plane
+//     per tile), synchronised only through full/empty mbarriers — no CTA-wide
+//     barrier in the steady state;
+//   * each consumer warp owns 128 candidates of a stage (4 per lane, one
+//     32-bit shared load per head plane), releases the stage, decodes the 4
+//     candidates with SWAR byte arithmetic (range checks and the packed axis
+//     word for all 4 at once), and runs gate(): budget and layout bitmasks
+//     and the memory model. The ~98% of a uniform batch that is gated out is
+//     finished here with coalesced 32-bit / 128-bit stores;
+//   * survivors go to the warp's own shared-memory queue (ballot + popc);
+//     every time it holds a full warp's worth, the warp runs the fp64 cost
+//     model (full_path()) on 32 survivors at once — dense, no divergence
 //     between cheap and expensive candidates.
 // eval_generic_kernel covers everything else (any alignment, A <= 64), one
 // candidate per thread.
@@ -25,24 +28,27 @@ namespace ls {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kTile = 4 * kThreads;  // candidates per tile
-constexpr int kStages = 3;
-constexpr int kQueue = 2048;  // survivor queue entries per CTA
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = 32 * (kConsumerWarps + 1);
+constexpr int kWarpCands = 128;
+constexpr int kTile = kConsumerWarps * kWarpCands;  // candidates per stage
+constexpr int kStages = 4;
+constexpr int kWarpQueue = 160;  // < 32 left over + 128 from one tile
+constexpr int kGenericThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
@@ -53,7 +59,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
-
 // 1-D bulk async copy global -> shared (TMA engine), completing on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -62,53 +67,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// Decode byte j of the packed plane words: head range check + domain
-// indices + 2-bit axis word in canonical op order.
-__device__ __forceinline__ bool decode_quad(const uint32_t* w, int j, const EvalMeta& M, Decoded& c) {
-  uint32_t bad = 0, X = M.pinned_axes;
-  const int sh = 8 * j;
-  const uint32_t b0 = (w[0] >> sh) & 0xffu, b1 = (w[1] >> sh) & 0xffu, b2 = (w[2] >> sh) & 0xffu,
-                 b3 = (w[3] >> sh) & 0xffu;
-  bad |= (b0 >= M.head_size[0]) | (b1 >= M.head_size[1]) | (b2 >= M.head_size[2]) | (b3 >= M.head_size[3]);
-#pragma unroll
-  for (int h = 4; h < 16; ++h) {
-    if (h < M.A) {
-      const uint32_t byte = (w[h] >> sh) & 0xffu;
-      bad |= byte > 2u;
-      const int op = M.head_op[h];
-      if (op >= 0) X = (X & ~(3u << (2 * op))) | ((byte & 3u) << (2 * op));
-    }
-  }
-  c.t = (int)b0;
-  c.e = (int)b1;
-  c.p = (int)b2;
-  c.b = (int)b3;
-  c.X = X;
-  return !bad;
-}
-
 __device__ __forceinline__ uint64_t pack_key(int64_t idx, const Decoded& c) {
   return (uint64_t)idx | ((uint64_t)c.t << 40) | ((uint64_t)c.e << 46) | ((uint64_t)c.p << 52) |
          ((uint64_t)c.b << 58);
 }
-
-__device__ __forceinline__ void unpack_key(uint64_t k, uint32_t X, int64_t& idx, Decoded& c) {
+__device__ __forceinline__ void unpack_key(uint64_t k, uint32_t Y, int64_t& idx, Decoded& c) {
   idx = (int64_t)(k & ((1ull << 40) - 1));
   c.t = (int)((k >> 40) & 63);
   c.e = (int)((k >> 46) & 63);
   c.p = (int)((k >> 52) & 63);
   c.b = (int)((k >> 58) & 63);
-  c.X = X;
+  c.Y = Y;
 }
 
 __device__ __forceinline__ void st2(double* base, int64_t i, double x, double y) {
   *reinterpret_cast<double2*>(base + i) = make_double2(x, y);
 }
 
-template <bool NEU, bool FULL>
-__device__ __forceinline__ void write_full(const EvalArgs& a, int64_t idx, const Verdict& v) {
+template <bool FULL>
+__device__ __forceinline__ void write_verdict(const EvalArgs& a, int64_t idx, const Verdict& v) {
   a.reason[idx] = (uint8_t)v.reason;
   if (a.thr) a.thr[idx] = v.thr;
   if (FULL) {
@@ -119,91 +96,129 @@ __device__ __forceinline__ void write_full(const EvalArgs& a, int64_t idx, const
   }
 }
 
+// SWAR decode of 4 candidates packed byte-wise in w[h] (candidate j in byte
+// j). Returns per-byte "bad" flags (head out of range, strategy.py:247-254)
+// and q[3]: for axis heads 4..15, 2-bit fields four heads per byte.
+__device__ __forceinline__ uint32_t swar_decode(const uint32_t* w, const EvalMeta& M, uint32_t* q) {
+  uint32_t badb = 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const uint32_t s4 = (uint32_t)M.head_size[h] * 0x01010101u;
+    const uint32_t r = (w[h] | 0x80808080u) - s4;  // per byte: high bit set iff (x & 0x7f) >= size
+    badb |= (r | w[h]) & 0x80808080u;
+  }
+  uint32_t orv = 0, three = 0;
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    const uint32_t a = w[4 + 4 * g], b = w[5 + 4 * g], c = w[6 + 4 * g], d = w[7 + 4 * g];
+    orv |= a | b | c | d;
+    const uint32_t m = 0x03030303u;
+    const uint32_t qq = (a & m) | ((b & m) << 2) | ((c & m) << 4) | ((d & m) << 6);
+    three |= qq & (qq >> 1) & 0x55555555u;  // a field holding 3
+    q[g] = qq;
+  }
+  return badb | (orv & 0xfcfcfcfcu) | three;
+}
+
+__device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, int j, Decoded& c) {
+  const int sh = 8 * j;
+  c.t = (int)((w[0] >> sh) & 0xffu);
+  c.e = (int)((w[1] >> sh) & 0xffu);
+  c.p = (int)((w[2] >> sh) & 0xffu);
+  c.b = (int)((w[3] >> sh) & 0xffu);
+  c.Y = ((q[0] >> sh) & 0xffu) | (((q[1] >> sh) & 0xffu) << 8) | (((q[2] >> sh) & 0xffu) << 16);
+}
+
 template <bool NEU, bool FULL, bool SMEM_GATE>
 __global__ void __launch_bounds__(kThreads, 2)
-    eval_tma_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
-                    const int64_t ntiles) {
+    eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
+                   const int64_t ntiles) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
   __shared__ __align__(8) uint64_t gate_bar;
-  __shared__ int qcount;
   const int A = M.A;
   const uint32_t stage_bytes = (uint32_t)A * kTile;
   uint8_t* ring = smem;
   uint64_t* G = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
-  uint64_t* qkey = SMEM_GATE ? G + L.gate_words : G;
-  uint32_t* qx = reinterpret_cast<uint32_t*>(qkey + kQueue);
+  uint64_t* qkey_all = SMEM_GATE ? G + L.gate_words : G;
+  uint32_t* qy_all = reinterpret_cast<uint32_t*>(qkey_all + kConsumerWarps * kWarpQueue);
   const uint64_t* Gt = SMEM_GATE ? G : gtab;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  auto issue_tile = [&](int stage, int64_t tile) {
-    uint64_t* bar = &full_bar[stage];
-    mbar_expect_tx(bar, stage_bytes);
-    const uint8_t* src = a.planes + tile * kTile;
-    uint8_t* dst = ring + stage * stage_bytes;
-    for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, bar);
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
     mbar_init(&gate_bar, 1);
-    qcount = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    fence_proxy_async();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0) {
-    if (SMEM_GATE) {
-      mbar_expect_tx(&gate_bar, (uint32_t)L.gate_words * 8u);
-      bulk_g2s(G, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
+
+  if (warp == kConsumerWarps) {  // ---------------- producer warp
+    if (lane == 0) {
+      if (SMEM_GATE) {
+        mbar_expect_tx(&gate_bar, (uint32_t)L.gate_words * 8u);
+        bulk_g2s(G, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
+      }
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i % kStages, k = i / kStages;
+        if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
+        mbar_expect_tx(&full_bar[s], stage_bytes);
+        const uint8_t* src = a.planes + tile * kTile;
+        uint8_t* dst = ring + s * stage_bytes;
+        for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
+      }
     }
-    for (int s = 0; s < kStages; ++s) {
-      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
-      if (tile < ntiles) issue_tile(s, tile);
-    }
+    return;
   }
+
+  // ---------------- consumer warps
+  uint64_t* qkey = qkey_all + warp * kWarpQueue;
+  uint32_t* qy = qy_all + warp * kWarpQueue;
+  int qcount = 0;  // warp-uniform
   if (SMEM_GATE) mbar_wait(&gate_bar, 0);
 
-  // Drain the survivor queue through the fp64 path (all threads).
-  auto drain = [&]() {
-    const int qc = qcount;
-    for (int q = tid; q < qc; q += kThreads) {
+  // fp64 pass over the 32 newest queue entries (or the first n < 32 at the end)
+  auto drain = [&](int n) {
+    __syncwarp();
+    if (lane < n) {
+      const int pos = qcount - n + lane;
       int64_t idx;
       Decoded c;
-      unpack_key(qkey[q], qx[q], idx, c);
+      unpack_key(qkey[pos], qy[pos], idx, c);
       Verdict v;
       full_path<NEU>(gtab, L, M, c, v);
-      write_full<NEU, FULL>(a, idx, v);
+      write_verdict<FULL>(a, idx, v);
     }
-    __syncthreads();
-    if (tid == 0) qcount = 0;
-    __syncthreads();
+    qcount -= n;
+    __syncwarp();
   };
 
-  // Pass A over 4 consecutive candidates starting at `base` (count valid).
+  // gate pass over the 4 candidates of this lane starting at `base`
   auto pass_a = [&](const uint32_t* w, int64_t base, int count) {
+    uint32_t q[3];
+    const uint32_t badb = swar_decode(w, M, q);
     uint32_t r4 = 0;
     double m[4];
-#pragma unroll 1
+#pragma unroll
     for (int j = 0; j < 4; ++j) {
       Decoded c;
-      const bool ok = decode_quad(w, j, M, c);
+      extract(w, q, j, c);
       double mem = 0.0;
       uint32_t reason = LS_REASON_DECODE_ERROR;
-      if (ok) reason = gate(Gt, L, M, c, mem);
-      const bool surv = j < count && ok && reason == LS_REASON_NONE;
+      if (((badb >> (8 * j)) & 0xffu) == 0) reason = gate(Gt, L, M, c, mem);
+      const bool surv = j < count && reason == LS_REASON_NONE;
       const unsigned mask = __ballot_sync(0xffffffffu, surv);
-      if (mask) {
-        const int leader = __ffs(mask) - 1;
-        int qb = 0;
-        if (lane == leader) qb = atomicAdd(&qcount, __popc(mask));
-        qb = __shfl_sync(0xffffffffu, qb, leader);
-        if (surv) {
-          const int pos = qb + __popc(mask & ((1u << lane) - 1u));
-          qkey[pos] = pack_key(base + j, c);
-          qx[pos] = c.X;
-        }
+      if (surv) {
+        const int pos = qcount + __popc(mask & ((1u << lane) - 1u));
+        qkey[pos] = pack_key(base + j, c);
+        qy[pos] = c.Y;
       }
+      qcount += __popc(mask);
       r4 |= reason << (8 * j);
       m[j] = mem;
     }
@@ -239,58 +254,46 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
+    while (qcount >= 32) drain(32);
   };
 
+  const int lane_off = warp * kWarpCands + 4 * lane;
   int i = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
     const int s = i % kStages;
     mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
     uint32_t w[16];
-    const uint8_t* st = ring + s * stage_bytes + 4 * tid;
+    const uint8_t* st = ring + s * stage_bytes + lane_off;
 #pragma unroll
     for (int h = 0; h < 16; ++h) w[h] = h < A ? *reinterpret_cast<const uint32_t*>(st + h * kTile) : 0u;
-    __syncthreads();  // stage s fully pulled into registers: refill it
-    if (tid == 0) {
-      const int64_t next = tile + (int64_t)kStages * gridDim.x;
-      if (next < ntiles) {
-        fence_proxy_async();
-        issue_tile(s, next);
-      }
-    }
-    pass_a(w, tile * kTile + 4 * tid, 4);
-    __syncthreads();
-    if (qcount >= kQueue / 2) drain();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+    pass_a(w, tile * kTile + lane_off, 4);
   }
   // ragged tail (< one tile): the CTA that would own the next tile
   const int64_t tail0 = ntiles * kTile;
   if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
-    const int64_t base = tail0 + 4 * tid;
-    int count = 0;
+    const int64_t base = tail0 + lane_off;
+    const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
     uint32_t w[16];
-    if (base < a.n) {
-      count = a.n - base < 4 ? (int)(a.n - base) : 4;
 #pragma unroll
-      for (int h = 0; h < 16; ++h) {
-        w[h] = 0;
-        if (h < A)
-          for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < 16; ++h) w[h] = 0;
+    for (int h = 0; h < 16; ++h) {
+      w[h] = 0;
+      if (h < A)
+        for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
     }
     pass_a(w, base, count);
-    __syncthreads();
   }
-  if (qcount > 0) drain();
+  if (qcount > 0) drain(qcount);
 }
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
 template <bool NEU>
-__global__ void __launch_bounds__(kThreads) eval_generic_kernel(const uint64_t* __restrict__ gtab, const TabLayout L,
-                                                                const EvalMeta M, const EvalArgs a) {
+__global__ void __launch_bounds__(kGenericThreads) eval_generic_kernel(const uint64_t* __restrict__ gtab,
+                                                                       const TabLayout L, const EvalMeta M,
+                                                                       const EvalArgs a) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t bad = 0, X = M.pinned_axes;
+    uint32_t bad = 0, Y = 0;
     int idx[4] = {0, 0, 0, 0};
     for (int h = 0; h < M.A; ++h) {
       const uint32_t byte = a.planes[(int64_t)h * a.stride + i];
@@ -298,8 +301,8 @@ __global__ void __launch_bounds__(kThreads) eval_generic_kernel(const uint64_t* 
       if (h < 4) {
         idx[h & 3] = (int)byte;
       } else {
-        const int op = M.head_op[h];
-        if (op >= 0) X = (X & ~(3u << (2 * op))) | ((byte & 3u) << (2 * op));
+        const int slot = M.head_slot[h];
+        if (slot >= 0) Y |= (byte & 3u) << (2 * slot);
       }
     }
     Decoded c;
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) eval_generic_kernel(const uint64_t* 
     c.e = idx[1];
     c.p = idx[2];
     c.b = idx[3];
-    c.X = X;
+    c.Y = Y;
     Verdict v;
     v.thr = v.tpot = v.comp = v.comm = v.pipe = 0.0;
     double mem = 0.0;
@@ -325,13 +328,14 @@ __global__ void __launch_bounds__(kThreads) eval_generic_kernel(const uint64_t* 
 
 template <bool NEU, bool FULL, bool SG>
 void set_attr(size_t smem) {
-  cudaFuncSetAttribute(eval_tma_kernel<NEU, FULL, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace
 
 size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) {
-  return (size_t)kStages * A * kTile + (smem_gate ? (size_t)L.gate_words * 8 : 0) + (size_t)kQueue * 12;
+  return (size_t)kStages * A * kTile + (smem_gate ? (size_t)L.gate_words * 8 : 0) +
+         (size_t)kConsumerWarps * kWarpQueue * 12;
 }
 
 bool tma_eligible(const EvalArgs& a, int A) {
@@ -362,29 +366,29 @@ int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate) {
   int nb = 0;
   const size_t smem = tma_smem_bytes(L, A, smem_gate);
   if (smem_gate)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_tma_kernel<true, false, true>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, true>, kThreads, smem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_tma_kernel<true, false, false>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, false>, kThreads, smem);
   return nb;
 }
 
 int generic_blocks_per_sm() {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_generic_kernel<true>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_generic_kernel<true>, kGenericThreads, 0);
   return nb;
 }
 
 template <bool NEU, bool FULL>
-static void launch_tma_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
-                         const EvalArgs& a, cudaStream_t s) {
+static void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
+                        const EvalArgs& a, cudaStream_t s) {
   const int64_t ntiles = a.n / kTile;
   int64_t blocks = ntiles > 0 ? ntiles : 1;
   if (blocks > lp.max_blocks) blocks = lp.max_blocks;
   const size_t smem = tma_smem_bytes(L, M.A, lp.smem_gate);
   if (lp.smem_gate)
-    eval_tma_kernel<NEU, FULL, true><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles);
+    eval_ws_kernel<NEU, FULL, true><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles);
   else
-    eval_tma_kernel<NEU, FULL, false><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles);
+    eval_ws_kernel<NEU, FULL, false><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles);
 }
 
 cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
@@ -393,17 +397,17 @@ cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t*
   const bool full = a.tpot || a.mem || a.comp || a.comm || a.pipe;
   if (lp.tma) {
     if (neumaier) {
-      if (full) launch_tma_t<true, true>(lp, tab, L, M, a, s);
-      else launch_tma_t<true, false>(lp, tab, L, M, a, s);
+      if (full) launch_ws_t<true, true>(lp, tab, L, M, a, s);
+      else launch_ws_t<true, false>(lp, tab, L, M, a, s);
     } else {
-      if (full) launch_tma_t<false, true>(lp, tab, L, M, a, s);
-      else launch_tma_t<false, false>(lp, tab, L, M, a, s);
+      if (full) launch_ws_t<false, true>(lp, tab, L, M, a, s);
+      else launch_ws_t<false, false>(lp, tab, L, M, a, s);
     }
   } else {
-    int64_t blocks = (a.n + kThreads - 1) / kThreads;
+    int64_t blocks = (a.n + kGenericThreads - 1) / kGenericThreads;
     if (blocks > lp.max_blocks) blocks = lp.max_blocks;
-    if (neumaier) eval_generic_kernel<true><<<(unsigned)blocks, kThreads, 0, s>>>(tab, L, M, a);
-    else eval_generic_kernel<false><<<(unsigned)blocks, kThreads, 0, s>>>(tab, L, M, a);
+    if (neumaier) eval_generic_kernel<true><<<(unsigned)blocks, kGenericThreads, 0, s>>>(tab, L, M, a);
+    else eval_generic_kernel<false><<<(unsigned)blocks, kGenericThreads, 0, s>>>(tab, L, M, a);
   }
   return cudaGetLastError();
 }

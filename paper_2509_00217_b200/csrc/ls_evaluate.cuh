@@ -74,13 +74,19 @@ __device__ __forceinline__ uint64_t gword(const uint64_t* __restrict__ T, int i)
   return __ldg(reinterpret_cast<const unsigned long long*>(T) + i);
 }
 
-// Decode one candidate's heads into domain indices and the 2-bit axis word
-// (Strategy.axis_of over canonical ops: controlled head, pin, or UNSHARDED).
-// Returns false when a head is out of range (DecodingError, strategy.py:247-254).
+// A decoded candidate: domain indices and Y, the 2-bit axis of every axis
+// head in its field slot (ls_tables.cuh head_slots).
 struct Decoded {
   int t, e, p, b;
-  uint32_t X;
+  uint32_t Y;
 };
+
+// Axis of canonical op k (Strategy.axis_of, strategy.py:209-214): its head's
+// field in Y, or its pin / UNSHARDED.
+__device__ __forceinline__ int op_axis(const EvalMeta& M, uint32_t Y, int k) {
+  const int src = M.op_src[k];
+  return src >= 0 ? (int)((Y >> src) & 3u) : (int)M.op_pin[k];
+}
 
 // Gate pass. G: gate segment (shared memory or global). Returns the reason
 // code for gated candidates, or LS_REASON_NONE for survivors (which still
@@ -88,16 +94,20 @@ struct Decoded {
 __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, const EvalMeta& M, const Decoded& c,
                                          double& mem) {
   mem = 0.0;
+  const uint4 te = *reinterpret_cast<const uint4*>(G + L.te + 2 * (c.t * L.ne + c.e));
+  const uint64_t over = (uint64_t)te.x | ((uint64_t)te.y << 32);
+  const uint64_t lay = (uint64_t)te.z | ((uint64_t)te.w << 32);
   // gate 1: world_size > device_budget (simulator.py:257)
-  if ((G[L.ovb + c.t * L.ne + c.e] >> c.p) & 1) return LS_REASON_OVER_DEVICE_BUDGET;
+  if ((over >> c.p) & 1) return LS_REASON_OVER_DEVICE_BUDGET;
   // gate 2: pp | num_layers, ep vs num_experts, per-op admissibility and
   // extent divisibility (simulator.py:268, layout.py:371-374, :214-221)
-  const uint32_t lo = c.X & 0x555555u, hi = (c.X >> 1) & 0x555555u;
-  const uint64_t bad = ((~(lo | hi) & 0x555555u) & G[L.bad + c.t]) | ((lo & ~hi) & G[L.bad + L.nt + c.t]) |
-                       ((hi & ~lo) & G[L.bad + 2 * L.nt + c.t]);
-  if (bad | ((M.pp_bad >> c.p) & 1) | ((M.ep_bad >> c.e) & 1)) return LS_REASON_LAYOUT_ERROR;
+  const uint4 tm = *reinterpret_cast<const uint4*>(G + L.tmask + 2 * c.t);
+  const uint32_t lo = c.Y & 0x555555u, hi = (c.Y >> 1) & 0x555555u;
+  const uint32_t bad =
+      (~(lo | hi) & 0x555555u & tm.x) | (lo & ~hi & tm.y) | (hi & ~lo & tm.z) | tm.w | (uint32_t)((lay >> c.p) & 1);
+  if (bad) return LS_REASON_LAYOUT_ERROR;
   // gate 3: memory_per_device > hbm_capacity (simulator.py:135-160, :279)
-  const int a2 = ((c.X >> 6) & 3) == 2;
+  const int a2 = (M.attn_src >= 0 ? (int)((c.Y >> M.attn_src) & 3u) : M.attn_pin) == 2;
   mem = (dget(G, L.mem_w + (c.t * L.ne + c.e) * L.np + c.p) +
          dget(G, L.mem_kv + ((a2 * L.nt + c.t) * L.np + c.p) * L.nb + c.b)) +
         dget(G, L.mem_ws + c.b);
@@ -109,11 +119,12 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
 template <bool NEU>
 __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
                                           const Decoded& c, Verdict& v) {
-  const uint32_t X = c.X;
   const int t = c.t, e = c.e, p = c.p, b = c.b;
-  const int ax_emb = X & 3, ax_qkv = (X >> 2) & 3, ax_attn = (X >> 6) & 3, ax_out = (X >> 8) & 3;
-  const int ax_f1 = (X >> 12) & 3, ax_f2 = (X >> 14) & 3, ax_s1 = (X >> 16) & 3, ax_s2 = (X >> 18) & 3;
-  const int ax_lmh = (X >> 22) & 3;
+  const int ax_emb = op_axis(M, c.Y, LS_OP_EMBEDDING), ax_qkv = op_axis(M, c.Y, LS_OP_QKV_PROJ);
+  const int ax_attn = op_axis(M, c.Y, LS_OP_ATTN_CORE), ax_out = op_axis(M, c.Y, LS_OP_ATTN_OUT_PROJ);
+  const int ax_f1 = op_axis(M, c.Y, LS_OP_EXPERT_FFN1), ax_f2 = op_axis(M, c.Y, LS_OP_EXPERT_FFN2);
+  const int ax_s1 = op_axis(M, c.Y, LS_OP_SHARED_FFN1), ax_s2 = op_axis(M, c.Y, LS_OP_SHARED_FFN2);
+  const int ax_lmh = op_axis(M, c.Y, LS_OP_LM_HEAD);
   const int a2 = ax_attn == 2;
   const int nt = L.nt, ne = L.ne, nb = L.nb;
   const int tb = t * nb + b, teb = (t * ne + e) * nb + b;

@@ -119,29 +119,45 @@ __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, in
   if (w >= L.tpv && w < L.tpv + nt) return (uint64_t)TP[w - L.tpv];
   if (w >= L.epv && w < L.epv + ne) return (uint64_t)EP[w - L.epv];
   if (w >= L.ppv && w < L.ppv + np) return (uint64_t)PP[w - L.ppv];
-  // layout-error masks per (axis, tp): bit 2k when op k under that axis is
-  // inadmissible or its sharded extent does not divide tp (layout.py:214-221)
-  if (w >= L.bad && w < L.bad + 3 * nt) {
-    const int i = w - L.bad, t = i % nt, a = i / nt;
+  // [t][e]: {bit p: tp*ep*pp > device_budget (simulator.py:257),
+  //          bit p: num_layers % pp or ep vs num_experts (simulator.py:268, layout.py:371-374)}
+  if (w >= L.te && w < L.te + 2 * nt * ne) {
+    const int i = w - L.te, t = (i / 2) / ne, e = (i / 2) % ne;
     uint64_t m = 0;
-    for (int op = 0; op < LS_NUM_OPS; ++op) {
-      if ((op == LS_OP_SHARED_FFN1 || op == LS_OP_SHARED_FFN2) && !d.has_shared_expert) continue;
-      bool bad = !((admits_mask(op) >> a) & 1);
-      if (!bad && a != 0 && TP[t] > 1) {
-        const int64_t ext = shard_extent(d, op, a);
-        bad = ext < 0 || ext % TP[t] != 0;
+    const bool ep_bad = EP[e] > d.num_experts || d.num_experts % EP[e] != 0;
+    for (int p = 0; p < np; ++p) {
+      if (i % 2 == 0) {
+        if (TP[t] * EP[e] * PP[p] > d.device_budget) m |= 1ull << p;
+      } else if (ep_bad || d.num_layers % PP[p] != 0) {
+        m |= 1ull << p;
       }
-      if (bad) m |= 1ull << (2 * op);
     }
     return m;
   }
-  // over device budget: [t][e] -> bit p
-  if (w >= L.ovb && w < L.ovb + nt * ne) {
-    const int i = w - L.ovb, t = i / ne, e = i % ne;
-    uint64_t m = 0;
-    for (int p = 0; p < np; ++p)
-      if (TP[t] * EP[e] * PP[p] > d.device_budget) m |= 1ull << p;
-    return m;
+  // [t]: per-axis-value layout-error masks over Y fields, plus one bit for
+  // pinned ops: op k under axis a is an error when inadmissible or when its
+  // sharded extent does not divide tp (layout.py:214-221).
+  if (w >= L.tmask && w < L.tmask + 2 * nt) {
+    const int i = w - L.tmask, t = i / 2;
+    int slot[LS_MAX_HEADS];
+    head_slots(d, slot);
+    uint32_t bad[3] = {0, 0, 0}, pinned_bad = 0;
+    for (int op = 0; op < LS_NUM_OPS; ++op) {
+      if ((op == LS_OP_SHARED_FFN1 || op == LS_OP_SHARED_FFN2) && !d.has_shared_expert) continue;
+      for (int a = 0; a < 3; ++a) {
+        bool b = !((admits_mask(op) >> a) & 1);
+        if (!b && a != 0 && TP[t] > 1) {
+          const int64_t ext = shard_extent(d, op, a);
+          b = ext < 0 || ext % TP[t] != 0;
+        }
+        if (!b) continue;
+        const int h = d.op_head[op];
+        if (h >= 0) bad[a] |= 1u << (2 * slot[h]);
+        else if (d.op_pinned[op] == a) pinned_bad = 1;
+      }
+    }
+    if (i % 2 == 0) return (uint64_t)bad[0] | ((uint64_t)bad[1] << 32);
+    return (uint64_t)bad[2] | ((uint64_t)pinned_bad << 32);
   }
   return 0;  // padding
 }

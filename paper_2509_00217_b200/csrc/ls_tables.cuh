@@ -5,15 +5,20 @@
 // Each of those quantities is a pure function of a few domain indices —
 // (op, axis, tp, batch[, ep][, attention axis]) — so a workload compiles
 // into a few thousand float64 words computed ONCE per context by
-// ls_build_tables (ls_tables.cu) with exactly the reference's expression
-// order. Kernels then only gather and sum per candidate, which removes ~66
-// IEEE divisions per full-path candidate while staying bit-identical (each
-// entry IS the value the reference computes).
+// build_tables (ls_tables.cu) with exactly the reference's expression order.
+// Kernels then only gather and sum per candidate, which removes ~66 IEEE
+// divisions per full-path candidate while staying bit-identical (each entry
+// IS the value the reference computes).
 //
-// The buffer starts with the GATE segment (everything the cheap first pass
-// needs: budget / layout masks and the memory terms); the evaluate kernel
-// bulk-copies just that prefix into shared memory. The op/collective time
-// segments behind it are read through L1 by the compacted fp64 pass.
+// The buffer starts with the GATE segment — everything the first pass needs
+// (budget / layout bitmasks and the three memory terms) — which the evaluate
+// kernel bulk-copies into shared memory. The op / collective time segments
+// behind it are read through L1 by the compacted fp64 pass.
+//
+// Axis words. Candidates are decoded into Y: 2 bits per AXIS HEAD (heads
+// 4.., in head order), the order the SoA planes arrive in. Layout masks are
+// therefore built per head; the fp64 pass maps heads back to canonical ops
+// through EvalMeta::op_src.
 //
 // All words are 8 bytes: doubles, or int64/uint64 bit patterns.
 #pragma once
@@ -37,7 +42,9 @@ struct TabLayout {
   int nt, ne, np, nb;  // tp / ep / pp / batch domain sizes
   int has_shared;
   // gate segment (staged to shared memory)
-  int ovb, bad, mem_w, mem_kv, mem_ws;
+  int te;      // [t][e] x 2 words: {over-budget mask over p, layout-error mask over p}
+  int tmask;   // [t] x 2 words: {bad0 | bad1 << 32, bad2 | pinned_bad << 32} (head-order 2-bit fields)
+  int mem_w, mem_kv, mem_ws;
   int gate_words;  // words of the gate segment, even
   // op-time segments
   int opt_emb, opt_qkv, opt_kv, opt_attn, opt_out, opt_router, opt_ffn1, opt_ffn2;
@@ -54,14 +61,13 @@ struct TabLayout {
 // Warp-uniform per-workload scalars, passed by value as a kernel parameter.
 struct EvalMeta {
   int A;                              // vector length
-  int pad_;
+  int attn_src;                       // 2*(h-4) of the head controlling attn_core, or -1
+  int attn_pin;                       // attn_core axis when not controlled
+  int pad0_;
   uint8_t head_size[LS_MAX_HEADS];    // domain size per head
-  int8_t head_op[LS_MAX_HEADS];       // canonical op controlled by head, -1 none
-  uint32_t pinned_axes;               // 2 bits per canonical op (pins / UNSHARDED)
-  uint32_t pad2_;
-  uint64_t pp_bad;                    // bit p: num_layers % pp != 0 (simulator.py:268)
-  uint64_t ep_bad;                    // bit e: ep > num_experts or ne % ep (layout.py:371-374)
-  int64_t device_budget;
+  int8_t head_slot[LS_MAX_HEADS];     // Y field of each head (head_slots), -1 none
+  int8_t op_src[LS_NUM_OPS];          // per canonical op: bit shift of its field in Y, or -1 (pinned)
+  int8_t op_pin[LS_NUM_OPS];          // pinned axis of uncontrolled ops (default UNSHARDED)
   int64_t node_size;
   double num_layers_d;
   double slo_tpot;
@@ -70,6 +76,22 @@ struct EvalMeta {
 };
 
 __host__ __device__ inline int round2(int w) { return (w + 1) & ~1; }
+
+// 2-bit field slot of each axis head in the Y word. For A <= 16 (the TMA
+// kernel's domain) slot = h - 4, so planes map to fields positionally; for
+// longer vectors only the heads that control a canonical op get a slot
+// (0..11, in head order) and the rest are range-checked only (-1).
+__host__ __device__ inline void head_slots(const ls_workload_desc& d, int* slot) {
+  for (int h = 0; h < LS_MAX_HEADS; ++h) slot[h] = -1;
+  if (d.vector_length <= 16) {
+    for (int h = 4; h < d.vector_length; ++h) slot[h] = h - 4;
+    return;
+  }
+  int next = 0;
+  for (int h = 4; h < d.vector_length; ++h)
+    for (int k = 0; k < LS_NUM_OPS; ++k)
+      if (d.op_head[k] == h) slot[h] = next++;
+}
 
 inline TabLayout make_layout(const ls_workload_desc& d) {
   TabLayout L{};
@@ -85,8 +107,8 @@ inline TabLayout make_layout(const ls_workload_desc& d) {
     w += round2(words);
     return at;
   };
-  L.ovb = seg(nt * ne);
-  L.bad = seg(3 * nt);
+  L.te = seg(2 * nt * ne);
+  L.tmask = seg(2 * nt);
   L.mem_w = seg(nt * ne * np);
   L.mem_kv = seg(2 * nt * np * nb);
   L.mem_ws = seg(nb);
