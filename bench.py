@@ -209,13 +209,12 @@ def run_ours(args, rank, world, local_rank):
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        ev.evaluate(planes, out=out)
+        _, recs, count = ev.evaluate_topk(planes, k=ELITE_K, index_base=base, out=out)
         if timed:
             b.record(stream)
             ev_start.append(a)
             ev_end.append(b)
-        recs, count = ev.topk_records(planes, out.reason, out.throughput, k=ELITE_K, index_base=base)
-        launches = 3
+        launches = 2
         if world > 1:
             dist.all_gather_into_tensor(gathered, recs)
             dist.all_gather_into_tensor(gcounts, count)
@@ -305,7 +304,7 @@ def run_ours(args, rank, world, local_rank):
                 "api": "Evaluator.evaluate_host -> ls_evaluate_host"},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved_gbs / pk.get("hbm_gbs"), "traffic": traffic,
-                     "kernel": "eval_vec4_kernel", "algorithmic_bytes_per_candidate": ALGO_BYTES,
+                     "kernel": "eval_ws_kernel (fused evaluate + elite) + topk_merge_kernel", "algorithmic_bytes_per_candidate": ALGO_BYTES,
                      "kernel_ms_avg": kern_avg, "peak_source": f"{pk_kind} hbm_gbs (MEASURED_PEAKS.json)"},
         "gpu_launches": launches,
         "clocks": clk,

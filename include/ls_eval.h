@@ -188,6 +188,19 @@ int ls_topk(ls_ctx* ctx, const uint8_t* planes, int64_t plane_stride, const uint
             const double* throughput, const double* key, int64_t n, int k, int64_t index_base,
             ls_elite_rec* out, int32_t* count_out, void* scratch, void* stream);
 
+/* Fused evaluate + elite (the sweep path): score n device-resident
+ * candidates and reduce the valid ones to the top-k by RAW throughput over
+ * distinct vectors (LS_KEY_RAW semantics of ls_topk) in the same pass.
+ * `out` may be NULL (or out->reason NULL): then no per-candidate verdicts
+ * are written at all (16 B/candidate of HBM traffic). k <= 32. scratch must
+ * hold ls_evaluate_topk_scratch_bytes(ctx, n, k) bytes of device memory.
+ * Unaligned planes or vectors longer than 16 heads need `out` with reason and
+ * throughput (evaluated first, then reduced by ls_topk). */
+size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* ctx, int64_t n, int k);
+int ls_evaluate_topk(ls_ctx* ctx, const uint8_t* planes, int64_t n, int64_t plane_stride,
+                     const ls_result_soa* out, int k, int64_t index_base, ls_elite_rec* topk_out,
+                     int32_t* count_out, void* scratch, void* stream);
+
 /* Merge m device-resident record lists (e.g. the all-gathered per-rank top-k)
  * into the global top-k with the same ordering and dedupe rule. */
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,

@@ -361,6 +361,64 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
+size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
+  if (!c || k < 1) return 0;
+  const size_t fused = (size_t)c->blocks_tma * (size_t)k * sizeof(ls_elite_rec) + (size_t)c->blocks_tma * 4 + 16;
+  return std::max(fused, topk_scratch_bytes(n, k, 0));
+}
+
+int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_stride, const ls_result_soa* out,
+                     int k, int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                     void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || k < 1 || !topk_out || !count_out || !scratch || (n > 0 && !planes) || plane_stride < n)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_topk arguments");
+  DeviceGuard g(c->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  EvalArgs a{};
+  a.planes = planes;
+  a.n = n;
+  a.stride = plane_stride;
+  if (out) {
+    a.reason = out->reason;
+    a.thr = out->throughput;
+    a.tpot = out->tpot_s;
+    a.mem = out->memory_bytes;
+    a.comp = out->compute_s;
+    a.comm = out->comm_s;
+    a.pipe = out->pipeline_s;
+  }
+  if (!a.reason) a.thr = a.tpot = a.mem = a.comp = a.comm = a.pipe = nullptr;
+  cudaError_t e;
+  if (k <= fused_k_max() && c->blocks_tma > 0 && tma_eligible(a, c->M.A)) {
+    LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
+    const int64_t grid = ws_grid(lp, n);
+    TopkArgs tk{k, index_base, static_cast<ls_elite_rec*>(scratch), nullptr};
+    tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
+    if (n == 0) {
+      cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
+      return LS_OK;
+    }
+    if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s)) !=
+        cudaSuccess)
+      return cuda_fail(e, "evaluate_topk launch");
+    if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, topk_out, count_out, s)) != cudaSuccess)
+      return cuda_fail(e, "topk merge launch");
+    return LS_OK;
+  }
+  if (!a.reason || !a.thr)
+    return fail(LS_ERR_UNSUPPORTED,
+                "unaligned planes, k > 32 or vectors longer than 16 heads need per-candidate reason + throughput "
+                "outputs");
+  int rc = do_evaluate(c, planes, n, plane_stride, out, s);
+  if (rc) return rc;
+  if (c->space_size == 0) return fail(LS_ERR_UNSUPPORTED, "vector codes overflow 63 bits for this action space");
+  if (k > 64) return fail(LS_ERR_INVALID_ARGUMENT, "k must be <= 64");
+  e = launch_topk(c->TM, planes, plane_stride, a.reason, a.thr, a.thr, n, k, index_base, topk_out, count_out, scratch,
+                  c->num_sms, s);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
+}
+
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k, ls_elite_rec* out,
                   int32_t* count_out, void* stream) {
   g_err.clear();

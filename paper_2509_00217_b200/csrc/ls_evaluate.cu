@@ -23,6 +23,7 @@
 
 #include "ls_evaluate.cuh"
 #include "ls_kernels.h"
+#include "ls_topk.cuh"
 
 namespace ls {
 
@@ -35,6 +36,7 @@ constexpr int kTile = kConsumerWarps * kWarpCands;  // candidates per stage
 constexpr int kStages = 4;
 constexpr int kWarpQueue = 160;  // < 32 left over + 128 from one tile
 constexpr int kGenericThreads = 256;
+constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -129,10 +131,10 @@ __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, in
   c.Y = ((q[0] >> sh) & 0xffu) | (((q[1] >> sh) & 0xffu) << 8) | (((q[2] >> sh) & 0xffu) << 16);
 }
 
-template <bool NEU, bool FULL, bool SMEM_GATE>
+template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK>
 __global__ void __launch_bounds__(kThreads, 2)
     eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
-                   const int64_t ntiles) {
+                   const int64_t ntiles, const TopkArgs tk) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
@@ -143,9 +145,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* G = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
   uint64_t* qkey_all = SMEM_GATE ? G + L.gate_words : G;
   uint32_t* qy_all = reinterpret_cast<uint32_t*>(qkey_all + kConsumerWarps * kWarpQueue);
+  uint8_t* lists = reinterpret_cast<uint8_t*>(qy_all + kConsumerWarps * kWarpQueue);
+  __shared__ int list_count[kConsumerWarps];
   const uint64_t* Gt = SMEM_GATE ? G : gtab;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  if (TOPK && threadIdx.x < kConsumerWarps) list_count[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -180,19 +185,34 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* qkey = qkey_all + warp * kWarpQueue;
   uint32_t* qy = qy_all + warp * kWarpQueue;
   int qcount = 0;  // warp-uniform
+  WarpList wl;
+  if (TOPK) wl.bind(lists + warp * warp_list_bytes(kFusedK), kFusedK, &list_count[warp]);
   if (SMEM_GATE) mbar_wait(&gate_bar, 0);
 
   // fp64 pass over the 32 newest queue entries (or the first n < 32 at the end)
   auto drain = [&](int n) {
     __syncwarp();
+    int64_t idx = 0;
+    Decoded c;
+    Verdict v;
+    v.reason = LS_REASON_DECODE_ERROR;
+    v.thr = 0.0;
     if (lane < n) {
       const int pos = qcount - n + lane;
-      int64_t idx;
-      Decoded c;
       unpack_key(qkey[pos], qy[pos], idx, c);
-      Verdict v;
       full_path<NEU>(gtab, L, M, c, v);
-      write_verdict<FULL>(a, idx, v);
+      if (a.reason) write_verdict<FULL>(a, idx, v);
+    }
+    if (TOPK) {  // fused elite: valid survivors offered to the warp's top-k list
+      Rec r{v.thr, v.thr, tk.index_base + idx, 0};
+      const bool ok = lane < n && v.reason == LS_REASON_NONE && wl.admits(r.key, r.idx, tk.k);
+      if (ok) {
+        uint64_t code = (uint64_t)c.t * M.code_stride[0] + (uint64_t)c.e * M.code_stride[1] +
+                        (uint64_t)c.p * M.code_stride[2] + (uint64_t)c.b * M.code_stride[3];
+        for (int h = 4; h < M.A; ++h) code += (uint64_t)((c.Y >> (2 * (h - 4))) & 3u) * M.code_stride[h];
+        r.code = code;
+      }
+      wl.offer(ok, r, tk.k);
     }
     qcount -= n;
     __syncwarp();
@@ -222,7 +242,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       r4 |= reason << (8 * j);
       m[j] = mem;
     }
-    if (count == 4) {
+    if (!a.reason) {
+      // sweep mode: no per-candidate verdicts, only the fused elite
+    } else if (count == 4) {
       *reinterpret_cast<uint32_t*>(a.reason + base) = r4;
       if (a.thr) {
         st2(a.thr, base, 0.0, 0.0);
@@ -285,6 +307,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     pass_a(w, base, count);
   }
   if (qcount > 0) drain(qcount);
+  if (TOPK) {  // merge the consumer warps' lists (named barrier: the producer warp is gone)
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+    if (warp == 0) {
+      for (int o = 1; o < kConsumerWarps; ++o) {
+        WarpList other;
+        other.bind(lists + o * warp_list_bytes(kFusedK), kFusedK, &list_count[o]);
+        wl.absorb(other, tk.k);
+      }
+      wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
+    }
+  }
 }
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
@@ -328,14 +361,15 @@ __global__ void __launch_bounds__(kGenericThreads) eval_generic_kernel(const uin
 
 template <bool NEU, bool FULL, bool SG>
 void set_attr(size_t smem) {
-  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace
 
 size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) {
   return (size_t)kStages * A * kTile + (smem_gate ? (size_t)L.gate_words * 8 : 0) +
-         (size_t)kConsumerWarps * kWarpQueue * 12;
+         (size_t)kConsumerWarps * kWarpQueue * 12 + (size_t)kConsumerWarps * warp_list_bytes(kFusedK);
 }
 
 bool tma_eligible(const EvalArgs& a, int A) {
@@ -366,9 +400,9 @@ int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate) {
   int nb = 0;
   const size_t smem = tma_smem_bytes(L, A, smem_gate);
   if (smem_gate)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, true>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, true, true>, kThreads, smem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, false>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, false, true>, kThreads, smem);
   return nb;
 }
 
@@ -378,37 +412,57 @@ int generic_blocks_per_sm() {
   return nb;
 }
 
-template <bool NEU, bool FULL>
+template <bool NEU, bool FULL, bool TOPK>
 static void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
-                        const EvalArgs& a, cudaStream_t s) {
+                        const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
   const int64_t ntiles = a.n / kTile;
-  int64_t blocks = ntiles > 0 ? ntiles : 1;
-  if (blocks > lp.max_blocks) blocks = lp.max_blocks;
   const size_t smem = tma_smem_bytes(L, M.A, lp.smem_gate);
+  const unsigned blocks = (unsigned)ws_grid(lp, a.n);
   if (lp.smem_gate)
-    eval_ws_kernel<NEU, FULL, true><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles);
+    eval_ws_kernel<NEU, FULL, true, TOPK><<<blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
   else
-    eval_ws_kernel<NEU, FULL, false><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles);
+    eval_ws_kernel<NEU, FULL, false, TOPK><<<blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
 }
+
+template <bool TOPK>
+static void launch_ws(const LaunchPlan& lp, bool neumaier, bool full, const uint64_t* tab, const TabLayout& L,
+                      const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
+  if (neumaier) {
+    if (full) launch_ws_t<true, true, TOPK>(lp, tab, L, M, a, tk, s);
+    else launch_ws_t<true, false, TOPK>(lp, tab, L, M, a, tk, s);
+  } else {
+    if (full) launch_ws_t<false, true, TOPK>(lp, tab, L, M, a, tk, s);
+    else launch_ws_t<false, false, TOPK>(lp, tab, L, M, a, tk, s);
+  }
+}
+
+int64_t ws_grid(const LaunchPlan& lp, int64_t n) {
+  const int64_t ntiles = n / kTile;
+  int64_t blocks = ntiles > 0 ? ntiles : 1;
+  return blocks > lp.max_blocks ? lp.max_blocks : blocks;
+}
+
+int fused_k_max() { return kFusedK; }
 
 cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
                             const EvalMeta& M, const EvalArgs& a, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
   const bool full = a.tpot || a.mem || a.comp || a.comm || a.pipe;
   if (lp.tma) {
-    if (neumaier) {
-      if (full) launch_ws_t<true, true>(lp, tab, L, M, a, s);
-      else launch_ws_t<true, false>(lp, tab, L, M, a, s);
-    } else {
-      if (full) launch_ws_t<false, true>(lp, tab, L, M, a, s);
-      else launch_ws_t<false, false>(lp, tab, L, M, a, s);
-    }
+    launch_ws<false>(lp, neumaier, full, tab, L, M, a, TopkArgs{}, s);
   } else {
     int64_t blocks = (a.n + kGenericThreads - 1) / kGenericThreads;
     if (blocks > lp.max_blocks) blocks = lp.max_blocks;
     if (neumaier) eval_generic_kernel<true><<<(unsigned)blocks, kGenericThreads, 0, s>>>(tab, L, M, a);
     else eval_generic_kernel<false><<<(unsigned)blocks, kGenericThreads, 0, s>>>(tab, L, M, a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
+                                 const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
+  const bool full = a.reason && (a.tpot || a.mem || a.comp || a.comm || a.pipe);
+  launch_ws<true>(lp, neumaier, full, tab, L, M, a, tk, s);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,20 @@ struct LaunchPlan {
 
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
 
+// Fused evaluate + top-k by raw (eval_ws_kernel<..., TOPK>): every CTA emits
+// its elite list to part[blockIdx.x * k ..] / part_counts[blockIdx.x].
+struct TopkArgs {
+  int k;
+  int64_t index_base;
+  ls_elite_rec* part;
+  int32_t* part_counts;
+};
+
 bool tma_eligible(const EvalArgs& a, int A);
+int64_t ws_grid(const LaunchPlan& lp, int64_t n);
+int fused_k_max();
+cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
+                                 const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s);
 cudaError_t prepare_eval_kernels(const TabLayout& L, int A, bool smem_gate);
 int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate);
 int generic_blocks_per_sm();

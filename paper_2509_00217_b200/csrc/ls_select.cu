@@ -21,6 +21,7 @@
 #include <float.h>
 
 #include "ls_kernels.h"
+#include "ls_topk.cuh"
 
 namespace ls {
 
@@ -138,229 +139,77 @@ __global__ void reward_kernel(const uint8_t* __restrict__ reason, const double* 
 
 // ---------------------------------------------------------------- top-k
 
-struct Rec {
-  double key, raw;
-  int64_t idx;
-  uint64_t code;
-};
-
-__device__ __forceinline__ bool better(double ka, int64_t ia, double kb, int64_t ib) {
-  return ka > kb || (ka == kb && ia < ib);
-}
-
-// A sorted (best first) list of at most k <= 64 distinct records in shared
-// memory, operated on by one full warp.
-struct WarpList {
-  double* key;
-  double* raw;
-  int64_t* idx;
-  uint64_t* code;
-  int* count;
-
-  // Warp-cooperative insert of r (all lanes pass the same r).
-  __device__ void insert(const Rec& r, int k) {
-    const int lane = threadIdx.x & 31;
-    const int cnt = *count;
-    // duplicate vector already listed?
-    int dup = -1;
-    for (int j = lane; j < cnt; j += 32)
-      if (code[j] == r.code) dup = j;
-    for (int o = 16; o > 0; o >>= 1) dup = max(dup, __shfl_xor_sync(0xffffffffu, dup, o));
-    int n = cnt;
-    if (dup >= 0) {
-      if (!better(r.key, r.idx, key[dup], idx[dup])) return;
-      remove_at(dup, n);
-      --n;
-    } else if (n == k) {
-      if (!better(r.key, r.idx, key[k - 1], idx[k - 1])) return;
-      --n;  // drop the worst
-    }
-    // insertion position = number of entries ranked before r
-    int before = 0;
-    for (int j = lane; j < n; j += 32) before += better(key[j], idx[j], r.key, r.idx) ? 1 : 0;
-    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
-    // shift [before, n) down by one: read all, then write
-    double kk[2], rr[2];
-    int64_t ii[2];
-    uint64_t cc[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int j = lane + 32 * s;
-      if (j >= before && j < n) {
-        kk[s] = key[j];
-        rr[s] = raw[j];
-        ii[s] = idx[j];
-        cc[s] = code[j];
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int j = lane + 32 * s;
-      if (j >= before && j < n) {
-        key[j + 1] = kk[s];
-        raw[j + 1] = rr[s];
-        idx[j + 1] = ii[s];
-        code[j + 1] = cc[s];
-      }
-    }
-    if (lane == 0) {
-      key[before] = r.key;
-      raw[before] = r.raw;
-      idx[before] = r.idx;
-      code[before] = r.code;
-      *count = n + 1;
-    }
-    __syncwarp();
-  }
-
-  __device__ void remove_at(int pos, int n) {
-    const int lane = threadIdx.x & 31;
-    double kk[2], rr[2];
-    int64_t ii[2];
-    uint64_t cc[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int j = lane + 32 * s;
-      if (j > pos && j < n) {
-        kk[s] = key[j];
-        rr[s] = raw[j];
-        ii[s] = idx[j];
-        cc[s] = code[j];
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int j = lane + 32 * s;
-      if (j > pos && j < n) {
-        key[j - 1] = kk[s];
-        raw[j - 1] = rr[s];
-        idx[j - 1] = ii[s];
-        code[j - 1] = cc[s];
-      }
-    }
-    __syncwarp();
-  }
-
-  // Would r enter the list (ignoring duplicates)? Cheap pre-filter.
-  __device__ __forceinline__ bool admits(double k_, int64_t i_, int k) const {
-    const int cnt = *count;
-    return cnt < k || better(k_, i_, key[k - 1], idx[k - 1]);
-  }
-};
-
 constexpr int kTopkThreads = 256;
 constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kTopkPerLane = 16;  // candidates per lane per chunk (one 16-byte reason load)
 
-struct ListSmem {
-  double key[kTopkWarps][64];
-  double raw[kTopkWarps][64];
-  int64_t idx[kTopkWarps][64];
-  uint64_t code[kTopkWarps][64];
+struct TopkSmem {
+  double lists[kTopkWarps][4 * 64];
   int count[kTopkWarps];
 };
 
-__device__ __forceinline__ WarpList warp_list(ListSmem& s, int w) {
-  WarpList l;
-  l.key = s.key[w];
-  l.raw = s.raw[w];
-  l.idx = s.idx[w];
-  l.code = s.code[w];
-  l.count = &s.count[w];
-  return l;
+__device__ __forceinline__ uint64_t vector_code(const TopkMeta& tm, const uint8_t* planes, int64_t stride, int64_t i) {
+  uint64_t c = 0;
+  for (int h = 0; h < tm.A; ++h) c += (uint64_t)planes[(int64_t)h * stride + i] * (uint64_t)tm.code_stride[h];
+  return c;
 }
 
-// Offer a stream of records, 32 at a time, to warp list `wl`.
-__device__ __forceinline__ void offer_lanes(WarpList& wl, bool have, const Rec& mine, int k) {
-  const bool cand = have && wl.admits(mine.key, mine.idx, k);
-  unsigned mask = __ballot_sync(0xffffffffu, cand);
-  while (mask) {
-    const int src = __ffs(mask) - 1;
-    mask &= mask - 1;
-    Rec r;
-    r.key = __shfl_sync(0xffffffffu, mine.key, src);
-    r.raw = __shfl_sync(0xffffffffu, mine.raw, src);
-    r.idx = __shfl_sync(0xffffffffu, mine.idx, src);
-    r.code = __shfl_sync(0xffffffffu, mine.code, src);
-    wl.insert(r, k);
-  }
-}
-
-// Write the CTA's merged list (warp 0 list after merging the others).
-__device__ void merge_warps_and_emit(ListSmem& s, int k, ls_elite_rec* out, int32_t* count_out) {
-  __syncthreads();
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w == 0) {
-    WarpList l0 = warp_list(s, 0);
-    for (int src = 1; src < kTopkWarps; ++src) {
-      const int cnt = s.count[src];
-      for (int j0 = 0; j0 < cnt; j0 += 32) {
-        const int j = j0 + lane;
-        Rec r;
-        const bool have = j < cnt;
-        if (have) {
-          r.key = s.key[src][j];
-          r.raw = s.raw[src][j];
-          r.idx = s.idx[src][j];
-          r.code = s.code[src][j];
-        } else {
-          r.key = 0;
-          r.raw = 0;
-          r.idx = 0;
-          r.code = 0;
-        }
-        offer_lanes(l0, have, r, k);
-      }
-    }
-    const int cnt = s.count[0];
-    for (int j = lane; j < cnt; j += 32) {
-      ls_elite_rec o;
-      o.key = s.key[0][j];
-      o.raw = s.raw[0][j];
-      o.index = s.idx[0][j];
-      o.code = s.code[0][j];
-      out[j] = o;
-    }
-    if (lane == 0) *count_out = cnt;
-  }
-}
-
+// Per-CTA top-k of valid candidates over a contiguous slice of the batch.
 __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(const TopkMeta tm, const uint8_t* __restrict__ planes,
                                                                   int64_t stride, const uint8_t* __restrict__ reason,
                                                                   const double* __restrict__ thr,
                                                                   const double* __restrict__ key, int64_t n, int k,
                                                                   int64_t index_base, ls_elite_rec* __restrict__ out,
                                                                   int32_t* __restrict__ counts) {
-  __shared__ ListSmem s;
+  __shared__ TopkSmem s;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) s.count[w] = 0;
   __syncwarp();
-  WarpList wl = warp_list(s, w);
-  // contiguous chunk per CTA, split into contiguous sub-chunks per warp
-  const int64_t per_cta = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = (int64_t)blockIdx.x * per_cta;
-  const int64_t hi = min(n, lo + per_cta);
-  const int64_t per_warp = (hi - lo + kTopkWarps - 1) / kTopkWarps;
-  const int64_t wlo = lo + (int64_t)w * per_warp;
-  const int64_t whi = min(hi, wlo + per_warp);
-  for (int64_t base = wlo; base < whi; base += 32) {
-    const int64_t i = base + lane;
-    const bool have = i < whi && reason[i] == LS_REASON_NONE;
-    Rec r;
-    r.key = have ? key[i] : 0.0;
-    r.raw = have ? thr[i] : 0.0;
-    r.idx = index_base + i;
-    r.code = 0;
-    const bool cand = have && wl.admits(r.key, r.idx, k);
-    if (cand) {
-      uint64_t c = 0;
-      for (int h = 0; h < tm.A; ++h) c += (uint64_t)planes[(int64_t)h * stride + i] * (uint64_t)tm.code_stride[h];
-      r.code = c;
+  WarpList wl;
+  wl.bind(s.lists[w], 64, &s.count[w]);
+  const int64_t chunk = 32 * kTopkPerLane;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const bool vec = ((uintptr_t)reason % 16) == 0;
+  for (int64_t ch = (int64_t)blockIdx.x * kTopkWarps + w; ch < nchunks; ch += (int64_t)gridDim.x * kTopkWarps) {
+    const int64_t base = ch * chunk + (int64_t)lane * kTopkPerLane;
+    uint32_t pending = 0;
+    if (vec && base + kTopkPerLane <= n) {
+      const uint4 r = *reinterpret_cast<const uint4*>(reason + base);
+      const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (((words[q] >> (8 * b)) & 0xffu) == LS_REASON_NONE) pending |= 1u << (4 * q + b);
+    } else {
+      for (int j = 0; j < kTopkPerLane; ++j)
+        if (base + j < n && reason[base + j] == LS_REASON_NONE) pending |= 1u << j;
     }
-    offer_lanes(wl, cand, r, k);
+    while (__any_sync(0xffffffffu, pending != 0)) {
+      Rec r{0.0, 0.0, 0, 0};
+      bool have = false;
+      if (pending) {
+        const int j = __ffs(pending) - 1;
+        pending &= pending - 1;
+        const int64_t i = base + j;
+        r.key = key[i];
+        r.raw = thr[i];
+        r.idx = index_base + i;
+        have = wl.admits(r.key, r.idx, k);
+        if (have) r.code = vector_code(tm, planes, stride, i);
+      }
+      wl.offer(have, r, k);
+    }
   }
-  merge_warps_and_emit(s, k, out + (int64_t)blockIdx.x * k, counts + blockIdx.x);
+  __syncthreads();
+  if (w == 0) {
+    for (int o = 1; o < kTopkWarps; ++o) {
+      WarpList other;
+      other.bind(s.lists[o], 64, &s.count[o]);
+      wl.absorb(other, k);
+    }
+    wl.emit(out + (int64_t)blockIdx.x * k, counts + blockIdx.x);
+  }
 }
 
 // Merge m lists of up to k_in records each into one list of k. One CTA.
@@ -368,32 +217,37 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite
                                                                   const int32_t* __restrict__ counts, int m, int k_in,
                                                                   int k, ls_elite_rec* __restrict__ out,
                                                                   int32_t* __restrict__ count_out) {
-  __shared__ ListSmem s;
+  __shared__ TopkSmem s;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) s.count[w] = 0;
   __syncwarp();
-  WarpList wl = warp_list(s, w);
+  WarpList wl;
+  wl.bind(s.lists[w], 64, &s.count[w]);
   for (int list = w; list < m; list += kTopkWarps) {
     const int cnt = min(counts[list], k_in);
     for (int j0 = 0; j0 < cnt; j0 += 32) {
       const int j = j0 + lane;
       const bool have = j < cnt;
-      Rec r;
+      Rec r{0.0, 0.0, 0, 0};
       if (have) {
         const ls_elite_rec& e = recs[(int64_t)list * k_in + j];
         r.key = e.key;
         r.raw = e.raw;
         r.idx = e.index;
         r.code = e.code;
-      } else {
-        r.key = r.raw = 0.0;
-        r.idx = 0;
-        r.code = 0;
       }
-      offer_lanes(wl, have, r, k);
+      wl.offer(have, r, k);
     }
   }
-  merge_warps_and_emit(s, k, out, count_out);
+  __syncthreads();
+  if (w == 0) {
+    for (int o = 1; o < kTopkWarps; ++o) {
+      WarpList other;
+      other.bind(s.lists[o], 64, &s.count[o]);
+      wl.absorb(other, k);
+    }
+    wl.emit(out, count_out);
+  }
 }
 
 }  // namespace
@@ -422,8 +276,8 @@ cudaError_t launch_reward_scan(const uint8_t* reason, const double* thr, int64_t
 
 static int topk_ctas(int64_t n, int num_sms) {
   (void)num_sms;
-  int64_t c = (n + 8191) / 8192;
-  const int64_t cap = 296;  // two CTAs per B200 SM
+  int64_t c = (n + 65535) / 65536;
+  const int64_t cap = 148 * 4;  // four CTAs per B200 SM
   if (c > cap) c = cap;
   if (c < 1) c = 1;
   return (int)c;

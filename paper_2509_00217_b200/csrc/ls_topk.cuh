@@ -1,0 +1,169 @@
+// ls_topk.cuh — warp-cooperative elite list (shared by the evaluate and
+// select kernels).
+//
+// EliteBuffer.offer (policy.py:86-102) keeps the best `capacity` DISTINCT
+// vectors, older first among equal rewards; build_report(by_raw)
+// (ppo.py:441-447) keeps the earliest best raw. For an empty start both are
+// "top-k over distinct vectors by (key desc, index asc), each vector ranked
+// by its best occurrence". A WarpList holds such a
+// list in shared memory; its insert rule — a duplicate vector is replaced
+// only by a better occurrence, the worst entry is evicted when full — keeps
+// the invariant "list == top-k distinct of everything offered" for ANY
+// arrival order, so per-warp lists, per-CTA merges and the cross-GPU merge of
+// all-gathered per-rank lists all compose exactly.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/ls_eval.h"
+
+namespace ls {
+
+struct Rec {
+  double key, raw;
+  int64_t idx;
+  uint64_t code;
+};
+
+__device__ __forceinline__ bool better(double ka, int64_t ia, double kb, int64_t ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+// Sorted (best first) list of at most k <= 64 distinct records in shared
+// memory, operated on by one full warp.
+struct WarpList {
+  double* key;
+  double* raw;
+  int64_t* idx;
+  uint64_t* code;
+  int* count;
+
+  __device__ void bind(void* base, int cap, int* cnt) {
+    key = static_cast<double*>(base);
+    raw = key + cap;
+    idx = reinterpret_cast<int64_t*>(raw + cap);
+    code = reinterpret_cast<uint64_t*>(idx + cap);
+    count = cnt;
+  }
+
+  __device__ void move_range(int from, int to_shift, int lo, int n) {
+    // entries j in [lo, n) move to j + to_shift (to_shift = +1 or -1)
+    const int lane = threadIdx.x & 31;
+    double kk[2], rr[2];
+    int64_t ii[2];
+    uint64_t cc[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int j = lane + 32 * s;
+      if (j >= lo && j < n) {
+        kk[s] = key[j];
+        rr[s] = raw[j];
+        ii[s] = idx[j];
+        cc[s] = code[j];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int j = lane + 32 * s;
+      if (j >= lo && j < n) {
+        key[j + to_shift] = kk[s];
+        raw[j + to_shift] = rr[s];
+        idx[j + to_shift] = ii[s];
+        code[j + to_shift] = cc[s];
+      }
+    }
+    __syncwarp();
+    (void)from;
+  }
+
+  // Warp-cooperative insert of r (all lanes pass the same r).
+  __device__ void insert(const Rec& r, int k) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = *count;
+    int dup = -1;
+    for (int j = lane; j < cnt; j += 32)
+      if (code[j] == r.code) dup = j;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dup = max(dup, __shfl_xor_sync(0xffffffffu, dup, o));
+    int n = cnt;
+    if (dup >= 0) {
+      if (!better(r.key, r.idx, key[dup], idx[dup])) return;
+      move_range(0, -1, dup + 1, n);
+      --n;
+    } else if (n == k) {
+      if (!better(r.key, r.idx, key[k - 1], idx[k - 1])) return;
+      --n;  // drop the worst
+    }
+    int before = 0;
+    for (int j = lane; j < n; j += 32) before += better(key[j], idx[j], r.key, r.idx) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    move_range(0, +1, before, n);
+    if (lane == 0) {
+      key[before] = r.key;
+      raw[before] = r.raw;
+      idx[before] = r.idx;
+      code[before] = r.code;
+      *count = n + 1;
+    }
+    __syncwarp();
+  }
+
+  // Could r enter the list (ignoring duplicates)? Cheap pre-filter.
+  __device__ __forceinline__ bool admits(double k_, int64_t i_, int k) const {
+    return *count < k || better(k_, i_, key[k - 1], idx[k - 1]);
+  }
+
+  // Offer one record per lane (lanes with have == false offer nothing).
+  __device__ void offer(bool have, const Rec& mine, int k) {
+    const bool cand = have && admits(mine.key, mine.idx, k);
+    unsigned mask = __ballot_sync(0xffffffffu, cand);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      Rec r;
+      r.key = __shfl_sync(0xffffffffu, mine.key, src);
+      r.raw = __shfl_sync(0xffffffffu, mine.raw, src);
+      r.idx = __shfl_sync(0xffffffffu, mine.idx, src);
+      r.code = __shfl_sync(0xffffffffu, mine.code, src);
+      insert(r, k);
+    }
+  }
+
+  // Offer every record of another list (any order is exact).
+  __device__ void absorb(const WarpList& o, int k) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = *o.count;
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      const int j = j0 + lane;
+      Rec r{0.0, 0.0, 0, 0};
+      const bool have = j < cnt;
+      if (have) {
+        r.key = o.key[j];
+        r.raw = o.raw[j];
+        r.idx = o.idx[j];
+        r.code = o.code[j];
+      }
+      offer(have, r, k);
+    }
+  }
+
+  __device__ void emit(ls_elite_rec* out, int32_t* count_out) const {
+    const int lane = threadIdx.x & 31;
+    const int cnt = *count;
+    for (int j = lane; j < cnt; j += 32) {
+      ls_elite_rec e;
+      e.key = key[j];
+      e.raw = raw[j];
+      e.index = idx[j];
+      e.code = code[j];
+      out[j] = e;
+    }
+    if (lane == 0) *count_out = cnt;
+  }
+};
+
+// Bytes of one WarpList of capacity cap.
+__host__ __device__ constexpr int warp_list_bytes(int cap) { return cap * 32; }
+
+}  // namespace ls

@@ -102,6 +102,7 @@ class Evaluator:
         self.vector_length = self.desc.vector_length
         self.head_sizes = tuple(int(self.desc.domain_len[h]) if h < 4 else 3 for h in range(self.vector_length))
         self.space_size = int(self._lib.ls_space_size(self._ctx))
+        self._scratch: torch.Tensor | None = None
 
     # -- lifecycle ----------------------------------------------------------
 
@@ -225,6 +226,32 @@ class Evaluator:
         vecs = codes_to_vectors(raw["code"], self.space) if n else np.zeros((0, self.vector_length), np.int64)
         return [Elite(tuple(int(x) for x in vecs[i]), float(raw["key"][i]), float(raw["raw"][i]), int(raw["index"][i]))
                 for i in range(n)]
+
+    def evaluate_topk(self, planes: torch.Tensor, k: int = 3, index_base: int = 0, out: BatchResult | None = None,
+                      fields=("throughput",), verdicts: bool = True):
+        """Fused sweep: score the batch and reduce it to the top-k by raw in one pass.
+
+        With ``verdicts=False`` nothing per-candidate is written (16 B of HBM
+        traffic per candidate); otherwise ``out`` (allocated if None) receives
+        the same verdicts ``evaluate`` produces. Returns (out, records, count).
+        """
+        if planes.device != self.device:
+            raise ValueError(f"planes live on {planes.device}, evaluator on {self.device}")
+        n, stride = self._check_planes(planes)
+        if verdicts and out is None:
+            out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=self.device))
+            for f in (FIELDS if fields == "all" else fields):
+                setattr(out, f, torch.empty(n, dtype=torch.float64, device=self.device))
+        soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
+        recs = torch.zeros((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
+        if self._scratch is None or self._scratch.numel() < nbytes:
+            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        check(self._lib.ls_evaluate_topk(self._ctx, ctypes.c_void_p(planes.data_ptr()), n, stride,
+                                         ctypes.byref(soa) if soa is not None else None, int(k), int(index_base),
+                                         _ptr(recs), _ptr(count), _ptr(self._scratch), self._stream()))
+        return (out if verdicts else None), recs, count
 
     def merge_records(self, recs: torch.Tensor, counts: torch.Tensor, k_in: int, k: int):
         """Merge m stacked record lists ([m*k_in, 32] bytes, counts [m]) into one top-k."""

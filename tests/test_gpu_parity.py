@@ -195,3 +195,30 @@ def test_topk_many_duplicates_and_merge(ev_factory):
     mrec, mcount = ev.merge_records(torch.cat(recs), torch.cat(counts), 16, 16)
     merged = ev.decode_records(mrec, mcount)
     assert [(e.vector, e.index, e.raw) for e in merged] == [(e.vector, e.index, e.raw) for e in got]
+
+
+@pytest.mark.parametrize("name", ["moe_1p2t", "moe_1p6t_2048", "dsv3_style_h100x256", "tiny", "unit_small"])
+@pytest.mark.parametrize("k", [1, 3, 8, 32])
+def test_fused_evaluate_topk_matches_sequential_by_raw(name, k, ev_factory):
+    """Fused sweep (evaluate + elite in one kernel) == sequential offers of
+    every valid candidate keyed by raw, with and without verdict output."""
+    from oracle.cost_model import simulate_planes
+    from oracle.search_semantics import elite_offers
+
+    wl, meta, data = load_eval(name)
+    ev = ev_factory(wl)
+    rng = np.random.default_rng(k)
+    base = data["vectors"]
+    vecs = np.concatenate([base, base[rng.integers(0, len(base), size=30_000)]])  # repeats
+    planes_np = np.ascontiguousarray(vecs.T.astype(np.uint8))
+    want_res = simulate_planes(wl.desc(), planes_np)
+    want = elite_offers(vecs, want_res["throughput"], want_res["reason"] == 0, k)
+    planes = _dev(planes_np)
+    out, recs, count = ev.evaluate_topk(planes, k=k, index_base=1000)
+    got = ev.decode_records(recs, count)
+    assert [e.vector for e in got] == [w[0] for w in want]
+    assert [e.index for e in got] == [w[2] + 1000 for w in want]
+    assert [e.raw for e in got] == [w[1] for w in want]
+    assert not mismatches(out.numpy(), want_res).any()
+    _, recs2, count2 = ev.evaluate_topk(planes, k=k, index_base=1000, verdicts=False)
+    assert [e.index for e in ev.decode_records(recs2, count2)] == [e.index for e in got]
