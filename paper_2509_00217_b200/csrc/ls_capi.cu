@@ -363,7 +363,7 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
 
 size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
   if (!c || k < 1) return 0;
-  const size_t fused = (size_t)c->blocks_tma * (size_t)k * sizeof(ls_elite_rec) + (size_t)c->blocks_tma * 4 + 16;
+  const size_t fused = (size_t)c->blocks_tma * (size_t)k * sizeof(ls_elite_rec) + (size_t)c->blocks_tma * 4 + 32;
   return std::max(fused, topk_scratch_bytes(n, k, 0));
 }
 
@@ -393,16 +393,21 @@ int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_
   if (k <= fused_k_max() && c->blocks_tma > 0 && tma_eligible(a, c->M.A)) {
     LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
     const int64_t grid = ws_grid(lp, n);
-    TopkArgs tk{k, index_base, static_cast<ls_elite_rec*>(scratch), nullptr};
+    TopkArgs tk{k, index_base, static_cast<ls_elite_rec*>(scratch), nullptr, nullptr};
     tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
+    tk.floor = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(tk.part_counts + grid) + 7) & ~uintptr_t(7));
     if (n == 0) {
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
       return LS_OK;
     }
+    if ((e = cudaMemsetAsync(tk.floor, 0, sizeof(unsigned long long), s)) != cudaSuccess)
+      return cuda_fail(e, "floor reset");
     if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s)) !=
         cudaSuccess)
       return cuda_fail(e, "evaluate_topk launch");
-    if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, topk_out, count_out, s)) != cudaSuccess)
+    if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, tk.floor, topk_out, count_out, s)) !=
+        cudaSuccess)
       return cuda_fail(e, "topk merge launch");
     return LS_OK;
   }
@@ -424,7 +429,8 @@ int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_
   g_err.clear();
   if (!recs || !counts || m < 1 || k_in < 1 || k_in > 64 || k < 1 || k > 64 || !out || !count_out)
     return fail(LS_ERR_INVALID_ARGUMENT, "bad topk_merge arguments");
-  cudaError_t e = launch_topk_merge(recs, counts, m, k_in, k, out, count_out, static_cast<cudaStream_t>(stream));
+  cudaError_t e =
+      launch_topk_merge(recs, counts, m, k_in, k, nullptr, out, count_out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge launch");
 }
 

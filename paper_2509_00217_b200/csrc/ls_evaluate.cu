@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   int qcount = 0;  // warp-uniform
   WarpList wl;
   if (TOPK) wl.bind(lists + warp * warp_list_bytes(kFusedK), kFusedK, &list_count[warp]);
+  double gfloor = -1.0e308;  // cached global pruning floor (raw keys are >= 0)
   if (SMEM_GATE) mbar_wait(&gate_bar, 0);
 
   // fp64 pass over the 32 newest queue entries (or the first n < 32 at the end)
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     if (TOPK) {  // fused elite: valid survivors offered to the warp's top-k list
       Rec r{v.thr, v.thr, tk.index_base + idx, 0};
-      const bool ok = lane < n && v.reason == LS_REASON_NONE && wl.admits(r.key, r.idx, tk.k);
+      const bool ok = lane < n && v.reason == LS_REASON_NONE && r.key >= gfloor && wl.admits(r.key, r.idx, tk.k);
       if (ok) {
         uint64_t code = (uint64_t)c.t * M.code_stride[0] + (uint64_t)c.e * M.code_stride[1] +
                         (uint64_t)c.p * M.code_stride[2] + (uint64_t)c.b * M.code_stride[3];
@@ -213,6 +214,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         r.code = code;
       }
       wl.offer(ok, r, tk.k);
+      if (__any_sync(0xffffffffu, ok)) {  // list may have moved: share / refresh the pruning floor
+        const double mine = wl.floor_key(tk.k);
+        if (lane == 0 && mine > gfloor) raise_floor(tk.floor, mine);
+        gfloor = fmax(mine, read_floor(tk.floor));
+      }
     }
     qcount -= n;
     __syncwarp();

@@ -31,6 +31,7 @@ struct TopkArgs {
   int64_t index_base;
   ls_elite_rec* part;
   int32_t* part_counts;
+  unsigned long long* floor;  // device word, zeroed before launch
 };
 
 bool tma_eligible(const EvalArgs& a, int A);
@@ -61,6 +62,7 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
                         const double* thr, const double* key, int64_t n, int k, int64_t index_base,
                         ls_elite_rec* out, int32_t* count_out, void* scratch, int num_sms, cudaStream_t s);
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
+                              const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);
 
 }  // namespace ls

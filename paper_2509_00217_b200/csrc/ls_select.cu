@@ -215,28 +215,39 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(const TopkMeta
 // Merge m lists of up to k_in records each into one list of k. One CTA.
 __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite_rec* __restrict__ recs,
                                                                   const int32_t* __restrict__ counts, int m, int k_in,
-                                                                  int k, ls_elite_rec* __restrict__ out,
+                                                                  int k, const unsigned long long* floor,
+                                                                  ls_elite_rec* __restrict__ out,
                                                                   int32_t* __restrict__ count_out) {
   __shared__ TopkSmem s;
+  __shared__ unsigned long long s_floor;  // CTA-wide pruning floor (raw-keyed merges only)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_floor = 0;
   if (lane == 0) s.count[w] = 0;
-  __syncwarp();
+  __syncthreads();
   WarpList wl;
   wl.bind(s.lists[w], 64, &s.count[w]);
+  double fl = floor ? read_floor(floor) : -1.0e308;
   for (int list = w; list < m; list += kTopkWarps) {
     const int cnt = min(counts[list], k_in);
     for (int j0 = 0; j0 < cnt; j0 += 32) {
       const int j = j0 + lane;
-      const bool have = j < cnt;
       Rec r{0.0, 0.0, 0, 0};
+      bool have = j < cnt;
       if (have) {
         const ls_elite_rec& e = recs[(int64_t)list * k_in + j];
         r.key = e.key;
         r.raw = e.raw;
         r.idx = e.index;
         r.code = e.code;
+        have = r.key >= fl;
       }
+      if (!__any_sync(0xffffffffu, have)) break;  // lists are sorted: the rest is below the floor
       wl.offer(have, r, k);
+      if (floor) {
+        const double mine = wl.floor_key(k);
+        if (lane == 0 && mine > fl) raise_floor(&s_floor, mine);
+        fl = fmax(fl, fmax(mine, read_floor(&s_floor)));
+      }
     }
   }
   __syncthreads();
@@ -296,13 +307,14 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
   int32_t* counts = reinterpret_cast<int32_t*>(part + (size_t)c * k);
   topk_local_kernel<<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k, index_base,
                                                part, counts);
-  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(part, counts, c, k, k, out, count_out);
+  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
+                              const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s) {
-  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, out, count_out);
+  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
   return cudaGetLastError();
 }
 

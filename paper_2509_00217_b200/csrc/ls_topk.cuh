@@ -114,6 +114,10 @@ struct WarpList {
     return *count < k || better(k_, i_, key[k - 1], idx[k - 1]);
   }
 
+  // Key of the k-th entry once the list is full (else -inf): any record
+  // with a strictly smaller key is beaten by k distinct vectors already.
+  __device__ __forceinline__ double floor_key(int k) const { return *count < k ? -1.0e308 : key[k - 1]; }
+
   // Offer one record per lane (lanes with have == false offer nothing).
   __device__ void offer(bool have, const Rec& mine, int k) {
     const bool cand = have && admits(mine.key, mine.idx, k);
@@ -162,6 +166,19 @@ struct WarpList {
     if (lane == 0) *count_out = cnt;
   }
 };
+
+// Global pruning floor shared by every list of one reduction: the largest
+// k-th key any full list has reached. Keys are non-negative doubles (raw
+// throughput), whose IEEE bit patterns order like unsigned integers, so the
+// floor is an atomicMax on the bits. A record strictly below it cannot make
+// the final top-k (k distinct vectors beat it), for any arrival order.
+__device__ __forceinline__ void raise_floor(unsigned long long* floor, double k_) {
+  if (floor && k_ >= 0.0) atomicMax(floor, (unsigned long long)__double_as_longlong(k_));
+}
+__device__ __forceinline__ double read_floor(const unsigned long long* floor) {
+  if (!floor) return -1.0e308;
+  return __longlong_as_double((long long)*reinterpret_cast<const volatile unsigned long long*>(floor));
+}
 
 // Bytes of one WarpList of capacity cap.
 __host__ __device__ constexpr int warp_list_bytes(int cap) { return cap * 32; }

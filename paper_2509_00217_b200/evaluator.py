@@ -238,6 +238,11 @@ class Evaluator:
         if planes.device != self.device:
             raise ValueError(f"planes live on {planes.device}, evaluator on {self.device}")
         n, stride = self._check_planes(planes)
+        fused_ok = (planes.data_ptr() % 16 == 0 and stride % 16 == 0 and self.vector_length <= 16 and k <= 32)
+        if not verdicts and not fused_ok:
+            # the fused sweep needs TMA-aligned planes; otherwise evaluate, then reduce
+            out, recs, count = self.evaluate_topk(planes, k, index_base, None, ("throughput",), True)
+            return None, recs, count
         if verdicts and out is None:
             out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=self.device))
             for f in (FIELDS if fields == "all" else fields):
