@@ -1,22 +1,25 @@
 // ls_evaluate.cu — the batched strategy-evaluation kernels.
 //
 // eval_ws_kernel — the hot path (16-byte aligned SoA planes, A <= 16).
-// Persistent, warp-specialized CTAs (1 producer warp + 8 consumer warps):
-//   * the producer warp's elected lane bulk-copies (TMA, cp.async.bulk) the
+// Persistent, warp-specialized CTAs with three roles and no CTA-wide barrier
+// in the steady state:
+//   * producer warp — its elected lane bulk-copies (TMA, cp.async.bulk) the
 //     workload's gate tables into shared memory once, then keeps a 4-stage
 //     ring of 1024-candidate tiles in flight (one 1 KB slice per head plane
-//     per tile), synchronised only through full/empty mbarriers — no CTA-wide
-//     barrier in the steady state;
-//   * each consumer warp owns 128 candidates of a stage (4 per lane, one
-//     32-bit shared load per head plane), releases the stage, decodes the 4
+//     per tile), synchronised through full/empty mbarriers;
+//   * 8 gate warps — each owns 128 candidates of a stage (4 per lane, one
+//     32-bit shared load per head plane), releases the stage, decodes its 4
 //     candidates with SWAR byte arithmetic (range checks and the packed axis
-//     word for all 4 at once), and runs gate(): budget and layout bitmasks
-//     and the memory model. The ~98% of a uniform batch that is gated out is
-//     finished here with coalesced 32-bit / 128-bit stores;
-//   * survivors go to the warp's own shared-memory queue (ballot + popc);
-//     every time it holds a full warp's worth, the warp runs the fp64 cost
-//     model (full_path()) on 32 survivors at once — dense, no divergence
-//     between cheap and expensive candidates.
+//     word for all 4 at once) and runs gate(): budget and layout bitmasks and
+//     the memory model. The ~98% of a uniform batch that is gated out is
+//     finished here with coalesced 32-bit / 128-bit stores. Survivors are
+//     compacted into the warp's queue (ballot + popc) and handed off 32 at a
+//     time through a 2-slot shared-memory mailbox;
+//   * 2 fp64 warps — drain the mailboxes: the fp64 cost model (full_path())
+//     on 32 survivors at once, verdict stores, and (fused sweep) the offer to
+//     the warp's elite list. Gate warps never wait on fp64 latency; when a
+//     mailbox is full (survivor-heavy batches) the gate warp scores its own
+//     batch instead, so the pipeline degrades to compute-bound, never stalls.
 // eval_generic_kernel covers everything else (any alignment, A <= 64), one
 // candidate per thread.
 #include <cuda_runtime.h>
@@ -29,12 +32,15 @@ namespace ls {
 
 namespace {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = 32 * (kConsumerWarps + 1);
+constexpr int kGateWarps = 8;
+constexpr int kFpWarps = 2;
+constexpr int kWorkWarps = kGateWarps + kFpWarps;
+constexpr int kThreads = 32 * (kWorkWarps + 1);  // + producer warp
 constexpr int kWarpCands = 128;
-constexpr int kTile = kConsumerWarps * kWarpCands;  // candidates per stage
+constexpr int kTile = kGateWarps * kWarpCands;  // candidates per stage
 constexpr int kStages = 4;
 constexpr int kWarpQueue = 160;  // < 32 left over + 128 from one tile
+constexpr int kSlots = 2;        // mailbox slots per gate warp
 constexpr int kGenericThreads = 256;
 constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
 
@@ -131,6 +137,59 @@ __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, in
   c.Y = ((q[0] >> sh) & 0xffu) | (((q[1] >> sh) & 0xffu) << 8) | (((q[2] >> sh) & 0xffu) << 16);
 }
 
+// Dynamic shared memory of eval_ws_kernel: TMA ring, gate tables, per-gate
+// warp survivor queues, mailboxes and the work warps' elite lists.
+struct WsSmem {
+  uint8_t* ring;
+  uint64_t* gate;
+  uint64_t* qkey;  // [kGateWarps][kWarpQueue]
+  uint32_t* qy;
+  uint64_t* mkey;  // mailboxes [kGateWarps][kSlots][32]
+  uint32_t* my;
+  uint8_t* lists;  // [kWorkWarps] elite lists
+};
+
+inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
+  return (size_t)kStages * A * kTile + (smem_gate ? (size_t)gate_words * 8 : 0) +
+         (size_t)kGateWarps * kWarpQueue * 12 + (size_t)kGateWarps * kSlots * 32 * 12 +
+         (size_t)kWorkWarps * warp_list_bytes(kFusedK);
+}
+
+// fp64 pass over n <= 32 survivors (lane i takes entry i of keys/ys), with
+// verdict stores and the optional elite offer. Called by whole warps.
+template <bool NEU, bool FULL, bool TOPK>
+__device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, const TabLayout& L, const EvalMeta& M,
+                                        const EvalArgs& a, const TopkArgs& tk, const uint64_t* keys,
+                                        const uint32_t* ys, int n, WarpList& wl, double& gfloor) {
+  const int lane = threadIdx.x & 31;
+  int64_t idx = 0;
+  Decoded c;
+  Verdict v;
+  v.reason = LS_REASON_DECODE_ERROR;
+  v.thr = 0.0;
+  if (lane < n) {
+    unpack_key(keys[lane], ys[lane], idx, c);
+    full_path<NEU>(gtab, L, M, c, v);
+    if (a.reason) write_verdict<FULL>(a, idx, v);
+  }
+  if (TOPK) {  // fused elite: valid survivors offered to this warp's list
+    Rec r{v.thr, v.thr, tk.index_base + idx, 0};
+    const bool ok = lane < n && v.reason == LS_REASON_NONE && r.key >= gfloor && wl.admits(r.key, r.idx, tk.k);
+    if (ok) {
+      uint64_t code = (uint64_t)c.t * M.code_stride[0] + (uint64_t)c.e * M.code_stride[1] +
+                      (uint64_t)c.p * M.code_stride[2] + (uint64_t)c.b * M.code_stride[3];
+      for (int h = 4; h < M.A; ++h) code += (uint64_t)((c.Y >> (2 * (h - 4))) & 3u) * M.code_stride[h];
+      r.code = code;
+    }
+    wl.offer(ok, r, tk.k);
+    if (__any_sync(0xffffffffu, ok)) {  // the list may have moved: share / refresh the pruning floor
+      const double mine = wl.floor_key(tk.k);
+      if (lane == 0 && mine > gfloor) raise_floor(tk.floor, mine);
+      gfloor = fmax(mine, read_floor(tk.floor));
+    }
+  }
+}
+
 template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK>
 __global__ void __launch_bounds__(kThreads, 2)
     eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
@@ -139,22 +198,30 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
   __shared__ __align__(8) uint64_t gate_bar;
+  __shared__ int list_count[kWorkWarps];
+  __shared__ int mb_n[kGateWarps][kSlots];
+  __shared__ volatile int mb_state[kGateWarps][kSlots];  // 0 empty, 1 full
+  __shared__ volatile int gates_done;
   const int A = M.A;
   const uint32_t stage_bytes = (uint32_t)A * kTile;
-  uint8_t* ring = smem;
-  uint64_t* G = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
-  uint64_t* qkey_all = SMEM_GATE ? G + L.gate_words : G;
-  uint32_t* qy_all = reinterpret_cast<uint32_t*>(qkey_all + kConsumerWarps * kWarpQueue);
-  uint8_t* lists = reinterpret_cast<uint8_t*>(qy_all + kConsumerWarps * kWarpQueue);
-  __shared__ int list_count[kConsumerWarps];
-  const uint64_t* Gt = SMEM_GATE ? G : gtab;
+  WsSmem S;
+  S.ring = smem;
+  S.gate = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
+  S.qkey = SMEM_GATE ? S.gate + L.gate_words : S.gate;
+  S.qy = reinterpret_cast<uint32_t*>(S.qkey + kGateWarps * kWarpQueue);
+  S.mkey = reinterpret_cast<uint64_t*>(S.qy + kGateWarps * kWarpQueue);
+  S.my = reinterpret_cast<uint32_t*>(S.mkey + kGateWarps * kSlots * 32);
+  S.lists = reinterpret_cast<uint8_t*>(S.my + kGateWarps * kSlots * 32);
+  const uint64_t* Gt = SMEM_GATE ? S.gate : gtab;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (TOPK && threadIdx.x < kConsumerWarps) list_count[threadIdx.x] = 0;
+  if (threadIdx.x < kWorkWarps) list_count[threadIdx.x] = 0;
+  if (threadIdx.x < kGateWarps * kSlots) mb_state[threadIdx.x / kSlots][threadIdx.x % kSlots] = 0;
   if (threadIdx.x == 0) {
+    gates_done = 0;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kConsumerWarps);
+      mbar_init(&empty_bar[s], kGateWarps);
     }
     mbar_init(&gate_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -162,11 +229,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {  // ---------------- producer warp
+  if (warp == kWorkWarps) {  // ---------------- producer warp
     if (lane == 0) {
       if (SMEM_GATE) {
         mbar_expect_tx(&gate_bar, (uint32_t)L.gate_words * 8u);
-        bulk_g2s(G, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
+        bulk_g2s(S.gate, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
       }
       int i = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
@@ -174,151 +241,183 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
         mbar_expect_tx(&full_bar[s], stage_bytes);
         const uint8_t* src = a.planes + tile * kTile;
-        uint8_t* dst = ring + s * stage_bytes;
+        uint8_t* dst = S.ring + s * stage_bytes;
         for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
       }
     }
     return;
   }
 
-  // ---------------- consumer warps
-  uint64_t* qkey = qkey_all + warp * kWarpQueue;
-  uint32_t* qy = qy_all + warp * kWarpQueue;
-  int qcount = 0;  // warp-uniform
   WarpList wl;
-  if (TOPK) wl.bind(lists + warp * warp_list_bytes(kFusedK), kFusedK, &list_count[warp]);
+  if (TOPK) wl.bind(S.lists + warp * warp_list_bytes(kFusedK), kFusedK, &list_count[warp]);
   double gfloor = -1.0e308;  // cached global pruning floor (raw keys are >= 0)
-  if (SMEM_GATE) mbar_wait(&gate_bar, 0);
 
-  // fp64 pass over the 32 newest queue entries (or the first n < 32 at the end)
-  auto drain = [&](int n) {
-    __syncwarp();
-    int64_t idx = 0;
-    Decoded c;
-    Verdict v;
-    v.reason = LS_REASON_DECODE_ERROR;
-    v.thr = 0.0;
-    if (lane < n) {
-      const int pos = qcount - n + lane;
-      unpack_key(qkey[pos], qy[pos], idx, c);
-      full_path<NEU>(gtab, L, M, c, v);
-      if (a.reason) write_verdict<FULL>(a, idx, v);
-    }
-    if (TOPK) {  // fused elite: valid survivors offered to the warp's top-k list
-      Rec r{v.thr, v.thr, tk.index_base + idx, 0};
-      const bool ok = lane < n && v.reason == LS_REASON_NONE && r.key >= gfloor && wl.admits(r.key, r.idx, tk.k);
-      if (ok) {
-        uint64_t code = (uint64_t)c.t * M.code_stride[0] + (uint64_t)c.e * M.code_stride[1] +
-                        (uint64_t)c.p * M.code_stride[2] + (uint64_t)c.b * M.code_stride[3];
-        for (int h = 4; h < M.A; ++h) code += (uint64_t)((c.Y >> (2 * (h - 4))) & 3u) * M.code_stride[h];
-        r.code = code;
-      }
-      wl.offer(ok, r, tk.k);
-      if (__any_sync(0xffffffffu, ok)) {  // list may have moved: share / refresh the pruning floor
-        const double mine = wl.floor_key(tk.k);
-        if (lane == 0 && mine > gfloor) raise_floor(tk.floor, mine);
-        gfloor = fmax(mine, read_floor(tk.floor));
-      }
-    }
-    qcount -= n;
-    __syncwarp();
-  };
-
-  // gate pass over the 4 candidates of this lane starting at `base`
-  auto pass_a = [&](const uint32_t* w, int64_t base, int count) {
-    uint32_t q[3];
-    const uint32_t badb = swar_decode(w, M, q);
-    uint32_t r4 = 0;
-    double m[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      Decoded c;
-      extract(w, q, j, c);
-      double mem = 0.0;
-      uint32_t reason = LS_REASON_DECODE_ERROR;
-      if (((badb >> (8 * j)) & 0xffu) == 0) reason = gate(Gt, L, M, c, mem);
-      const bool surv = j < count && reason == LS_REASON_NONE;
-      const unsigned mask = __ballot_sync(0xffffffffu, surv);
-      if (surv) {
-        const int pos = qcount + __popc(mask & ((1u << lane) - 1u));
-        qkey[pos] = pack_key(base + j, c);
-        qy[pos] = c.Y;
-      }
-      qcount += __popc(mask);
-      r4 |= reason << (8 * j);
-      m[j] = mem;
-    }
-    if (!a.reason) {
-      // sweep mode: no per-candidate verdicts, only the fused elite
-    } else if (count == 4) {
-      *reinterpret_cast<uint32_t*>(a.reason + base) = r4;
-      if (a.thr) {
-        st2(a.thr, base, 0.0, 0.0);
-        st2(a.thr, base + 2, 0.0, 0.0);
-      }
-      if (FULL) {
-        if (a.mem) {
-          st2(a.mem, base, m[0], m[1]);
-          st2(a.mem, base + 2, m[2], m[3]);
-        }
-        double* zf[4] = {a.tpot, a.comp, a.comm, a.pipe};
-#pragma unroll
-        for (int f = 0; f < 4; ++f)
-          if (zf[f]) {
-            st2(zf[f], base, 0.0, 0.0);
-            st2(zf[f], base + 2, 0.0, 0.0);
+  if (warp >= kGateWarps) {  // ---------------- fp64 warps: drain the mailboxes
+    const int f = warp - kGateWarps;
+    for (;;) {
+      bool found = false;
+      for (int g = f; g < kGateWarps; g += kFpWarps) {
+        for (int sl = 0; sl < kSlots; ++sl) {
+          if (mb_state[g][sl] != 1) continue;
+          __threadfence_block();
+          found = true;
+          const int base = (g * kSlots + sl) * 32;
+          fp64_batch<NEU, FULL, TOPK>(gtab, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl, gfloor);
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            mb_state[g][sl] = 0;
           }
+          __syncwarp();
+        }
       }
-    } else {
-      for (int j = 0; j < count; ++j) {
-        a.reason[base + j] = (uint8_t)(r4 >> (8 * j));
-        if (a.thr) a.thr[base + j] = 0.0;
-        if (FULL) {
-          if (a.mem) a.mem[base + j] = m[j];
-          if (a.tpot) a.tpot[base + j] = 0.0;
-          if (a.comp) a.comp[base + j] = 0.0;
-          if (a.comm) a.comm[base + j] = 0.0;
-          if (a.pipe) a.pipe[base + j] = 0.0;
+      if (!found) {
+        if (gates_done == kGateWarps) {
+          __threadfence_block();
+          bool any = false;  // gate warps finished: one last sweep of the slots
+          for (int g = f; g < kGateWarps; g += kFpWarps)
+            for (int sl = 0; sl < kSlots; ++sl) any |= mb_state[g][sl] == 1;
+          if (!any) break;
+        } else {
+          __nanosleep(128);
         }
       }
     }
-    while (qcount >= 32) drain(32);
-  };
+  } else {  // ---------------- gate warps
+    uint64_t* qkey = S.qkey + warp * kWarpQueue;
+    uint32_t* qy = S.qy + warp * kWarpQueue;
+    int qcount = 0;  // warp-uniform
+    if (SMEM_GATE) mbar_wait(&gate_bar, 0);
 
-  const int lane_off = warp * kWarpCands + 4 * lane;
-  int i = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-    const int s = i % kStages;
-    mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
-    uint32_t w[16];
-    const uint8_t* st = ring + s * stage_bytes + lane_off;
+    // hand the newest n (<= 32) queue entries to a free mailbox slot, or
+    // score them here when both slots are still busy
+    auto flush = [&](int n) {
+      __syncwarp();
+      const int pos0 = qcount - n;
+      int slot = -1;
+      for (int sl = 0; sl < kSlots && slot < 0; ++sl)
+        if (mb_state[warp][sl] == 0) slot = sl;
+      if (slot >= 0) {
+        __threadfence_block();
+        const int base = (warp * kSlots + slot) * 32;
+        if (lane < n) {
+          S.mkey[base + lane] = qkey[pos0 + lane];
+          S.my[base + lane] = qy[pos0 + lane];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mb_n[warp][slot] = n;
+          __threadfence_block();
+          mb_state[warp][slot] = 1;
+        }
+      } else {
+        fp64_batch<NEU, FULL, TOPK>(gtab, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor);
+      }
+      qcount -= n;
+      __syncwarp();
+    };
+
+    auto pass_a = [&](const uint32_t* w, int64_t base, int count) {
+      uint32_t q[3];
+      const uint32_t badb = swar_decode(w, M, q);
+      uint32_t r4 = 0;
+      double m[4];
 #pragma unroll
-    for (int h = 0; h < 16; ++h) w[h] = h < A ? *reinterpret_cast<const uint32_t*>(st + h * kTile) : 0u;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
-    pass_a(w, tile * kTile + lane_off, 4);
-  }
-  // ragged tail (< one tile): the CTA that would own the next tile
-  const int64_t tail0 = ntiles * kTile;
-  if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
-    const int64_t base = tail0 + lane_off;
-    const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
-    uint32_t w[16];
+      for (int j = 0; j < 4; ++j) {
+        Decoded c;
+        extract(w, q, j, c);
+        double mem = 0.0;
+        uint32_t reason = LS_REASON_DECODE_ERROR;
+        if (((badb >> (8 * j)) & 0xffu) == 0) reason = gate(Gt, L, M, c, mem);
+        const bool surv = j < count && reason == LS_REASON_NONE;
+        const unsigned mask = __ballot_sync(0xffffffffu, surv);
+        if (surv) {
+          const int pos = qcount + __popc(mask & ((1u << lane) - 1u));
+          qkey[pos] = pack_key(base + j, c);
+          qy[pos] = c.Y;
+        }
+        qcount += __popc(mask);
+        r4 |= reason << (8 * j);
+        m[j] = mem;
+      }
+      if (!a.reason) {
+        // sweep mode: no per-candidate verdicts, only the fused elite
+      } else if (count == 4) {
+        *reinterpret_cast<uint32_t*>(a.reason + base) = r4;
+        if (a.thr) {
+          st2(a.thr, base, 0.0, 0.0);
+          st2(a.thr, base + 2, 0.0, 0.0);
+        }
+        if (FULL) {
+          if (a.mem) {
+            st2(a.mem, base, m[0], m[1]);
+            st2(a.mem, base + 2, m[2], m[3]);
+          }
+          double* zf[4] = {a.tpot, a.comp, a.comm, a.pipe};
 #pragma unroll
-    for (int h = 0; h < 16; ++h) {
-      w[h] = 0;
-      if (h < A)
-        for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
+          for (int f = 0; f < 4; ++f)
+            if (zf[f]) {
+              st2(zf[f], base, 0.0, 0.0);
+              st2(zf[f], base + 2, 0.0, 0.0);
+            }
+        }
+      } else {
+        for (int j = 0; j < count; ++j) {
+          a.reason[base + j] = (uint8_t)(r4 >> (8 * j));
+          if (a.thr) a.thr[base + j] = 0.0;
+          if (FULL) {
+            if (a.mem) a.mem[base + j] = m[j];
+            if (a.tpot) a.tpot[base + j] = 0.0;
+            if (a.comp) a.comp[base + j] = 0.0;
+            if (a.comm) a.comm[base + j] = 0.0;
+            if (a.pipe) a.pipe[base + j] = 0.0;
+          }
+        }
+      }
+      while (qcount >= 32) flush(32);
+    };
+
+    const int lane_off = warp * kWarpCands + 4 * lane;
+    int i = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      const int s = i % kStages;
+      mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
+      uint32_t w[16];
+      const uint8_t* st = S.ring + s * stage_bytes + lane_off;
+#pragma unroll
+      for (int h = 0; h < 16; ++h) w[h] = h < A ? *reinterpret_cast<const uint32_t*>(st + h * kTile) : 0u;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+      pass_a(w, tile * kTile + lane_off, 4);
     }
-    pass_a(w, base, count);
+    // ragged tail (< one tile): the CTA that would own the next tile
+    const int64_t tail0 = ntiles * kTile;
+    if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
+      const int64_t base = tail0 + lane_off;
+      const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+      uint32_t w[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        w[h] = 0;
+        if (h < A)
+          for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
+      }
+      pass_a(w, base, count);
+    }
+    if (qcount > 0) flush(qcount);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd((int*)&gates_done, 1);
+    }
   }
-  if (qcount > 0) drain(qcount);
-  if (TOPK) {  // merge the consumer warps' lists (named barrier: the producer warp is gone)
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+
+  if (TOPK) {  // merge the work warps' lists (named barrier: the producer warp is gone)
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
     if (warp == 0) {
-      for (int o = 1; o < kConsumerWarps; ++o) {
+      for (int o = 1; o < kWorkWarps; ++o) {
         WarpList other;
-        other.bind(lists + o * warp_list_bytes(kFusedK), kFusedK, &list_count[o]);
+        other.bind(S.lists + o * warp_list_bytes(kFusedK), kFusedK, &list_count[o]);
         wl.absorb(other, tk.k);
       }
       wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
@@ -371,12 +470,34 @@ void set_attr(size_t smem) {
   cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+template <bool NEU, bool FULL, bool TOPK>
+void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, const EvalArgs& a,
+                 const TopkArgs& tk, cudaStream_t s) {
+  const int64_t ntiles = a.n / kTile;
+  const size_t smem = ws_dynamic_bytes(M.A, L.gate_words, lp.smem_gate);
+  int64_t blocks = ntiles > 0 ? ntiles : 1;
+  if (blocks > lp.max_blocks) blocks = lp.max_blocks;
+  if (lp.smem_gate)
+    eval_ws_kernel<NEU, FULL, true, TOPK><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
+  else
+    eval_ws_kernel<NEU, FULL, false, TOPK><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
+}
+
+template <bool TOPK>
+void launch_ws(const LaunchPlan& lp, bool neumaier, bool full, const uint64_t* tab, const TabLayout& L,
+               const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
+  if (neumaier) {
+    if (full) launch_ws_t<true, true, TOPK>(lp, tab, L, M, a, tk, s);
+    else launch_ws_t<true, false, TOPK>(lp, tab, L, M, a, tk, s);
+  } else {
+    if (full) launch_ws_t<false, true, TOPK>(lp, tab, L, M, a, tk, s);
+    else launch_ws_t<false, false, TOPK>(lp, tab, L, M, a, tk, s);
+  }
+}
+
 }  // namespace
 
-size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) {
-  return (size_t)kStages * A * kTile + (smem_gate ? (size_t)L.gate_words * 8 : 0) +
-         (size_t)kConsumerWarps * kWarpQueue * 12 + (size_t)kConsumerWarps * warp_list_bytes(kFusedK);
-}
+size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) { return ws_dynamic_bytes(A, L.gate_words, smem_gate); }
 
 bool tma_eligible(const EvalArgs& a, int A) {
   const bool al16 = ((uintptr_t)a.planes % 16) == 0 && a.stride % 16 == 0;
@@ -416,30 +537,6 @@ int generic_blocks_per_sm() {
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_generic_kernel<true>, kGenericThreads, 0);
   return nb;
-}
-
-template <bool NEU, bool FULL, bool TOPK>
-static void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
-                        const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
-  const int64_t ntiles = a.n / kTile;
-  const size_t smem = tma_smem_bytes(L, M.A, lp.smem_gate);
-  const unsigned blocks = (unsigned)ws_grid(lp, a.n);
-  if (lp.smem_gate)
-    eval_ws_kernel<NEU, FULL, true, TOPK><<<blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
-  else
-    eval_ws_kernel<NEU, FULL, false, TOPK><<<blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
-}
-
-template <bool TOPK>
-static void launch_ws(const LaunchPlan& lp, bool neumaier, bool full, const uint64_t* tab, const TabLayout& L,
-                      const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
-  if (neumaier) {
-    if (full) launch_ws_t<true, true, TOPK>(lp, tab, L, M, a, tk, s);
-    else launch_ws_t<true, false, TOPK>(lp, tab, L, M, a, tk, s);
-  } else {
-    if (full) launch_ws_t<false, true, TOPK>(lp, tab, L, M, a, tk, s);
-    else launch_ws_t<false, false, TOPK>(lp, tab, L, M, a, tk, s);
-  }
 }
 
 int64_t ws_grid(const LaunchPlan& lp, int64_t n) {

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--dist", default="uniform")
     ap.add_argument("--fields", default="raw")
+    ap.add_argument("--topk", type=int, default=0, help="fused evaluate + elite of this size")
+    ap.add_argument("--no-verdicts", action="store_true")
     args = ap.parse_args()
     wl = load_workload(args.config)
     ev = Evaluator(wl, device=0)
@@ -40,7 +42,10 @@ def main():
     for _ in range(args.reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        ev.evaluate(planes, fields=fields, out=out)
+        if args.topk:
+            ev.evaluate_topk(planes, k=args.topk, out=out, verdicts=not args.no_verdicts)
+        else:
+            ev.evaluate(planes, fields=fields, out=out)
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b)
