@@ -43,9 +43,15 @@ constexpr int kWarpQueue = 160;  // < 32 left over + 128 from one tile
 constexpr int kSlots = 2;        // mailbox slots per gate warp
 constexpr int kGenericThreads = 256;
 constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
+constexpr uint32_t kStageBytes = 16 * kTile;  // 16 plane slices per stage (planes >= A stay zero)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -150,7 +156,7 @@ struct WsSmem {
 };
 
 inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
-  return (size_t)kStages * A * kTile + (smem_gate ? (size_t)gate_words * 8 : 0) +
+  return (size_t)kStages * kStageBytes + (smem_gate ? (size_t)gate_words * 8 : 0) +
          (size_t)kGateWarps * kWarpQueue * 12 + (size_t)kGateWarps * kSlots * 32 * 12 +
          (size_t)kWorkWarps * warp_list_bytes(kFusedK);
 }
@@ -203,10 +209,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ volatile int mb_state[kGateWarps][kSlots];  // 0 empty, 1 full
   __shared__ volatile int gates_done;
   const int A = M.A;
-  const uint32_t stage_bytes = (uint32_t)A * kTile;
+  const uint32_t stage_bytes = (uint32_t)A * kTile;  // bytes the producer copies per stage
   WsSmem S;
   S.ring = smem;
-  S.gate = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
+  S.gate = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   S.qkey = SMEM_GATE ? S.gate + L.gate_words : S.gate;
   S.qy = reinterpret_cast<uint32_t*>(S.qkey + kGateWarps * kWarpQueue);
   S.mkey = reinterpret_cast<uint64_t*>(S.qy + kGateWarps * kWarpQueue);
@@ -215,6 +221,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint64_t* Gt = SMEM_GATE ? S.gate : gtab;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  const uint32_t ring_base = smem_u32(S.ring);
+  // plane slices >= A are never written by the TMA: zero them once so the
+  // gate warps can load all 16 unconditionally (zero = in range, UNSHARDED)
+  for (int s = 0; s < kStages; ++s)
+    for (int o = A * kTile + 16 * (int)threadIdx.x; o < (int)kStageBytes; o += 16 * kThreads)
+      *reinterpret_cast<uint4*>(S.ring + s * kStageBytes + o) = make_uint4(0, 0, 0, 0);
   if (threadIdx.x < kWorkWarps) list_count[threadIdx.x] = 0;
   if (threadIdx.x < kGateWarps * kSlots) mb_state[threadIdx.x / kSlots][threadIdx.x % kSlots] = 0;
   if (threadIdx.x == 0) {
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
         mbar_expect_tx(&full_bar[s], stage_bytes);
         const uint8_t* src = a.planes + tile * kTile;
-        uint8_t* dst = S.ring + s * stage_bytes;
+        uint8_t* dst = S.ring + s * kStageBytes;
         for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
       }
     }
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp >= kGateWarps) {  // ---------------- fp64 warps: drain the mailboxes
     const int f = warp - kGateWarps;
+    unsigned backoff = 128;  // ns; idle fp64 warps back off so gate warps keep the issue slots
     for (;;) {
       bool found = false;
       for (int g = f; g < kGateWarps; g += kFpWarps) {
@@ -279,8 +292,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int sl = 0; sl < kSlots; ++sl) any |= mb_state[g][sl] == 1;
           if (!any) break;
         } else {
-          __nanosleep(128);
+          __nanosleep(backoff);
+          backoff = backoff < 4096 ? 2 * backoff : 4096;
         }
+      } else {
+        backoff = 128;
       }
     }
   } else {  // ---------------- gate warps
@@ -326,9 +342,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int j = 0; j < 4; ++j) {
         Decoded c;
         extract(w, q, j, c);
-        double mem = 0.0;
-        uint32_t reason = LS_REASON_DECODE_ERROR;
-        if (((badb >> (8 * j)) & 0xffu) == 0) reason = gate(Gt, L, M, c, mem);
+        const bool dbad = ((badb >> (8 * j)) & 0xffu) != 0;
+        if (dbad) c.t = c.e = c.p = c.b = 0;  // keep the branch-free lookups in range
+        double mem;
+        uint32_t reason = gate_bf(Gt, L, M, c, mem);
+        if (dbad) {
+          reason = LS_REASON_DECODE_ERROR;
+          mem = 0.0;
+        }
         const bool surv = j < count && reason == LS_REASON_NONE;
         const unsigned mask = __ballot_sync(0xffffffffu, surv);
         if (surv) {
@@ -383,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int s = i % kStages;
       mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
       uint32_t w[16];
-      const uint8_t* st = S.ring + s * stage_bytes + lane_off;
+      const uint32_t st = ring_base + (uint32_t)s * kStageBytes + (uint32_t)lane_off;
 #pragma unroll
-      for (int h = 0; h < 16; ++h) w[h] = h < A ? *reinterpret_cast<const uint32_t*>(st + h * kTile) : 0u;
+      for (int h = 0; h < 16; ++h) w[h] = lds_u32(st + h * kTile);  // planes >= A are zero-filled
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
       pass_a(w, tile * kTile + lane_off, 4);

@@ -115,6 +115,29 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
   return LS_REASON_NONE;
 }
 
+// Branch-free gate() for the SWAR pass: every table lookup is issued
+// unconditionally (indices already in range — decode-failed candidates are
+// clamped by the caller) and the reason is selected in gate order, so a warp
+// never diverges on which gate fired. mem is 0 unless the memory gate ran,
+// matching SimResult's field conventions (simulator.py:246-255, :281-284).
+__device__ __forceinline__ uint32_t gate_bf(const uint64_t* G, const TabLayout& L, const EvalMeta& M, const Decoded& c,
+                                            double& mem) {
+  const uint4 te = *reinterpret_cast<const uint4*>(G + L.te + 2 * (c.t * L.ne + c.e));
+  const uint4 tm = *reinterpret_cast<const uint4*>(G + L.tmask + 2 * c.t);
+  const int a2 = (M.attn_src >= 0 ? (int)((c.Y >> M.attn_src) & 3u) : M.attn_pin) == 2;
+  const double m = (dget(G, L.mem_w + (c.t * L.ne + c.e) * L.np + c.p) +
+                    dget(G, L.mem_kv + ((a2 * L.nt + c.t) * L.np + c.p) * L.nb + c.b)) +
+                   dget(G, L.mem_ws + c.b);
+  const uint32_t over = (c.p < 32 ? te.x >> c.p : te.y >> (c.p - 32)) & 1u;
+  const uint32_t lay = (c.p < 32 ? te.z >> c.p : te.w >> (c.p - 32)) & 1u;
+  const uint32_t lo = c.Y & 0x555555u, hi = (c.Y >> 1) & 0x555555u;
+  const uint32_t bad = (~(lo | hi) & 0x555555u & tm.x) | (lo & ~hi & tm.y) | (hi & ~lo & tm.z) | tm.w | lay;
+  const uint32_t reason = over ? LS_REASON_OVER_DEVICE_BUDGET
+                               : (bad ? LS_REASON_LAYOUT_ERROR : (m > M.hbm_capacity ? LS_REASON_OOM : LS_REASON_NONE));
+  mem = (over | bad) ? 0.0 : m;
+  return reason;
+}
+
 // fp64 pass for a candidate that passed gate(). T: the full table (global).
 template <bool NEU>
 __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,

@@ -227,27 +227,29 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite
   WarpList wl;
   wl.bind(s.lists[w], 64, &s.count[w]);
   double fl = floor ? read_floor(floor) : -1.0e308;
-  for (int list = w; list < m; list += kTopkWarps) {
-    const int cnt = min(counts[list], k_in);
-    for (int j0 = 0; j0 < cnt; j0 += 32) {
-      const int j = j0 + lane;
-      Rec r{0.0, 0.0, 0, 0};
-      bool have = j < cnt;
-      if (have) {
-        const ls_elite_rec& e = recs[(int64_t)list * k_in + j];
+  // records flattened across lists, 32 per warp step: independent loads, so
+  // the single CTA is bound by a few L2 round trips, not by m sequential lists
+  const int total = m * k_in;
+  for (int base = w * 32; base < total; base += kTopkWarps * 32) {
+    const int i = base + lane;
+    Rec r{0.0, 0.0, 0, 0};
+    bool have = false;
+    if (i < total) {
+      const int list = i / k_in, j = i - list * k_in;
+      if (j < counts[list]) {
+        const ls_elite_rec& e = recs[i];
         r.key = e.key;
         r.raw = e.raw;
         r.idx = e.index;
         r.code = e.code;
         have = r.key >= fl;
       }
-      if (!__any_sync(0xffffffffu, have)) break;  // lists are sorted: the rest is below the floor
-      wl.offer(have, r, k);
-      if (floor) {
-        const double mine = wl.floor_key(k);
-        if (lane == 0 && mine > fl) raise_floor(&s_floor, mine);
-        fl = fmax(fl, fmax(mine, read_floor(&s_floor)));
-      }
+    }
+    wl.offer(have, r, k);
+    if (floor) {
+      const double mine = wl.floor_key(k);
+      if (lane == 0 && mine > fl) raise_floor(&s_floor, mine);
+      fl = fmax(fl, fmax(mine, read_floor(&s_floor)));
     }
   }
   __syncthreads();

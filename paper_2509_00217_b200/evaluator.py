@@ -207,8 +207,8 @@ class Evaluator:
         n, stride = self._check_planes(planes)
         if key is None:
             key = throughput
-        recs = torch.zeros((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
-        count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.empty(1, dtype=torch.int32, device=self.device)
         scratch = torch.empty(int(self._lib.ls_topk_scratch_bytes(n, k)), dtype=torch.uint8, device=self.device)
         check(self._lib.ls_topk(self._ctx, _ptr(planes), stride, _ptr(reason), _ptr(throughput), _ptr(key), n, int(k),
                                 int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), self._stream()))
@@ -248,8 +248,8 @@ class Evaluator:
             for f in (FIELDS if fields == "all" else fields):
                 setattr(out, f, torch.empty(n, dtype=torch.float64, device=self.device))
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
-        recs = torch.zeros((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
-        count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.empty(1, dtype=torch.int32, device=self.device)
         nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
         if self._scratch is None or self._scratch.numel() < nbytes:
             self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -261,8 +261,8 @@ class Evaluator:
     def merge_records(self, recs: torch.Tensor, counts: torch.Tensor, k_in: int, k: int):
         """Merge m stacked record lists ([m*k_in, 32] bytes, counts [m]) into one top-k."""
         m = counts.shape[0]
-        out = torch.zeros((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
-        count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        out = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.empty(1, dtype=torch.int32, device=self.device)
         check(self._lib.ls_topk_merge(_ptr(recs), _ptr(counts), m, int(k_in), int(k), _ptr(out), _ptr(count),
                                       self._stream()))
         return out, count
