@@ -436,10 +436,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (TOPK) {  // merge the work warps' lists (named barrier: the producer warp is gone)
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
     if (warp == 0) {
+      const double fl = read_floor(tk.floor);  // global floor so far: most entries are already beaten
       for (int o = 1; o < kWorkWarps; ++o) {
         WarpList other;
         other.bind(S.lists + o * warp_list_bytes(kFusedK), kFusedK, &list_count[o]);
-        wl.absorb(other, tk.k);
+        wl.absorb(other, tk.k, fl);
       }
       wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
     }

@@ -134,14 +134,15 @@ struct WarpList {
     }
   }
 
-  // Offer every record of another list (any order is exact).
-  __device__ void absorb(const WarpList& o, int k) {
+  // Offer every record of another list (any order is exact). Records with a
+  // key strictly below `floor` are skipped: k distinct vectors beat them.
+  __device__ void absorb(const WarpList& o, int k, double floor = -1.0e308) {
     const int lane = threadIdx.x & 31;
     const int cnt = *o.count;
     for (int j0 = 0; j0 < cnt; j0 += 32) {
       const int j = j0 + lane;
       Rec r{0.0, 0.0, 0, 0};
-      const bool have = j < cnt;
+      const bool have = j < cnt && o.key[j] >= floor;
       if (have) {
         r.key = o.key[j];
         r.raw = o.raw[j];
