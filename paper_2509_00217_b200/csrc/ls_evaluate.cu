@@ -166,7 +166,7 @@ inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
 template <bool NEU, bool FULL, bool TOPK>
 __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, const TabLayout& L, const EvalMeta& M,
                                         const EvalArgs& a, const TopkArgs& tk, const uint64_t* keys,
-                                        const uint32_t* ys, int n, WarpList& wl, double& gfloor) {
+                                        const uint32_t* ys, int n, RegList& wl, double& gfloor) {
   const int lane = threadIdx.x & 31;
   int64_t idx = 0;
   Decoded c;
@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     return;
   }
 
-  WarpList wl;
-  if (TOPK) wl.bind(S.lists + warp * warp_list_bytes(kFusedK), kFusedK, &list_count[warp]);
+  RegList wl;  // this warp's elite list, one entry per lane
+  wl.init();
   double gfloor = -1.0e308;  // cached global pruning floor (raw keys are >= 0)
 
   if (warp >= kGateWarps) {  // ---------------- fp64 warps: drain the mailboxes
@@ -434,14 +434,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 
   if (TOPK) {  // merge the work warps' lists (named barrier: the producer warp is gone)
+    Rec* slots = reinterpret_cast<Rec*>(S.lists);
+    wl.store(slots + warp * 32, &list_count[warp]);
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
     if (warp == 0) {
       const double fl = read_floor(tk.floor);  // global floor so far: most entries are already beaten
-      for (int o = 1; o < kWorkWarps; ++o) {
-        WarpList other;
-        other.bind(S.lists + o * warp_list_bytes(kFusedK), kFusedK, &list_count[o]);
-        wl.absorb(other, tk.k, fl);
-      }
+      for (int o = 1; o < kWorkWarps; ++o) wl.absorb(slots + o * 32, list_count[o], tk.k, fl);
       wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
     }
   }

@@ -143,10 +143,39 @@ constexpr int kTopkThreads = 256;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kTopkPerLane = 16;  // candidates per lane per chunk (one 16-byte reason load)
 
+// Per-warp list storage: RegList (k <= 32, registers) or WarpList (k <= 64,
+// shared memory); both merge across warps through Rec slots.
 struct TopkSmem {
-  double lists[kTopkWarps][4 * 64];
+  double lists[kTopkWarps][4 * 64];  // WarpList storage (k > 32 only)
+  Rec slots[kTopkWarps][64];         // cross-warp merge
   int count[kTopkWarps];
+  int slot_count[kTopkWarps];
 };
+
+template <class List>
+__device__ __forceinline__ void list_init(List& l, TopkSmem& s, int w);
+template <>
+__device__ __forceinline__ void list_init<RegList>(RegList& l, TopkSmem&, int) {
+  l.init();
+}
+template <>
+__device__ __forceinline__ void list_init<WarpList>(WarpList& l, TopkSmem& s, int w) {
+  if ((threadIdx.x & 31) == 0) s.count[w] = 0;
+  __syncwarp();
+  l.bind(s.lists[w], 64, &s.count[w]);
+}
+
+// Merge the CTA's warp lists into warp 0's and write it out.
+template <class List>
+__device__ void merge_and_emit(List& l, TopkSmem& s, int k, double floor, ls_elite_rec* out, int32_t* count_out) {
+  const int w = threadIdx.x >> 5;
+  l.store(s.slots[w], &s.slot_count[w]);
+  __syncthreads();
+  if (w == 0) {
+    for (int o = 1; o < kTopkWarps; ++o) l.absorb(s.slots[o], s.slot_count[o], k, floor);
+    l.emit(out, count_out);
+  }
+}
 
 __device__ __forceinline__ uint64_t vector_code(const TopkMeta& tm, const uint8_t* planes, int64_t stride, int64_t i) {
   uint64_t c = 0;
@@ -155,6 +184,7 @@ __device__ __forceinline__ uint64_t vector_code(const TopkMeta& tm, const uint8_
 }
 
 // Per-CTA top-k of valid candidates over a contiguous slice of the batch.
+template <class List>
 __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(const TopkMeta tm, const uint8_t* __restrict__ planes,
                                                                   int64_t stride, const uint8_t* __restrict__ reason,
                                                                   const double* __restrict__ thr,
@@ -163,10 +193,8 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(const TopkMeta
                                                                   int32_t* __restrict__ counts) {
   __shared__ TopkSmem s;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) s.count[w] = 0;
-  __syncwarp();
-  WarpList wl;
-  wl.bind(s.lists[w], 64, &s.count[w]);
+  List wl;
+  list_init(wl, s, w);
   const int64_t chunk = 32 * kTopkPerLane;
   const int64_t nchunks = (n + chunk - 1) / chunk;
   const bool vec = ((uintptr_t)reason % 16) == 0;
@@ -201,31 +229,24 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(const TopkMeta
       wl.offer(have, r, k);
     }
   }
-  __syncthreads();
-  if (w == 0) {
-    for (int o = 1; o < kTopkWarps; ++o) {
-      WarpList other;
-      other.bind(s.lists[o], 64, &s.count[o]);
-      wl.absorb(other, k);
-    }
-    wl.emit(out + (int64_t)blockIdx.x * k, counts + blockIdx.x);
-  }
+  merge_and_emit(wl, s, k, -1.0e308, out + (int64_t)blockIdx.x * k, counts + blockIdx.x);
 }
 
 // Merge m lists of up to k_in records each into one list of k. One CTA.
+// `floor` (raw-keyed reductions only) prunes records k distinct vectors beat.
+template <class List>
 __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite_rec* __restrict__ recs,
                                                                   const int32_t* __restrict__ counts, int m, int k_in,
                                                                   int k, const unsigned long long* floor,
                                                                   ls_elite_rec* __restrict__ out,
                                                                   int32_t* __restrict__ count_out) {
   __shared__ TopkSmem s;
-  __shared__ unsigned long long s_floor;  // CTA-wide pruning floor (raw-keyed merges only)
+  __shared__ unsigned long long s_floor;  // CTA-wide pruning floor
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_floor = 0;
-  if (lane == 0) s.count[w] = 0;
   __syncthreads();
-  WarpList wl;
-  wl.bind(s.lists[w], 64, &s.count[w]);
+  List wl;
+  list_init(wl, s, w);
   double fl = floor ? read_floor(floor) : -1.0e308;
   // records flattened across lists, 32 per warp step: independent loads, so
   // the single CTA is bound by a few L2 round trips, not by m sequential lists
@@ -252,15 +273,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite
       fl = fmax(fl, fmax(mine, read_floor(&s_floor)));
     }
   }
-  __syncthreads();
-  if (w == 0) {
-    for (int o = 1; o < kTopkWarps; ++o) {
-      WarpList other;
-      other.bind(s.lists[o], 64, &s.count[o]);
-      wl.absorb(other, k);
-    }
-    wl.emit(out, count_out);
-  }
+  merge_and_emit(wl, s, k, floor ? fl : -1.0e308, out, count_out);
 }
 
 }  // namespace
@@ -307,16 +320,25 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
   const int c = topk_ctas(n, num_sms);
   ls_elite_rec* part = static_cast<ls_elite_rec*>(scratch);
   int32_t* counts = reinterpret_cast<int32_t*>(part + (size_t)c * k);
-  topk_local_kernel<<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k, index_base,
-                                               part, counts);
-  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
+  if (k <= 32) {
+    topk_local_kernel<RegList><<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k,
+                                                          index_base, part, counts);
+    topk_merge_kernel<RegList><<<1, kTopkThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
+  } else {
+    topk_local_kernel<WarpList><<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k,
+                                                           index_base, part, counts);
+    topk_merge_kernel<WarpList><<<1, kTopkThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s) {
-  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
+  if (k <= 32)
+    topk_merge_kernel<RegList><<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
+  else
+    topk_merge_kernel<WarpList><<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
   return cudaGetLastError();
 }
 

@@ -153,6 +153,27 @@ struct WarpList {
     }
   }
 
+  // Same interface as RegList for cross-warp merges through Rec slots.
+  __device__ void store(Rec* slots, int* cnt) const {
+    const int lane = threadIdx.x & 31;
+    const int c = *count;
+    for (int j = lane; j < c; j += 32) slots[j] = Rec{key[j], raw[j], idx[j], code[j]};
+    if (lane == 0) *cnt = c;
+  }
+  __device__ void absorb(const Rec* slots, int n, int k, double floor = -1.0e308) {
+    const int lane = threadIdx.x & 31;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      Rec r{0.0, 0.0, 0, 0};
+      bool have = false;
+      if (j < n) {
+        r = slots[j];
+        have = r.key >= floor;
+      }
+      offer(have, r, k);
+    }
+  }
+
   __device__ void emit(ls_elite_rec* out, int32_t* count_out) const {
     const int lane = threadIdx.x & 31;
     const int cnt = *count;
@@ -165,6 +186,130 @@ struct WarpList {
       out[j] = e;
     }
     if (lane == 0) *count_out = cnt;
+  }
+};
+
+// Register-resident variant for k <= 32: lane j holds entry j, so an insert
+// is a handful of ballots and one shuffle — no shared memory, no syncwarp.
+// Same ordering, dedupe and eviction rule as WarpList.
+struct RegList {
+  double key, raw;
+  int64_t idx;
+  uint64_t code;
+  int count;  // warp-uniform
+
+  __device__ __forceinline__ void init() {
+    key = raw = 0.0;
+    idx = 0;
+    code = 0;
+    count = 0;
+  }
+
+  __device__ __forceinline__ bool admits(double k_, int64_t i_, int k) const {
+    if (count < k) return true;
+    const double kk = __shfl_sync(0xffffffffu, key, k - 1);
+    const int64_t ki = __shfl_sync(0xffffffffu, idx, k - 1);
+    return better(k_, i_, kk, ki);
+  }
+
+  __device__ __forceinline__ double floor_key(int k) const {
+    const double kk = __shfl_sync(0xffffffffu, key, k - 1);
+    return count < k ? -1.0e308 : kk;
+  }
+
+  // Warp-cooperative insert of r (all lanes pass the same r).
+  __device__ void insert(const Rec& r, int k) {
+    const int lane = threadIdx.x & 31;
+    const unsigned dup = __ballot_sync(0xffffffffu, lane < count && code == r.code);
+    if (dup) {
+      const int d = __ffs(dup) - 1;
+      const double dk = __shfl_sync(0xffffffffu, key, d);
+      const int64_t di = __shfl_sync(0xffffffffu, idx, d);
+      if (!better(r.key, r.idx, dk, di)) return;
+      // remove entry d: lanes >= d take their right neighbour
+      const double k2 = __shfl_down_sync(0xffffffffu, key, 1), r2 = __shfl_down_sync(0xffffffffu, raw, 1);
+      const int64_t i2 = __shfl_down_sync(0xffffffffu, idx, 1);
+      const uint64_t c2 = __shfl_down_sync(0xffffffffu, code, 1);
+      if (lane >= d) {
+        key = k2;
+        raw = r2;
+        idx = i2;
+        code = c2;
+      }
+      --count;
+    } else if (count == k) {
+      const double kk = __shfl_sync(0xffffffffu, key, k - 1);
+      const int64_t ki = __shfl_sync(0xffffffffu, idx, k - 1);
+      if (!better(r.key, r.idx, kk, ki)) return;
+      --count;  // drop the worst
+    }
+    const int pos = __popc(__ballot_sync(0xffffffffu, lane < count && better(key, idx, r.key, r.idx)));
+    const double k1 = __shfl_up_sync(0xffffffffu, key, 1), r1 = __shfl_up_sync(0xffffffffu, raw, 1);
+    const int64_t i1 = __shfl_up_sync(0xffffffffu, idx, 1);
+    const uint64_t c1 = __shfl_up_sync(0xffffffffu, code, 1);
+    if (lane > pos) {
+      key = k1;
+      raw = r1;
+      idx = i1;
+      code = c1;
+    } else if (lane == pos) {
+      key = r.key;
+      raw = r.raw;
+      idx = r.idx;
+      code = r.code;
+    }
+    ++count;
+  }
+
+  // Offer one record per lane (lanes with have == false offer nothing).
+  __device__ void offer(bool have, const Rec& mine, int k) {
+    const bool cand = have && admits(mine.key, mine.idx, k);
+    unsigned mask = __ballot_sync(0xffffffffu, cand);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      Rec r;
+      r.key = __shfl_sync(0xffffffffu, mine.key, src);
+      r.raw = __shfl_sync(0xffffffffu, mine.raw, src);
+      r.idx = __shfl_sync(0xffffffffu, mine.idx, src);
+      r.code = __shfl_sync(0xffffffffu, mine.code, src);
+      insert(r, k);
+    }
+  }
+
+  // Spill to / fill from shared memory (lane j <-> slot j) for cross-warp merges.
+  __device__ void store(Rec* slots, int* cnt) const {
+    const int lane = threadIdx.x & 31;
+    if (lane < count) slots[lane] = Rec{key, raw, idx, code};
+    if (lane == 0) *cnt = count;
+  }
+
+  // Offer n records held in shared memory slots (any order is exact).
+  __device__ void absorb(const Rec* slots, int n, int k, double floor = -1.0e308) {
+    const int lane = threadIdx.x & 31;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      Rec r{0.0, 0.0, 0, 0};
+      bool have = false;
+      if (j < n) {
+        r = slots[j];
+        have = r.key >= floor;
+      }
+      offer(have, r, k);
+    }
+  }
+
+  __device__ void emit(ls_elite_rec* out, int32_t* count_out) const {
+    const int lane = threadIdx.x & 31;
+    if (lane < count) {
+      ls_elite_rec e;
+      e.key = key;
+      e.raw = raw;
+      e.index = idx;
+      e.code = code;
+      out[lane] = e;
+    }
+    if (lane == 0) *count_out = count;
   }
 };
 
