@@ -196,26 +196,25 @@ struct RegList {
   double key, raw;
   int64_t idx;
   uint64_t code;
-  int count;  // warp-uniform
+  int count;         // warp-uniform
+  double kth_key;    // warp-uniform copy of entry k-1 (valid when count == k)
+  int64_t kth_idx;
 
   __device__ __forceinline__ void init() {
     key = raw = 0.0;
     idx = 0;
     code = 0;
     count = 0;
+    kth_key = -1.0e308;
+    kth_idx = 0;
   }
 
+  // Shuffle-free, so it may be called from divergent code.
   __device__ __forceinline__ bool admits(double k_, int64_t i_, int k) const {
-    if (count < k) return true;
-    const double kk = __shfl_sync(0xffffffffu, key, k - 1);
-    const int64_t ki = __shfl_sync(0xffffffffu, idx, k - 1);
-    return better(k_, i_, kk, ki);
+    return count < k || better(k_, i_, kth_key, kth_idx);
   }
 
-  __device__ __forceinline__ double floor_key(int k) const {
-    const double kk = __shfl_sync(0xffffffffu, key, k - 1);
-    return count < k ? -1.0e308 : kk;
-  }
+  __device__ __forceinline__ double floor_key(int k) const { return count < k ? -1.0e308 : kth_key; }
 
   // Warp-cooperative insert of r (all lanes pass the same r).
   __device__ void insert(const Rec& r, int k) {
@@ -238,9 +237,7 @@ struct RegList {
       }
       --count;
     } else if (count == k) {
-      const double kk = __shfl_sync(0xffffffffu, key, k - 1);
-      const int64_t ki = __shfl_sync(0xffffffffu, idx, k - 1);
-      if (!better(r.key, r.idx, kk, ki)) return;
+      if (!better(r.key, r.idx, kth_key, kth_idx)) return;
       --count;  // drop the worst
     }
     const int pos = __popc(__ballot_sync(0xffffffffu, lane < count && better(key, idx, r.key, r.idx)));
@@ -259,6 +256,8 @@ struct RegList {
       code = r.code;
     }
     ++count;
+    kth_key = __shfl_sync(0xffffffffu, key, k - 1);
+    kth_idx = __shfl_sync(0xffffffffu, idx, k - 1);
   }
 
   // Offer one record per lane (lanes with have == false offer nothing).
