@@ -183,6 +183,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2509_00217_b200.config import load_workload
+    from paper_2509_00217_b200.dist import ShardedSweep
     from paper_2509_00217_b200.evaluator import BatchResult, Evaluator, pinned_results
 
     torch.cuda.set_device(local_rank)
@@ -199,9 +200,7 @@ def run_ours(args, rank, world, local_rank):
     out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=dev),
                       throughput=torch.empty(n, dtype=torch.float64, device=dev))
     base = rank * n  # contiguous global index range per rank
-    rec_bytes = 32
-    gathered = torch.empty((world * ELITE_K, rec_bytes), dtype=torch.uint8, device=dev) if world > 1 else None
-    gcounts = torch.empty(world, dtype=torch.int32, device=dev) if world > 1 else None
+    sweep = ShardedSweep(ev, k=ELITE_K)
     stream = torch.cuda.current_stream(dev)
     ev_start, ev_end = [], []
 
@@ -209,18 +208,20 @@ def run_ours(args, rank, world, local_rank):
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        _, recs, count = ev.evaluate_topk(planes, k=ELITE_K, index_base=base, out=out)
+        if world > 1:
+            _, recs, count = ev.evaluate_topk(planes, k=ELITE_K, index_base=base, out=out)
+            if timed:
+                b.record(stream)
+                ev_start.append(a)
+                ev_end.append(b)
+            recs, count = sweep.merge(recs, count)
+            return recs, count, 3
+        _, recs, count = sweep.run(planes, index_base=base, out=out)
         if timed:
             b.record(stream)
             ev_start.append(a)
             ev_end.append(b)
-        launches = 2
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, recs)
-            dist.all_gather_into_tensor(gcounts, count)
-            recs, count = ev.merge_records(gathered, gcounts, ELITE_K, ELITE_K)
-            launches += 1
-        return recs, count, launches
+        return recs, count, 2
 
     for _ in range(args.warmup):
         step(False)

@@ -58,3 +58,26 @@ def best_by_raw(reason, throughput):
         if best is None or thr > throughput[best]:
             best = i
     return best
+
+
+def elite_merge(lists, capacity):
+    """Merge elite lists [(vector, key, index), ...] with the device merge rule:
+    a duplicate vector is replaced only by a better occurrence (key desc,
+    index asc), the worst entry is evicted when full. Exact for any order."""
+    out = []  # sorted best first
+    def better(a, b):
+        return a[1] > b[1] or (a[1] == b[1] and a[2] < b[2])
+    for lst in lists:
+        for rec in lst:
+            dup = next((i for i, e in enumerate(out) if e[0] == rec[0]), None)
+            if dup is not None:
+                if not better(rec, out[dup]):
+                    continue
+                out.pop(dup)
+            elif len(out) >= capacity:
+                if not better(rec, out[-1]):
+                    continue
+                out.pop()
+            pos = sum(1 for e in out if better(e, rec))
+            out.insert(pos, rec)
+    return out

@@ -1,0 +1,86 @@
+"""Multi-GPU sharding of batched evaluation (one process per GPU).
+
+Candidates are independent — ``simulate`` is pure (reference SPEC.md:241) —
+so a batch shards by contiguous global index ranges with no data-path
+communication. Only two small exchanges cross ranks:
+
+* the elite: every rank reduces its shard to a top-k on device
+  (``Evaluator.evaluate_topk``), the per-rank records (k x 32 B) are
+  all-gathered (NCCL over NVLink on B200) and merged on device with
+  ``ls_topk_merge``; contiguous ranges keep "earliest global index wins"
+  consistent, and the merge rule is exact for any arrival order;
+* reward shaping across ranks (``SearchEnv.step`` semantics, env.py:159-164):
+  each rank needs the best valid raw of all EARLIER ranks as its starting
+  baseline — one all-gather of one float per rank.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+__all__ = ["shard_range", "exclusive_prefix_best", "ShardedSweep", "SweepResult"]
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) slice of n global candidates owned by `rank`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world {world}")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def exclusive_prefix_best(local_best: float, b0: float, group=None) -> tuple[float, float]:
+    """(baseline for this rank, best over all ranks) for the exclusive running max.
+
+    ``local_best`` is this rank's best valid raw (or -inf when none). Works on
+    any backend (gloo for the CPU tests, NCCL on GPUs).
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.device("cpu") if dist.get_backend(group) == "gloo" else torch.device("cuda", torch.cuda.current_device())
+    mine = torch.tensor([local_best], dtype=torch.float64, device=dev)
+    allv = torch.empty(world, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    vals = allv.cpu().tolist()
+    base = max([b0] + vals[:rank])
+    return base, max([b0] + vals)
+
+
+@dataclass
+class SweepResult:
+    elites: list  # list[Elite], best first
+    local_count: int
+
+
+class ShardedSweep:
+    """Evaluate a globally indexed batch split across ranks and merge the elite."""
+
+    def __init__(self, evaluator, k: int = 8, group=None):
+        self.ev = evaluator
+        self.k = int(k)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = evaluator.device
+        self._gathered = torch.empty((self.world * self.k, 32), dtype=torch.uint8, device=dev)
+        self._gcounts = torch.empty(self.world, dtype=torch.int32, device=dev)
+
+    def run(self, planes: torch.Tensor, index_base: int, out=None, verdicts: bool = True):
+        """Score this rank's planes (global indices index_base..) and return the global elite.
+
+        Returns (out, recs, count) with recs/count the merged global top-k on device.
+        """
+        out, recs, count = self.ev.evaluate_topk(planes, k=self.k, index_base=index_base, out=out,
+                                                 verdicts=verdicts)
+        recs, count = self.merge(recs, count)
+        return out, recs, count
+
+    def merge(self, recs: torch.Tensor, count: torch.Tensor):
+        """All-gather every rank's device top-k (k x 32 B) and merge on device."""
+        if self.world == 1:
+            return recs, count
+        dist.all_gather_into_tensor(self._gathered, recs, group=self.group)
+        dist.all_gather_into_tensor(self._gcounts, count, group=self.group)
+        return self.ev.merge_records(self._gathered, self._gcounts, self.k, self.k)

@@ -1,0 +1,67 @@
+"""Two-GPU sharded sweep over NCCL: per-rank fused evaluate + elite, all-gather
+of the per-rank records, device merge — must equal the single-GPU elite of the
+whole batch. Skipped on boxes with fewer than 2 GPUs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, k, q):
+    import torch.distributed as dist
+
+    from paper_2509_00217_b200.config import load_workload
+    from paper_2509_00217_b200.dist import ShardedSweep, shard_range
+    from paper_2509_00217_b200.evaluator import Evaluator
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        wl = load_workload("moe_1p6t_h100x2048")
+        ev = Evaluator(wl, device=rank)
+        rng = np.random.default_rng(11)
+        planes = np.stack([rng.integers(0, s, size=n, dtype=np.uint8) for s in ev.head_sizes])
+        lo, hi = shard_range(n, rank, world)
+        mine = torch.from_numpy(np.ascontiguousarray(planes[:, lo:hi])).cuda(rank)
+        sweep = ShardedSweep(ev, k=k)
+        _, recs, count = sweep.run(mine, index_base=lo)
+        elites = ev.decode_records(recs, count)
+        if rank == 0:
+            whole = torch.from_numpy(planes).cuda(rank)
+            _, r1, c1 = ev.evaluate_topk(whole, k=k)
+            q.put(([(e.vector, e.raw, e.index) for e in elites],
+                   [(e.vector, e.raw, e.index) for e in ev.decode_records(r1, c1)]))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("k", [3, 8])
+def test_two_gpu_elite_equals_single_gpu(k):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n = 5_000_003
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, k, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    merged, single = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert merged == single and len(merged) == k
