@@ -201,6 +201,30 @@ int ls_evaluate_topk(ls_ctx* ctx, const uint8_t* planes, int64_t n, int64_t plan
                      const ls_result_soa* out, int k, int64_t index_base, ls_elite_rec* topk_out,
                      int32_t* count_out, void* scratch, void* stream);
 
+/* On-device candidate streams: the candidates are generated in registers,
+ * never read from memory (0 B/candidate of input traffic).
+ *   LS_GEN_UNIFORM          i.i.d. uniform over every head (the random-walk
+ *                           proposal, baselines.py:50-54), a counter-based
+ *                           function of (seed, stream index);
+ *   LS_GEN_ENUM             stream index i -> the i-th vector of
+ *                           itertools.product over all head domains (the
+ *                           order of the reference's exhaustive sweeps);
+ *   LS_GEN_ENUM_ADMISSIBLE  the same over admissible axes only
+ *                           (FusedOpDescriptor.admits, strategy.py:57-59).
+ * Vectors of up to 16 heads. */
+enum { LS_GEN_UNIFORM = 1, LS_GEN_ENUM = 2, LS_GEN_ENUM_ADMISSIBLE = 3 };
+
+/* Length of an enumeration stream (0 for LS_GEN_UNIFORM or on error). */
+uint64_t ls_stream_size(ls_ctx* ctx, int mode);
+/* Materialise stream positions [start, start + n) as SoA planes. */
+int ls_generate(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, uint8_t* planes,
+                int64_t plane_stride, void* stream);
+/* Evaluate stream positions [start, start + n) and reduce them to the top-k
+ * by raw throughput over distinct vectors (index = stream position). k <= 32;
+ * scratch as for ls_evaluate_topk_scratch_bytes(ctx, n, k). */
+int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int k, ls_elite_rec* topk_out,
+             int32_t* count_out, void* scratch, void* stream);
+
 /* Merge m device-resident record lists (e.g. the all-gathered per-rank top-k)
  * into the global top-k with the same ordering and dedupe rule. */
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,

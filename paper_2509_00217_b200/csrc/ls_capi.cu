@@ -12,8 +12,10 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/ls_eval.h"
+#include "ls_formulas.cuh"
 #include "ls_kernels.h"
 
 using namespace ls;
@@ -58,6 +60,11 @@ struct ls_ctx {
   bool smem_gate = false;
   int64_t blocks_tma = 0, blocks_generic = 0;
   uint64_t space_size = 0;
+  // on-device candidate streams, built lazily per mode
+  std::mutex gen_mu;
+  GenMeta gen[4] = {};
+  bool gen_ready[4] = {};
+  uint32_t* gen_tabs[4] = {};
   // host pipeline
   std::mutex host_mu;
   cudaStream_t hs[2] = {nullptr, nullptr};
@@ -161,6 +168,81 @@ void build_meta(ls_ctx* c) {
   for (int h = 0; h < LS_MAX_HEADS; ++h) c->TM.code_stride[h] = M.code_stride[h];
 }
 
+uint64_t ceil_recip(uint64_t d) {  // ceil(2^64 / d), d >= 2
+  const unsigned __int128 one = (unsigned __int128)1 << 64;
+  return (uint64_t)((one + d - 1) / d);
+}
+
+// Mixed-radix tables of one candidate stream mode (see GenMeta). Axis heads
+// take radix 3 (GEN_UNIFORM, GEN_ENUM) or the number of axes the op they
+// control admits (GEN_ENUM_ADMISSIBLE, FusedOpDescriptor.admits,
+// strategy.py:57-59); the last min(6, #axis heads) heads form the low group.
+int build_gen(ls_ctx* c, int mode) {
+  if (c->gen_ready[mode]) return LS_OK;
+  const ls_workload_desc& d = c->desc;
+  const int A = d.vector_length;
+  if (A > 16) return fail(LS_ERR_UNSUPPORTED, "on-device candidate streams support vectors of up to 16 heads");
+  int radix[16], axes[16][3];
+  for (int h = 4; h < A; ++h) {
+    radix[h] = 3;
+    for (int v = 0; v < 3; ++v) axes[h][v] = v;
+    if (mode == GEN_ENUM_ADMISSIBLE) {
+      for (int k = 0; k < LS_NUM_OPS; ++k) {
+        if (d.op_head[k] != h) continue;
+        if ((k == LS_OP_SHARED_FFN1 || k == LS_OP_SHARED_FFN2) && !d.has_shared_expert) break;
+        const int mask = admits_mask(k);
+        int r = 0;
+        for (int v = 0; v < 3; ++v)
+          if ((mask >> v) & 1) axes[h][r++] = v;
+        radix[h] = r;
+      }
+    }
+  }
+  const int naxis = A - 4, nlo = naxis < 6 ? naxis : 6, lo0 = A - nlo;
+  uint64_t lo_size = 1, hi_size = 1;
+  for (int h = lo0; h < A; ++h) lo_size *= radix[h];
+  for (int h = 4; h < lo0; ++h) hi_size *= radix[h];
+  std::vector<uint32_t> tab(hi_size + lo_size);
+  auto fill = [&](uint32_t* out, uint64_t size, int h0, int h1) {
+    for (uint64_t r = 0; r < size; ++r) {
+      uint64_t x = r;
+      uint32_t y = 0;
+      for (int h = h1 - 1; h >= h0; --h) {
+        y |= (uint32_t)axes[h][x % radix[h]] << (2 * (h - 4));
+        x /= radix[h];
+      }
+      out[r] = y;
+    }
+  };
+  fill(tab.data(), hi_size, 4, lo0);
+  fill(tab.data() + hi_size, lo_size, lo0, A);
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->gen_tabs[mode], tab.size() * 4)) != cudaSuccess) return cuda_fail(e, "gen tables");
+  if ((e = cudaMemcpy(c->gen_tabs[mode], tab.data(), tab.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "gen tables copy");
+  GenMeta& g = c->gen[mode];
+  g.coarse_size = (uint64_t)d.domain_len[0] * d.domain_len[1] * d.domain_len[2] * d.domain_len[3];
+  g.lo_size = lo_size;
+  g.axis_size = lo_size * hi_size;
+  g.nb = (uint64_t)d.domain_len[3];
+  g.np = (uint64_t)d.domain_len[2];
+  g.ne = (uint64_t)d.domain_len[1];
+  g.m_axis = g.axis_size > 1 ? ceil_recip(g.axis_size) : 0;
+  g.m_lo = lo_size > 1 ? ceil_recip(lo_size) : 0;
+  g.m_b = g.nb > 1 ? ceil_recip(g.nb) : 0;
+  g.m_p = g.np > 1 ? ceil_recip(g.np) : 0;
+  g.m_e = g.ne > 1 ? ceil_recip(g.ne) : 0;
+  g.hi_tab = c->gen_tabs[mode];
+  g.lo_tab = c->gen_tabs[mode] + hi_size;
+  c->gen_ready[mode] = true;
+  return LS_OK;
+}
+
+uint64_t stream_size(const GenMeta& g) {
+  const unsigned __int128 t = (unsigned __int128)g.coarse_size * g.axis_size;
+  return t >> 62 ? 0 : (uint64_t)t;
+}
+
 }  // namespace
 
 extern "C" {
@@ -226,6 +308,7 @@ int ls_ctx_destroy(ls_ctx* c) {
     cudaFree(c->h_reason[s]);
     for (int f = 0; f < 6; ++f) cudaFree(c->h_f[s][f]);
   }
+  for (int m = 0; m < 4; ++m) cudaFree(c->gen_tabs[m]);
   cudaFree(c->d_tab);
   delete c;
   return LS_OK;
@@ -432,6 +515,79 @@ int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_
   cudaError_t e =
       launch_topk_merge(recs, counts, m, k_in, k, nullptr, out, count_out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge launch");
+}
+
+uint64_t ls_stream_size(ls_ctx* c, int mode) {
+  if (!c || mode < LS_GEN_UNIFORM || mode > LS_GEN_ENUM_ADMISSIBLE) return 0;
+  std::lock_guard<std::mutex> lock(c->gen_mu);
+  DeviceGuard g(c->device);
+  if (build_gen(c, mode)) return 0;
+  return mode == LS_GEN_UNIFORM ? 0 : stream_size(c->gen[mode]);
+}
+
+static int gen_meta(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, GenMeta* out) {
+  if (mode < LS_GEN_UNIFORM || mode > LS_GEN_ENUM_ADMISSIBLE) return fail(LS_ERR_INVALID_ARGUMENT, "bad stream mode");
+  if (start < 0 || n < 0) return fail(LS_ERR_INVALID_ARGUMENT, "negative start or n");
+  std::lock_guard<std::mutex> lock(c->gen_mu);
+  int rc = build_gen(c, mode);
+  if (rc) return rc;
+  *out = c->gen[mode];
+  out->start = start;
+  out->seed = seed;
+  if (mode != LS_GEN_UNIFORM) {
+    const uint64_t total = stream_size(*out);
+    if (total == 0) return fail(LS_ERR_UNSUPPORTED, "enumeration space too large for exact 64-bit indexing");
+    if ((uint64_t)start + (uint64_t)n > total) return fail(LS_ERR_INVALID_ARGUMENT, "start + n exceeds the stream size");
+  } else if ((uint64_t)start + (uint64_t)n >= (1ull << 40)) {
+    return fail(LS_ERR_INVALID_ARGUMENT, "uniform stream indices must stay below 2^40");
+  }
+  return LS_OK;
+}
+
+int ls_generate(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, uint8_t* planes, int64_t plane_stride,
+                void* stream) {
+  g_err.clear();
+  if (!c || (n > 0 && !planes) || plane_stride < n) return fail(LS_ERR_INVALID_ARGUMENT, "bad generate arguments");
+  DeviceGuard g(c->device);
+  GenMeta gm;
+  int rc = gen_meta(c, mode, seed, start, n, &gm);
+  if (rc) return rc;
+  cudaError_t e =
+      launch_generate(mode, gm, n, c->desc.vector_length, planes, plane_stride, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "generate launch");
+}
+
+int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k, ls_elite_rec* topk_out,
+             int32_t* count_out, void* scratch, void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || k < 1 || k > fused_k_max() || !topk_out || !count_out || !scratch)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad sweep arguments (k must be in [1, 32])");
+  if (c->blocks_tma == 0) return fail(LS_ERR_UNSUPPORTED, "sweeps need vectors of up to 16 heads");
+  DeviceGuard g(c->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GenMeta gm;
+  int rc = gen_meta(c, mode, seed, start, n, &gm);
+  if (rc) return rc;
+  if (n == 0) {
+    cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
+    return LS_OK;
+  }
+  LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
+  const int64_t grid = std::min<int64_t>((n + 1023) / 1024, c->blocks_tma);
+  TopkArgs tk{k, start, static_cast<ls_elite_rec*>(scratch), nullptr, nullptr};
+  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
+  tk.floor = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(tk.part_counts + grid) + 7) &
+                                                   ~uintptr_t(7));
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(tk.floor, 0, sizeof(unsigned long long), s)) != cudaSuccess)
+    return cuda_fail(e, "floor reset");
+  if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=
+      cudaSuccess)
+    return cuda_fail(e, "sweep launch");
+  if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, tk.floor, topk_out, count_out, s)) !=
+      cudaSuccess)
+    return cuda_fail(e, "sweep merge launch");
+  return LS_OK;
 }
 
 }  // extern "C"

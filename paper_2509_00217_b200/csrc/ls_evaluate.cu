@@ -143,6 +143,45 @@ __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, in
   c.Y = ((q[0] >> sh) & 0xffu) | (((q[1] >> sh) & 0xffu) << 8) | (((q[2] >> sh) & 0xffu) << 16);
 }
 
+// ---- on-device candidate streams (ls_sweep) ----------------------------
+// Counter-based 64-bit mix (splitmix64 finaliser); host twin: generator.py.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// floor(x / d) via a 64-bit reciprocal: exact whenever x * d < 2^64.
+__device__ __forceinline__ uint64_t divq(uint64_t x, uint64_t magic, uint64_t d) {
+  return d == 1 ? x : __umul64hi(x, magic);
+}
+// Stream index -> decoded candidate. GEN_UNIFORM: i.i.d. uniform over every
+// head (baselines.uniform_vector semantics, baselines.py:50-54) from two
+// counter-based draws; GEN_ENUM / GEN_ENUM_ADMISSIBLE: the index-th vector of
+// itertools.product over the head domains (all axes / admissible axes only),
+// head 0 most significant — the order of the reference's exhaustive sweeps.
+template <int MODE>
+__device__ __forceinline__ void gen_candidate(const GenMeta& g, uint64_t gidx, Decoded& c) {
+  uint64_t coarse, axis;
+  if (MODE == GEN_UNIFORM) {
+    const uint64_t r1 = splitmix64(g.seed ^ (2 * gidx)), r2 = splitmix64(g.seed ^ (2 * gidx + 1));
+    coarse = __umul64hi(r1, g.coarse_size);
+    axis = __umul64hi(r2, g.axis_size);
+  } else {
+    coarse = divq(gidx, g.m_axis, g.axis_size);
+    axis = gidx - coarse * g.axis_size;
+  }
+  const uint64_t hi = divq(axis, g.m_lo, g.lo_size), lo = axis - hi * g.lo_size;
+  c.Y = __ldg(g.hi_tab + hi) | __ldg(g.lo_tab + lo);
+  const uint64_t q1 = divq(coarse, g.m_b, g.nb);
+  c.b = (int)(coarse - q1 * g.nb);
+  const uint64_t q2 = divq(q1, g.m_p, g.np);
+  c.p = (int)(q1 - q2 * g.np);
+  const uint64_t q3 = divq(q2, g.m_e, g.ne);
+  c.e = (int)(q2 - q3 * g.ne);
+  c.t = (int)q3;
+}
+
 // Dynamic shared memory of eval_ws_kernel: TMA ring, gate tables, per-gate
 // warp survivor queues, mailboxes and the work warps' elite lists.
 struct WsSmem {
@@ -196,10 +235,10 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
   }
 }
 
-template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK>
+template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK, int MODE>
 __global__ void __launch_bounds__(kThreads, 2)
     eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
-                   const int64_t ntiles, const TopkArgs tk) {
+                   const int64_t ntiles, const TopkArgs tk, const GenMeta gm) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
@@ -248,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         bulk_g2s(S.gate, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
       }
       int i = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      for (int64_t tile = blockIdx.x; MODE == GEN_PLANES && tile < ntiles; tile += gridDim.x, ++i) {
         const int s = i % kStages, k = i / kStages;
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
         mbar_expect_tx(&full_bar[s], stage_bytes);
@@ -333,15 +372,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
     };
 
-    auto pass_a = [&](const uint32_t* w, int64_t base, int count) {
-      uint32_t q[3];
-      const uint32_t badb = swar_decode(w, M, q);
+    // gate pass over this lane's 4 decoded candidates (stream indices base..)
+    auto pass_a = [&](Decoded* cs, uint32_t badb, int64_t base, int count) {
       uint32_t r4 = 0;
       double m[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        Decoded c;
-        extract(w, q, j, c);
+        Decoded c = cs[j];
         const bool dbad = ((badb >> (8 * j)) & 0xffu) != 0;
         if (dbad) c.t = c.e = c.p = c.b = 0;  // keep the branch-free lookups in range
         double mem;
@@ -399,31 +436,54 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
 
     const int lane_off = warp * kWarpCands + 4 * lane;
-    int i = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-      const int s = i % kStages;
-      mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
-      uint32_t w[16];
-      const uint32_t st = ring_base + (uint32_t)s * kStageBytes + (uint32_t)lane_off;
+    if (MODE == GEN_PLANES) {
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i % kStages;
+        mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
+        uint32_t w[16];
+        const uint32_t st = ring_base + (uint32_t)s * kStageBytes + (uint32_t)lane_off;
 #pragma unroll
-      for (int h = 0; h < 16; ++h) w[h] = lds_u32(st + h * kTile);  // planes >= A are zero-filled
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
-      pass_a(w, tile * kTile + lane_off, 4);
-    }
-    // ragged tail (< one tile): the CTA that would own the next tile
-    const int64_t tail0 = ntiles * kTile;
-    if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
-      const int64_t base = tail0 + lane_off;
-      const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
-      uint32_t w[16];
+        for (int h = 0; h < 16; ++h) w[h] = lds_u32(st + h * kTile);  // planes >= A are zero-filled
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        uint32_t q[3];
+        const uint32_t badb = swar_decode(w, M, q);
+        Decoded cs[4];
 #pragma unroll
-      for (int h = 0; h < 16; ++h) {
-        w[h] = 0;
-        if (h < A)
-          for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
+        for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
+        pass_a(cs, badb, tile * kTile + lane_off, 4);
       }
-      pass_a(w, base, count);
+      // ragged tail (< one tile): the CTA that would own the next tile
+      const int64_t tail0 = ntiles * kTile;
+      if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
+        const int64_t base = tail0 + lane_off;
+        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+        uint32_t w[16];
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          w[h] = 0;
+          if (h < A)
+            for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
+        }
+        uint32_t q[3];
+        const uint32_t badb = swar_decode(w, M, q);
+        Decoded cs[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
+        pass_a(cs, badb, base, count);
+      }
+    } else {  // candidates generated in registers: nothing read from HBM
+      const int64_t gtiles = (a.n + kTile - 1) / kTile;
+      for (int64_t tile = blockIdx.x; tile < gtiles; tile += gridDim.x) {
+        const int64_t base = tile * kTile + lane_off;
+        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+        Decoded cs[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)  // past-the-end lanes regenerate the last valid index (never enqueued)
+          gen_candidate<MODE>(gm, (uint64_t)(gm.start + (base + j < a.n ? base + j : a.n - 1)), cs[j]);
+        pass_a(cs, 0u, base, count);
+      }
     }
     if (qcount > 0) flush(qcount);
     __syncwarp();
@@ -486,21 +546,44 @@ __global__ void __launch_bounds__(kGenericThreads) eval_generic_kernel(const uin
 
 template <bool NEU, bool FULL, bool SG>
 void set_attr(size_t smem) {
-  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int b = (int)smem;
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, false, GEN_PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, true, GEN_PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (!FULL) {
+    cudaFuncSetAttribute(eval_ws_kernel<NEU, false, SG, true, GEN_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         b);
+    cudaFuncSetAttribute(eval_ws_kernel<NEU, false, SG, true, GEN_ENUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(eval_ws_kernel<NEU, false, SG, true, GEN_ENUM_ADMISSIBLE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  }
 }
 
-template <bool NEU, bool FULL, bool TOPK>
+template <bool NEU, bool FULL, bool TOPK, int MODE = GEN_PLANES>
 void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, const EvalArgs& a,
-                 const TopkArgs& tk, cudaStream_t s) {
-  const int64_t ntiles = a.n / kTile;
+                 const TopkArgs& tk, cudaStream_t s, const GenMeta& gm = GenMeta{}) {
+  const int64_t ntiles = MODE == GEN_PLANES ? a.n / kTile : (a.n + kTile - 1) / kTile;
   const size_t smem = ws_dynamic_bytes(M.A, L.gate_words, lp.smem_gate);
   int64_t blocks = ntiles > 0 ? ntiles : 1;
   if (blocks > lp.max_blocks) blocks = lp.max_blocks;
   if (lp.smem_gate)
-    eval_ws_kernel<NEU, FULL, true, TOPK><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
+    eval_ws_kernel<NEU, FULL, true, TOPK, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
   else
-    eval_ws_kernel<NEU, FULL, false, TOPK><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk);
+    eval_ws_kernel<NEU, FULL, false, TOPK, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
+}
+
+// Write the generated stream as SoA planes (tests, users who want the vectors).
+template <int MODE>
+__global__ void generate_kernel(const GenMeta gm, int64_t n, int A, const EvalMeta M, uint8_t* planes,
+                                int64_t stride) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    Decoded c;
+    gen_candidate<MODE>(gm, (uint64_t)(gm.start + i), c);
+    planes[i] = (uint8_t)c.t;
+    planes[stride + i] = (uint8_t)c.e;
+    planes[2 * stride + i] = (uint8_t)c.p;
+    planes[3 * stride + i] = (uint8_t)c.b;
+    for (int h = 4; h < A; ++h) planes[(int64_t)h * stride + i] = (uint8_t)((c.Y >> (2 * (h - 4))) & 3u);
+  }
 }
 
 template <bool TOPK>
@@ -547,9 +630,11 @@ int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate) {
   int nb = 0;
   const size_t smem = tma_smem_bytes(L, A, smem_gate);
   if (smem_gate)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, true, true>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, true, true, GEN_PLANES>, kThreads,
+                                                  smem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, false, true>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_ws_kernel<true, false, false, true, GEN_PLANES>, kThreads,
+                                                  smem);
   return nb;
 }
 
@@ -586,6 +671,34 @@ cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint
                                  const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
   const bool full = a.reason && (a.tpot || a.mem || a.comp || a.comm || a.pipe);
   launch_ws<true>(lp, neumaier, full, tab, L, M, a, tk, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const LaunchPlan& lp, bool neumaier, int mode, const uint64_t* tab, const TabLayout& L,
+                         const EvalMeta& M, int64_t n, const TopkArgs& tk, const GenMeta& gm, cudaStream_t s) {
+  EvalArgs a{};
+  a.n = n;  // no planes, no per-candidate verdicts: only the fused elite leaves the SMs
+  auto go = [&](auto neu) {
+    constexpr bool NEU = decltype(neu)::value;
+    if (mode == GEN_UNIFORM) launch_ws_t<NEU, false, true, GEN_UNIFORM>(lp, tab, L, M, a, tk, s, gm);
+    else if (mode == GEN_ENUM) launch_ws_t<NEU, false, true, GEN_ENUM>(lp, tab, L, M, a, tk, s, gm);
+    else launch_ws_t<NEU, false, true, GEN_ENUM_ADMISSIBLE>(lp, tab, L, M, a, tk, s, gm);
+  };
+  if (neumaier) go(std::true_type{});
+  else go(std::false_type{});
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8_t* planes, int64_t stride,
+                            cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  EvalMeta dummy{};
+  if (mode == GEN_UNIFORM) generate_kernel<GEN_UNIFORM><<<(unsigned)blocks, threads, 0, s>>>(gm, n, A, dummy, planes, stride);
+  else if (mode == GEN_ENUM) generate_kernel<GEN_ENUM><<<(unsigned)blocks, threads, 0, s>>>(gm, n, A, dummy, planes, stride);
+  else generate_kernel<GEN_ENUM_ADMISSIBLE><<<(unsigned)blocks, threads, 0, s>>>(gm, n, A, dummy, planes, stride);
   return cudaGetLastError();
 }
 

@@ -34,7 +34,27 @@ struct TopkArgs {
   unsigned long long* floor;  // device word, zeroed before launch
 };
 
+// Candidate sources of eval_ws_kernel.
+enum : int { GEN_PLANES = 0, GEN_UNIFORM = 1, GEN_ENUM = 2, GEN_ENUM_ADMISSIBLE = 3 };
+
+// On-device candidate stream: index -> (coarse rank, axis rank) -> decoded
+// candidate. Axis ranks split into a high and a low group of axis heads whose
+// packed Y fields come from two small tables.
+struct GenMeta {
+  int64_t start;  // stream index of the launch's first candidate
+  uint64_t seed;
+  uint64_t coarse_size, axis_size, lo_size;
+  uint64_t m_axis, m_lo, m_b, m_p, m_e;  // ceil(2^64 / d) for the divisors above
+  uint64_t nb, np, ne;
+  const uint32_t* hi_tab;  // [axis_size / lo_size] packed Y of the high group
+  const uint32_t* lo_tab;  // [lo_size] packed Y of the low group
+};
+
 bool tma_eligible(const EvalArgs& a, int A);
+cudaError_t launch_sweep(const LaunchPlan& lp, bool neumaier, int mode, const uint64_t* tab, const TabLayout& L,
+                         const EvalMeta& M, int64_t n, const TopkArgs& tk, const GenMeta& gm, cudaStream_t s);
+cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8_t* planes, int64_t stride,
+                            cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n);
 int fused_k_max();
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,

@@ -258,6 +258,31 @@ class Evaluator:
                                          _ptr(recs), _ptr(count), _ptr(self._scratch), self._stream()))
         return (out if verdicts else None), recs, count
 
+    # -- on-device candidate streams ----------------------------------------
+
+    def stream_size(self, mode: int) -> int:
+        """Length of an enumeration stream (GEN_ENUM / GEN_ENUM_ADMISSIBLE)."""
+        return int(self._lib.ls_stream_size(self._ctx, int(mode)))
+
+    def generate(self, mode: int, n: int, start: int = 0, seed: int = 0) -> torch.Tensor:
+        """Stream positions [start, start + n) as [A, N] uint8 planes on the device."""
+        planes = torch.empty((self.vector_length, max(int(n), 0)), dtype=torch.uint8, device=self.device)
+        check(self._lib.ls_generate(self._ctx, int(mode), int(seed) & (2**64 - 1), int(start), int(n),
+                                    _ptr(planes), max(int(n), 1), self._stream()))
+        return planes
+
+    def sweep(self, mode: int, n: int, start: int = 0, seed: int = 0, k: int = 8):
+        """Evaluate stream positions [start, start + n) generated on the device
+        and return the top-k by raw over distinct vectors (records, count)."""
+        recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.empty(1, dtype=torch.int32, device=self.device)
+        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, int(n), int(k)))
+        if self._scratch is None or self._scratch.numel() < nbytes:
+            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        check(self._lib.ls_sweep(self._ctx, int(mode), int(seed) & (2**64 - 1), int(start), int(n), int(k),
+                                 _ptr(recs), _ptr(count), _ptr(self._scratch), self._stream()))
+        return recs, count
+
     def merge_records(self, recs: torch.Tensor, counts: torch.Tensor, k_in: int, k: int):
         """Merge m stacked record lists ([m*k_in, 32] bytes, counts [m]) into one top-k."""
         m = counts.shape[0]
