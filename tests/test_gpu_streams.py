@@ -60,7 +60,7 @@ def _elite_by_raw(wl, vectors, k, base=0):
     ("moe_1p2t", 1, 2_000_003, 0),
     ("moe_1p6t_2048", 1, 1_000_000, 5_000_000),
     ("dsv3_style_h100x256", 3, 1_500_000, 7_777),
-    ("edge_odd", 2, 900_000, 0),
+    ("edge_odd", 2, 364_500, 0),  # the whole space: 5*5*4*5 coarse x 3^6 axes
 ])
 @pytest.mark.parametrize("k", [1, 8])
 def test_sweep_matches_sequential_elite(name, mode, n, start, k, make_ev):
