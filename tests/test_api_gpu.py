@@ -163,4 +163,4 @@ class TestEnv:
         assert bat.eval_log == seq.eval_log
         assert bat.best_raw == seq.best_raw and bat.evals_used == 400
         with pytest.raises(BudgetExhausted):
-            bat.step_batch(vecs[:3601])
+            bat.step_batch(np.concatenate([vecs, vecs])[:3601])  # 3600 evaluations left
