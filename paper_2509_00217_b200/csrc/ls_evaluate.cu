@@ -134,13 +134,17 @@ __device__ __forceinline__ uint32_t swar_decode(const uint32_t* w, const EvalMet
   return badb | (orv & 0xfcfcfcfcu) | three;
 }
 
+// Candidate j of a lane: byte j of the coarse planes and of the q words
+// (byte permutes; j is a compile-time constant after unrolling).
 __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, int j, Decoded& c) {
-  const int sh = 8 * j;
-  c.t = (int)((w[0] >> sh) & 0xffu);
-  c.e = (int)((w[1] >> sh) & 0xffu);
-  c.p = (int)((w[2] >> sh) & 0xffu);
-  c.b = (int)((w[3] >> sh) & 0xffu);
-  c.Y = ((q[0] >> sh) & 0xffu) | (((q[1] >> sh) & 0xffu) << 8) | (((q[2] >> sh) & 0xffu) << 16);
+  const uint32_t sel = 0x4440u | (uint32_t)j;  // byte j into byte 0, zeros above
+  c.t = (int)__byte_perm(w[0], 0, sel);
+  c.e = (int)__byte_perm(w[1], 0, sel);
+  c.p = (int)__byte_perm(w[2], 0, sel);
+  c.b = (int)__byte_perm(w[3], 0, sel);
+  // Y = q0.byte j | q1.byte j << 8 | q2.byte j << 16
+  const uint32_t y01 = __byte_perm(q[0], q[1], 0x4440u | ((4u + j) << 4) | (uint32_t)j);
+  c.Y = __byte_perm(y01, q[2], 0x4000u | ((4u + j) << 8) | 0x10u) & 0x00ffffffu;
 }
 
 // ---- on-device candidate streams (ls_sweep) ----------------------------
@@ -374,29 +378,31 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     // gate pass over this lane's 4 decoded candidates (stream indices base..)
     auto pass_a = [&](Decoded* cs, uint32_t badb, int64_t base, int count) {
-      uint32_t r4 = 0;
+      uint32_t r4 = 0, reason[4];
       double m[4];
+      // the 4 gate evaluations are independent: issue them back to back (ILP)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        Decoded c = cs[j];
         const bool dbad = ((badb >> (8 * j)) & 0xffu) != 0;
-        if (dbad) c.t = c.e = c.p = c.b = 0;  // keep the branch-free lookups in range
-        double mem;
-        uint32_t reason = gate_bf(Gt, L, M, c, mem);
+        if (dbad) cs[j].t = cs[j].e = cs[j].p = cs[j].b = 0;  // keep the branch-free lookups in range
+        reason[j] = gate(Gt, L, M, cs[j], m[j]);
         if (dbad) {
-          reason = LS_REASON_DECODE_ERROR;
-          mem = 0.0;
+          reason[j] = LS_REASON_DECODE_ERROR;
+          m[j] = 0.0;
         }
-        const bool surv = j < count && reason == LS_REASON_NONE;
+        r4 |= reason[j] << (8 * j);
+      }
+      // then compact the survivors into the warp queue
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool surv = j < count && reason[j] == LS_REASON_NONE;
         const unsigned mask = __ballot_sync(0xffffffffu, surv);
         if (surv) {
           const int pos = qcount + __popc(mask & ((1u << lane) - 1u));
-          qkey[pos] = pack_key(base + j, c);
-          qy[pos] = c.Y;
+          qkey[pos] = pack_key(base + j, cs[j]);
+          qy[pos] = cs[j].Y;
         }
         qcount += __popc(mask);
-        r4 |= reason << (8 * j);
-        m[j] = mem;
       }
       if (!a.reason) {
         // sweep mode: no per-candidate verdicts, only the fused elite

@@ -88,53 +88,27 @@ __device__ __forceinline__ int op_axis(const EvalMeta& M, uint32_t Y, int k) {
   return src >= 0 ? (int)((Y >> src) & 3u) : (int)M.op_pin[k];
 }
 
-// Gate pass. G: gate segment (shared memory or global). Returns the reason
-// code for gated candidates, or LS_REASON_NONE for survivors (which still
-// need full_path); mem receives memory_per_device when computed.
+// Gate pass (every candidate), branch-free: one 128-bit lookup of the
+// (t, e, p) entry gives the weights term, the gate bits and the kv row; the
+// reason is then selected in the reference's gate order — device budget
+// (simulator.py:257), layout (:268, layout.py:371-374, :214-221), memory
+// (:135-160, :279). Returns LS_REASON_NONE for survivors (which still need
+// full_path). mem is set only when the memory gate ran, as in SimResult.
+// Indices must be in range (callers clamp decode-failed candidates).
 __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, const EvalMeta& M, const Decoded& c,
                                          double& mem) {
-  mem = 0.0;
-  const uint4 te = *reinterpret_cast<const uint4*>(G + L.te + 2 * (c.t * L.ne + c.e));
-  const uint64_t over = (uint64_t)te.x | ((uint64_t)te.y << 32);
-  const uint64_t lay = (uint64_t)te.z | ((uint64_t)te.w << 32);
-  // gate 1: world_size > device_budget (simulator.py:257)
-  if ((over >> c.p) & 1) return LS_REASON_OVER_DEVICE_BUDGET;
-  // gate 2: pp | num_layers, ep vs num_experts, per-op admissibility and
-  // extent divisibility (simulator.py:268, layout.py:371-374, :214-221)
-  const uint4 tm = *reinterpret_cast<const uint4*>(G + L.tmask + 2 * c.t);
-  const uint32_t lo = c.Y & 0x555555u, hi = (c.Y >> 1) & 0x555555u;
-  const uint32_t bad =
-      (~(lo | hi) & 0x555555u & tm.x) | (lo & ~hi & tm.y) | (hi & ~lo & tm.z) | tm.w | (uint32_t)((lay >> c.p) & 1);
-  if (bad) return LS_REASON_LAYOUT_ERROR;
-  // gate 3: memory_per_device > hbm_capacity (simulator.py:135-160, :279)
-  const int a2 = (M.attn_src >= 0 ? (int)((c.Y >> M.attn_src) & 3u) : M.attn_pin) == 2;
-  mem = (dget(G, L.mem_w + (c.t * L.ne + c.e) * L.np + c.p) +
-         dget(G, L.mem_kv + ((a2 * L.nt + c.t) * L.np + c.p) * L.nb + c.b)) +
-        dget(G, L.mem_ws + c.b);
-  if (mem > M.hbm_capacity) return LS_REASON_OOM;
-  return LS_REASON_NONE;
-}
-
-// Branch-free gate() for the SWAR pass: every table lookup is issued
-// unconditionally (indices already in range — decode-failed candidates are
-// clamped by the caller) and the reason is selected in gate order, so a warp
-// never diverges on which gate fired. mem is 0 unless the memory gate ran,
-// matching SimResult's field conventions (simulator.py:246-255, :281-284).
-__device__ __forceinline__ uint32_t gate_bf(const uint64_t* G, const TabLayout& L, const EvalMeta& M, const Decoded& c,
-                                            double& mem) {
-  const uint4 te = *reinterpret_cast<const uint4*>(G + L.te + 2 * (c.t * L.ne + c.e));
-  const uint4 tm = *reinterpret_cast<const uint4*>(G + L.tmask + 2 * c.t);
-  const int a2 = (M.attn_src >= 0 ? (int)((c.Y >> M.attn_src) & 3u) : M.attn_pin) == 2;
-  const double m = (dget(G, L.mem_w + (c.t * L.ne + c.e) * L.np + c.p) +
-                    dget(G, L.mem_kv + ((a2 * L.nt + c.t) * L.np + c.p) * L.nb + c.b)) +
+  const int tep = (c.t * L.ne + c.e) * L.np + c.p;
+  const uint4 ent = *reinterpret_cast<const uint4*>(G + L.tep + 2 * tep);
+  const double w = __hiloint2double((int)ent.y, (int)ent.x);
+  const uint32_t bits = ent.z, kv_row = ent.w;
+  const uint32_t a2 = M.attn_src >= 0 ? (c.Y >> (M.attn_src + 1)) & 1u : (uint32_t)(M.attn_pin == 2);
+  const double m = (w + dget(G, L.mem_kv + (int)(a2 * (uint32_t)(L.nt * L.np * L.nb) + kv_row) + c.b)) +
                    dget(G, L.mem_ws + c.b);
-  const uint32_t over = (c.p < 32 ? te.x >> c.p : te.y >> (c.p - 32)) & 1u;
-  const uint32_t lay = (c.p < 32 ? te.z >> c.p : te.w >> (c.p - 32)) & 1u;
-  const uint32_t lo = c.Y & 0x555555u, hi = (c.Y >> 1) & 0x555555u;
-  const uint32_t bad = (~(lo | hi) & 0x555555u & tm.x) | (lo & ~hi & tm.y) | (hi & ~lo & tm.z) | tm.w | lay;
+  const bool over = (bits & GATE_BUDGET) != 0;
+  const bool bad = ((c.Y & bits & GATE_FIELDS) | (bits & (GATE_PINNED | GATE_LAYOUT))) != 0;
   const uint32_t reason = over ? LS_REASON_OVER_DEVICE_BUDGET
                                : (bad ? LS_REASON_LAYOUT_ERROR : (m > M.hbm_capacity ? LS_REASON_OOM : LS_REASON_NONE));
-  mem = (over | bad) ? 0.0 : m;
+  mem = (over || bad) ? 0.0 : m;
   return reason;
 }
 

@@ -23,6 +23,34 @@ __device__ inline void unflat(int i, int d1, int d2, int d3, int* c0, int* c1, i
   *c0 = i / d1;
 }
 
+// Gate bits of one (tp, ep, pp) (see GATE_* in ls_tables.cuh): device budget
+// (simulator.py:257), pp | num_layers and ep vs num_experts (simulator.py:268,
+// layout.py:371-374), and per axis field whether the op it controls is
+// inadmissible under DIM0 / DIM1 or its sharded extent does not divide tp
+// (layout.py:214-221); UNSHARDED is always admitted and never sharded.
+__device__ uint32_t gate_bits(const ls_workload_desc& d, int64_t tp, int64_t ep, int64_t pp) {
+  int slot[LS_MAX_HEADS];
+  head_slots(d, slot);
+  uint32_t g = 0;
+  if (tp * ep * pp > d.device_budget) g |= GATE_BUDGET;
+  if (ep > d.num_experts || d.num_experts % ep != 0 || d.num_layers % pp != 0) g |= GATE_LAYOUT;
+  for (int op = 0; op < LS_NUM_OPS; ++op) {
+    if ((op == LS_OP_SHARED_FFN1 || op == LS_OP_SHARED_FFN2) && !d.has_shared_expert) continue;
+    for (int a = 1; a < 3; ++a) {
+      bool bad = !((admits_mask(op) >> a) & 1);
+      if (!bad && tp > 1) {
+        const int64_t ext = shard_extent(d, op, a);
+        bad = ext < 0 || ext % tp != 0;
+      }
+      if (!bad) continue;
+      const int h = d.op_head[op];
+      if (h >= 0) g |= 1u << (2 * slot[h] + (a - 1));
+      else if (d.op_pinned[op] == a) g |= GATE_PINNED;
+    }
+  }
+  return g;
+}
+
 __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, int w) {
   const int nt = L.nt, ne = L.ne, np = L.np, nb = L.nb;
   const int64_t* TP = d.domain[0];
@@ -85,14 +113,17 @@ __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, in
     const double payload = (routed_tokens(d, B[b], EP[e]) * (double)d.hidden_dim) * (double)d.dtype_bytes;
     return dbits(coll_time(d, false, EP[e], payload, TP[t] * EP[e] <= d.node_size));
   }
-  // weights per device: [t][e][p]
-  if (w >= L.mem_w && w < L.mem_w + nt * ne * np) {
-    unflat(w - L.mem_w, 1, nt, ne * np, &c0, &c1, &c2, &c3);
-    const int t = c2, e = c3 / np, p = c3 % np;
-    int64_t dense, routed;
-    param_counts(d, &dense, &routed);
-    return dbits(((double)(dense * d.dtype_bytes) / (double)TP[t]) / (double)PP[p] +
-                 ((double)(routed * d.dtype_bytes) / (double)(EP[e] * TP[t])) / (double)PP[p]);
+  // gate entry per (t, e, p): word 0 = weights per device (memory_per_device,
+  // simulator.py:147-150); word 1 = gate bits | kv row base << 32
+  if (w >= L.tep && w < L.tep + 2 * nt * ne * np) {
+    const int i = (w - L.tep) / 2, t = i / (ne * np), e = (i / np) % ne, p = i % np;
+    if ((w - L.tep) % 2 == 0) {
+      int64_t dense, routed;
+      param_counts(d, &dense, &routed);
+      return dbits(((double)(dense * d.dtype_bytes) / (double)TP[t]) / (double)PP[p] +
+                   ((double)(routed * d.dtype_bytes) / (double)(EP[e] * TP[t])) / (double)PP[p]);
+    }
+    return (uint64_t)gate_bits(d, TP[t], EP[e], PP[p]) | ((uint64_t)((t * np + p) * nb) << 32);
   }
   // KV cache per device: [attn_dim1][t][p][b]
   if (w >= L.mem_kv && w < L.mem_kv + 2 * nt * np * nb) {
@@ -119,46 +150,6 @@ __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, in
   if (w >= L.tpv && w < L.tpv + nt) return (uint64_t)TP[w - L.tpv];
   if (w >= L.epv && w < L.epv + ne) return (uint64_t)EP[w - L.epv];
   if (w >= L.ppv && w < L.ppv + np) return (uint64_t)PP[w - L.ppv];
-  // [t][e]: {bit p: tp*ep*pp > device_budget (simulator.py:257),
-  //          bit p: num_layers % pp or ep vs num_experts (simulator.py:268, layout.py:371-374)}
-  if (w >= L.te && w < L.te + 2 * nt * ne) {
-    const int i = w - L.te, t = (i / 2) / ne, e = (i / 2) % ne;
-    uint64_t m = 0;
-    const bool ep_bad = EP[e] > d.num_experts || d.num_experts % EP[e] != 0;
-    for (int p = 0; p < np; ++p) {
-      if (i % 2 == 0) {
-        if (TP[t] * EP[e] * PP[p] > d.device_budget) m |= 1ull << p;
-      } else if (ep_bad || d.num_layers % PP[p] != 0) {
-        m |= 1ull << p;
-      }
-    }
-    return m;
-  }
-  // [t]: per-axis-value layout-error masks over Y fields, plus one bit for
-  // pinned ops: op k under axis a is an error when inadmissible or when its
-  // sharded extent does not divide tp (layout.py:214-221).
-  if (w >= L.tmask && w < L.tmask + 2 * nt) {
-    const int i = w - L.tmask, t = i / 2;
-    int slot[LS_MAX_HEADS];
-    head_slots(d, slot);
-    uint32_t bad[3] = {0, 0, 0}, pinned_bad = 0;
-    for (int op = 0; op < LS_NUM_OPS; ++op) {
-      if ((op == LS_OP_SHARED_FFN1 || op == LS_OP_SHARED_FFN2) && !d.has_shared_expert) continue;
-      for (int a = 0; a < 3; ++a) {
-        bool b = !((admits_mask(op) >> a) & 1);
-        if (!b && a != 0 && TP[t] > 1) {
-          const int64_t ext = shard_extent(d, op, a);
-          b = ext < 0 || ext % TP[t] != 0;
-        }
-        if (!b) continue;
-        const int h = d.op_head[op];
-        if (h >= 0) bad[a] |= 1u << (2 * slot[h]);
-        else if (d.op_pinned[op] == a) pinned_bad = 1;
-      }
-    }
-    if (i % 2 == 0) return (uint64_t)bad[0] | ((uint64_t)bad[1] << 32);
-    return (uint64_t)bad[2] | ((uint64_t)pinned_bad << 32);
-  }
   return 0;  // padding
 }
 

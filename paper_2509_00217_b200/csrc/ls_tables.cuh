@@ -37,14 +37,27 @@ enum : int { FAM_NONE = 0, FAM_AR = 1, FAM_ONCE = 2 };
 // Payload classes of TP-group collectives: tokens x features x dtype.
 enum : int { CLS_QKV = 0, CLS_H = 1, CLS_F = 2, CLS_V = 3 };
 
+// Gate bits of a [t][e][p] entry. An axis field of Y holds 0 (UNSHARDED,
+// never a layout error), 1 (DIM0: only its low bit set) or 2 (DIM1: only its
+// high bit set), so "some op's axis is inadmissible or its extent does not
+// divide tp" (layout.py:214-221) is the single test  Y & GATE_FIELDS-mask:
+// bit 2f flags DIM0 bad for field f, bit 2f+1 flags DIM1 bad.
+enum : uint32_t {
+  GATE_FIELDS = 0x00ffffffu,  // 12 axis fields x {DIM0, DIM1}
+  GATE_PINNED = 1u << 24,     // a pinned (uncontrolled) op is a layout error at this tp
+  GATE_LAYOUT = 1u << 25,     // pp does not divide num_layers, or ep vs num_experts
+  GATE_BUDGET = 1u << 26      // tp * ep * pp > device_budget
+};
+
 // Offsets (in 8-byte words) of every table segment inside one buffer.
 struct TabLayout {
   int nt, ne, np, nb;  // tp / ep / pp / batch domain sizes
   int has_shared;
   // gate segment (staged to shared memory)
-  int te;      // [t][e] x 2 words: {over-budget mask over p, layout-error mask over p}
-  int tmask;   // [t] x 2 words: {bad0 | bad1 << 32, bad2 | pinned_bad << 32} (head-order 2-bit fields)
-  int mem_w, mem_kv, mem_ws;
+  // [t][e][p] x 2 words: {weights per device (f64),
+  //   lo32 = gate bits (GATE_*), hi32 = kv row base ((t*np + p)*nb)}
+  int tep;
+  int mem_kv, mem_ws;
   int gate_words;  // words of the gate segment, even
   // op-time segments
   int opt_emb, opt_qkv, opt_kv, opt_attn, opt_out, opt_router, opt_ffn1, opt_ffn2;
@@ -107,9 +120,7 @@ inline TabLayout make_layout(const ls_workload_desc& d) {
     w += round2(words);
     return at;
   };
-  L.te = seg(2 * nt * ne);
-  L.tmask = seg(2 * nt);
-  L.mem_w = seg(nt * ne * np);
+  L.tep = seg(2 * nt * ne * np);
   L.mem_kv = seg(2 * nt * np * nb);
   L.mem_ws = seg(nb);
   L.gate_words = w;
