@@ -1,0 +1,167 @@
+"""Search baselines over the GPU evaluator, batched where the reference's
+algorithm allows it (reference baselines.py:50-194).
+
+* ``random_walk`` draws the same i.i.d. uniform vectors as the reference
+  (numpy PCG64, one ``integers(k)`` per head in order), then scores the whole
+  budget in ONE batched pass (``SearchEnv.step_batch``: device evaluate +
+  exclusive-max reward scan) — records identical to the reference's.
+* ``simulated_annealing`` is a sequential Metropolis chain (each proposal
+  depends on the last acceptance) and steps one candidate at a time.
+* ``megatron_exhaustive`` scores the coarse grid with Megatron-pinned axes in
+  one batched pass and picks the best valid raw, earliest on ties.
+* ``exhaustive_search`` / ``random_sweep`` are the device-native callers:
+  candidates generated on the GPU (``ls_sweep``), no per-candidate traffic —
+  the whole 2.0e9-point 1.2T space in milliseconds.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+import time
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .env import SearchEnv
+from .evaluator import Elite, Evaluator
+from .generator import GEN_ENUM, GEN_ENUM_ADMISSIBLE, GEN_UNIFORM
+from .knobs import SaConfig
+from .report import SearchReport, build_report
+from .strategy import ActionSpaceSpec, canonical_fused_ops, megatron_fine_dims
+
+__all__ = ["NoValidConfiguration", "SaConfig", "uniform_vector", "mutate_vector", "acceptance_probability",
+           "cosine_decay", "random_walk", "simulated_annealing", "megatron_exhaustive", "SweepReport",
+           "exhaustive_search", "random_sweep"]
+
+
+class NoValidConfiguration(RuntimeError):
+    """An exhaustive sweep found nothing that passes the validity gates."""
+
+
+def cosine_decay(initial: float, progress: float) -> float:
+    """Cosine decay from ``initial`` at progress 0 to 0 at 1 (reference ppo.py:164-167)."""
+    clamped = min(max(progress, 0.0), 1.0)
+    return initial * 0.5 * (1.0 + math.cos(math.pi * clamped))
+
+
+def uniform_vector(space: ActionSpaceSpec, rng: np.random.Generator) -> tuple[int, ...]:
+    return tuple(int(rng.integers(k)) for k in space.head_sizes)
+
+
+def mutate_vector(vector, space: ActionSpaceSpec, rng: np.random.Generator, moves: int = 1) -> tuple[int, ...]:
+    mutable = [i for i, k in enumerate(space.head_sizes) if k > 1]
+    if not mutable:
+        return tuple(vector)
+    picks = rng.choice(len(mutable), size=min(moves, len(mutable)), replace=False)
+    out = list(vector)
+    for pick in np.atleast_1d(picks):
+        coord = mutable[int(pick)]
+        drawn = int(rng.integers(space.head_sizes[coord] - 1))
+        out[coord] = drawn if drawn < out[coord] else drawn + 1
+    return tuple(out)
+
+
+def acceptance_probability(delta: float, temperature: float) -> float:
+    if delta >= 0:
+        return 1.0
+    if temperature <= 0:
+        return 0.0
+    return math.exp(delta / temperature)
+
+
+def random_walk(env: SearchEnv, budget: int, seed: int) -> SearchReport:
+    """Budget-many i.i.d. uniform samples, best by reward — one GPU pass."""
+    if budget < 1:
+        raise ValueError("random walk budget must be >= 1")
+    start = time.perf_counter()
+    rng = np.random.default_rng(seed)
+    vectors = np.asarray([uniform_vector(env.space, rng) for _ in range(budget)], dtype=np.int64)
+    first = env.evals_used
+    env.step_batch(vectors)
+    records = env.eval_log[first:first + budget]
+    return build_report("rw", seed, records, (), budget, time.perf_counter() - start)
+
+
+def simulated_annealing(env: SearchEnv, cfg: SaConfig, budget: int, seed: int) -> SearchReport:
+    """Single-chain annealing on the shaped reward, cosine temperature."""
+    if budget < 1:
+        raise ValueError("simulated annealing budget must be >= 1")
+    start = time.perf_counter()
+    rng = np.random.default_rng(seed)
+    first = env.evals_used
+    current = uniform_vector(env.space, rng)
+    current_reward, _, _ = env.step(current)
+    for step in range(1, budget):
+        temperature = cosine_decay(cfg.t_initial, step / budget)
+        candidate = mutate_vector(current, env.space, rng, cfg.neighbor_moves)
+        candidate_reward, _, _ = env.step(candidate)
+        if rng.random() < acceptance_probability(candidate_reward - current_reward, temperature):
+            current, current_reward = candidate, candidate_reward
+    records = env.eval_log[first:first + budget]
+    return build_report("sa", seed, records, (), budget, time.perf_counter() - start)
+
+
+def megatron_exhaustive(env_factory: Callable[[int], SearchEnv], space: ActionSpaceSpec) -> SearchReport:
+    """Every coarse degree tuple with Megatron-pinned axes, best valid by raw."""
+    grid_size = len(space.tp_domain) * len(space.ep_domain) * len(space.pp_domain) * len(space.batch_domain)
+    start = time.perf_counter()
+    with env_factory(grid_size) as env:
+        if env.space != space:
+            raise ValueError("env_factory produced an environment over a different space")
+        ops = canonical_fused_ops(env.model)
+        dims = dict(zip((op.name for op in ops), megatron_fine_dims(ops)))
+        tail = tuple(int(dims[name]) for name in space.op_names)
+        grid = itertools.product(*(range(k) for k in space.head_sizes[:4]))
+        env.step_batch(np.asarray([c + tail for c in grid], dtype=np.int64))
+        records = env.eval_log[-grid_size:]
+        if not any(r.valid for r in records):
+            raise NoValidConfiguration(f"no valid configuration among {grid_size} megatron-pinned points")
+    return build_report("exhaustive", None, records, (), grid_size, time.perf_counter() - start, by_raw=True)
+
+
+@dataclass(frozen=True)
+class SweepReport:
+    """Outcome of a device-native sweep: the elite by raw, best first."""
+
+    mode: int
+    evaluated: int
+    elites: tuple[Elite, ...]
+    device_ms: float
+
+    @property
+    def best(self) -> Elite | None:
+        return self.elites[0] if self.elites else None
+
+
+def _sweep(ev: Evaluator, mode: int, n: int, start: int, seed: int, k: int, chunk: int) -> SweepReport:
+    import torch
+
+    recs, counts = [], []
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(torch.cuda.current_stream(ev.device))
+    for lo in range(start, start + n, chunk):
+        r, c = ev.sweep(mode, min(chunk, start + n - lo), start=lo, seed=seed, k=k)
+        recs.append(r)
+        counts.append(c)
+    if len(recs) > 1:
+        r, c = ev.merge_records(torch.cat(recs), torch.cat(counts), k, k)
+    else:
+        r, c = recs[0], counts[0]
+    t1.record(torch.cuda.current_stream(ev.device))
+    elites = ev.decode_records(r, c)
+    return SweepReport(mode, n, tuple(elites), t0.elapsed_time(t1))
+
+
+def exhaustive_search(ev: Evaluator, admissible_only: bool = False, k: int = 8,
+                      chunk: int = 1 << 34) -> SweepReport:
+    """Score the whole action space (or its admissible-axis subspace) on the GPU;
+    the elite by raw, earliest itertools.product position on ties."""
+    mode = GEN_ENUM_ADMISSIBLE if admissible_only else GEN_ENUM
+    return _sweep(ev, mode, ev.stream_size(mode), 0, 0, k, chunk)
+
+
+def random_sweep(ev: Evaluator, n: int, seed: int = 0, k: int = 8, chunk: int = 1 << 34) -> SweepReport:
+    """n i.i.d. uniform candidates generated on the GPU (counter-based stream)."""
+    return _sweep(ev, GEN_UNIFORM, n, 0, seed, k, chunk)
