@@ -48,7 +48,7 @@ def main():
         meta[f"{name}_exhaustive"] = {"best_vector": list(rep.best_vector), "best_raw": rep.best_raw,
                                       "best_reward": rep.best_reward, "evals": rep.evals}
         print(name, "exhaustive", rep.best_raw, rep.best_vector)
-    np.savez_compressed(OUT / "search_baselines.npz", meta=np.asarray(json.dumps(meta)), **payload)
+    np.savez_compressed(OUT / "baselines_reference.npz", meta=np.asarray(json.dumps(meta)), **payload)
 
 
 if __name__ == "__main__":

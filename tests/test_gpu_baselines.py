@@ -1,5 +1,5 @@
 """Batched search baselines vs the reference's own runs
-(tests/golden/search_baselines.npz, made by make_golden_search.py):
+(tests/golden/baselines_reference.npz, made by make_golden_search.py):
 random_walk and simulated_annealing consume the same numpy PCG64 stream, so
 every record must match bit for bit; megatron_exhaustive picks the same
 winner; the device-native exhaustive sweep finds the global optimum."""
@@ -13,7 +13,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-GOLD = Path(__file__).resolve().parent / "golden" / "search_baselines.npz"
+GOLD = Path(__file__).resolve().parent / "golden" / "baselines_reference.npz"
 
 
 @pytest.fixture(scope="module")
