@@ -230,6 +230,33 @@ int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                   ls_elite_rec* out, int32_t* count_out, void* stream);
 
+/* ---- Search-loop step (device-resident environment state) ---------------
+ * One sequential environment step of a learning search, entirely on the
+ * device so a whole search round can be captured in a CUDA graph:
+ *   SearchEnv.step (env.py:134-180: score, Eq.-1 reward against the best raw
+ *   seen strictly before, flat penalty when invalid, best update, eval-log
+ *   append) and the valid-only EliteBuffer.offer (policy.py:86-102: reject
+ *   duplicates, reject reward <= min when full, stable insert by reward desc).
+ * The action is `A` int64 indices on the device. All state pointers are
+ * device memory owned by the caller. Writes the step's reward to
+ * *reward_out. If *log_pos >= log_capacity nothing is scored and the
+ * step's reason is LS_REASON_DECODE_ERROR with reward NaN (budget guard). */
+typedef struct ls_search_state {
+  double* best_raw;      /* [1] env.best_raw */
+  int64_t* elite_vec;    /* [elite_capacity * A], best first */
+  double* elite_reward;  /* [elite_capacity]; -inf marks an empty slot */
+  int32_t elite_capacity;
+  int64_t* log_pos;      /* [1] next eval-log slot (= evaluations done) */
+  int64_t log_capacity;
+  uint8_t* log_vec;      /* [log_capacity * A] */
+  double* log_raw;       /* [log_capacity] raw (0 when invalid) */
+  double* log_reward;    /* [log_capacity] */
+  uint8_t* log_reason;   /* [log_capacity] LS_REASON_* */
+  double alpha, beta, penalty;
+} ls_search_state;
+
+int ls_env_step(ls_ctx* ctx, const ls_search_state* state, const int64_t* action, double* reward_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

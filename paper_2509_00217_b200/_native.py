@@ -53,6 +53,26 @@ class ResultSoA(ctypes.Structure):
     ]
 
 
+class SearchState(ctypes.Structure):
+    """ls_search_state: device-resident environment + elite + eval-log state."""
+
+    _fields_ = [
+        ("best_raw", ctypes.c_void_p),
+        ("elite_vec", ctypes.c_void_p),
+        ("elite_reward", ctypes.c_void_p),
+        ("elite_capacity", ctypes.c_int32),
+        ("log_pos", ctypes.c_void_p),
+        ("log_capacity", ctypes.c_int64),
+        ("log_vec", ctypes.c_void_p),
+        ("log_raw", ctypes.c_void_p),
+        ("log_reward", ctypes.c_void_p),
+        ("log_reason", ctypes.c_void_p),
+        ("alpha", ctypes.c_double),
+        ("beta", ctypes.c_double),
+        ("penalty", ctypes.c_double),
+    ]
+
+
 class EliteRec(ctypes.Structure):
     _fields_ = [
         ("key", ctypes.c_double),
@@ -95,6 +115,8 @@ _SIGS = {
                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ls_topk_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ls_env_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SearchState), ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

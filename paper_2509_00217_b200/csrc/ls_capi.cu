@@ -517,6 +517,18 @@ int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge launch");
 }
 
+int ls_env_step(ls_ctx* c, const ls_search_state* st, const int64_t* action, double* reward_out, void* stream) {
+  g_err.clear();
+  if (!c || !st || !action || !reward_out) return fail(LS_ERR_INVALID_ARGUMENT, "null env_step argument");
+  if (!st->best_raw || !st->log_pos || !st->log_vec || !st->log_raw || !st->log_reward || !st->log_reason ||
+      st->log_capacity < 0 || st->elite_capacity < 1 || !st->elite_vec || !st->elite_reward)
+    return fail(LS_ERR_INVALID_ARGUMENT, "incomplete search state");
+  DeviceGuard g(c->device);
+  cudaError_t e = launch_env_step(c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, *st, action, reward_out,
+                                  static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "env_step launch");
+}
+
 uint64_t ls_stream_size(ls_ctx* c, int mode) {
   if (!c || mode < LS_GEN_UNIFORM || mode > LS_GEN_ENUM_ADMISSIBLE) return 0;
   std::lock_guard<std::mutex> lock(c->gen_mu);

@@ -85,4 +85,8 @@ cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, i
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);
 
+// Search-loop environment step (ls_search.cu)
+cudaError_t launch_env_step(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
+                            const ls_search_state& S, const int64_t* action, double* reward_out, cudaStream_t s);
+
 }  // namespace ls

@@ -1,0 +1,284 @@
+"""Chunked PPO strategy search on the GPU (reference pkg/src/shardsearch/ppo.py).
+
+Same algorithm and protocol as the reference's ``run_search`` (:466-528):
+one-step episodes, the elite buffer (capacity ``history_len``) as the
+observation, ``n_steps`` samples per rollout, ``epochs_per_update`` clipped-PPO
+epochs with Adam under a cosine learning rate (:164-167, :297-327), an
+early exit once every head is confident (:356-358), fresh parameters and
+optimizer per chunk with unspent allowance rolled forward (:489-518), and
+exactly ``budget`` evaluations.
+
+What is B200-native:
+
+* Every sample, update and confidence check runs on the device. The env
+  step — strategy scoring, Eq.-1 reward against the running best, eval-log
+  append and the elite-buffer offer — is one fused kernel (``ls_env_step``),
+  so nothing per-sample crosses PCIe; the host reads one status word per
+  round (the early-exit / numerics flag).
+* One PPO round (sample, step, sample, step, two update epochs, confidence)
+  is captured once into a CUDA graph and replayed; per-round inputs (the
+  learning rate, the uniform draws) are indexed on the device from a
+  chunk-local counter.
+* The uniform stream is the reference's: one numpy PCG64 generator drives
+  parameter initialisation and one ``random()`` per head per sample, in the
+  reference's order. Each chunk pre-draws its allowance's worth of uniforms and
+  rewinds the generator to the position the reference would have reached, so
+  later chunks see the same draws as the reference's restarts. The sampled
+  trajectory therefore equals the reference's for as long as the float64
+  probabilities agree — they differ only in BLAS rounding order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _native
+from .baselines import cosine_decay
+from .env import EvalRecord, SearchEnv
+from .evaluator import REASON_NAMES
+from .knobs import PpoConfig
+from .policy import NumericsError, TorchPolicy, sample_actions
+from .report import SearchReport, build_report
+from .strategy import DecodingError, canonical_fused_ops
+
+__all__ = ["PpoConfig", "ChunkExit", "ChunkOutcome", "GpuSearch", "ppo_loss", "run_search"]
+
+_CONFIDENT, _NONFINITE = 1, 2
+
+
+class ChunkExit(str, Enum):
+    EXHAUSTED = "exhausted"
+    EARLY_EXIT = "early_exit"
+
+
+@dataclass(frozen=True)
+class ChunkOutcome:
+    exit: ChunkExit
+    evals_used: int
+
+
+def ppo_loss(pol: TorchPolicy, obs, act, logp_old, value_old, reward, cfg: PpoConfig) -> torch.Tensor:
+    """Clipped-surrogate PPO loss over a rollout batch (reference loss_and_grads,
+    ppo.py:203-294): per sample -min(rho*A, clip(rho)*A) + value_coef*(v - r)^2
+    - entropy_coef*H, averaged; A = reward - value_old. Its autograd gradient is
+    the reference's hand-written one (the unclipped branch carries the
+    gradient on ties, the clamped branch is constant outside the band)."""
+    n = obs.shape[0]
+    log_probs, probs, value = pol(obs)
+    logp_new = log_probs.gather(2, act.unsqueeze(2)).sum(dim=(1, 2))
+    entropy = pol.entropy(log_probs, probs)
+    ratio = torch.exp(logp_new - logp_old)
+    advantage = reward - value_old
+    unclipped = ratio * advantage
+    clamped = ratio.clamp(1.0 - cfg.clip_eps, 1.0 + cfg.clip_eps) * advantage
+    surrogate = torch.where(unclipped <= clamped, unclipped, clamped)
+    err = value - reward
+    return (-surrogate / n).sum() + (cfg.value_coef * err * err / n).sum() - cfg.entropy_coef * (entropy / n).sum()
+
+
+class GpuSearch:
+    """Device-resident state of one PPO search over ``env``."""
+
+    def __init__(self, env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True) -> None:
+        if env.budget_left < cfg.budget:
+            raise ValueError(f"environment has {env.budget_left} evals left, need {cfg.budget}")
+        self.env, self.cfg, self.seed = env, cfg, seed
+        ev = env.evaluator
+        self.ev = ev
+        dev = self.device = ev.device
+        self.rng = np.random.default_rng(seed)
+        self.policy = TorchPolicy(env.space, canonical_fused_ops(env.model), history_len=cfg.history_len,
+                                  width=cfg.width, ffn_width=cfg.ffn_width, device=dev)
+        self.H = H = env.space.vector_length
+        T, B = cfg.history_len, cfg.budget
+        f64 = dict(dtype=torch.float64, device=dev)
+        i64 = dict(dtype=torch.int64, device=dev)
+        # environment / elite / log state (ls_search_state)
+        self.best = torch.tensor([env.best_raw], **f64)
+        self.elite_vec = torch.zeros((T, H), **i64)
+        self.elite_reward = torch.full((T,), float("-inf"), **f64)
+        self.log_pos = torch.zeros(1, **i64)
+        self.log_vec = torch.zeros((B, H), dtype=torch.uint8, device=dev)
+        self.log_raw = torch.zeros(B, **f64)
+        self.log_reward = torch.zeros(B, **f64)
+        self.log_reason = torch.zeros(B, dtype=torch.uint8, device=dev)
+        rc = env.reward_cfg
+        self._state = _native.SearchState(self.best.data_ptr(), self.elite_vec.data_ptr(), self.elite_reward.data_ptr(),
+                                          T, self.log_pos.data_ptr(), B, self.log_vec.data_ptr(),
+                                          self.log_raw.data_ptr(), self.log_reward.data_ptr(),
+                                          self.log_reason.data_ptr(), rc.alpha, rc.beta, rc.invalid_penalty)
+        # chunk-local inputs, indexed on the device by the chunk's sample counter
+        self.spent = torch.zeros(1, **i64)
+        self.uniforms = torch.zeros(B * H, **f64)
+        self.lr_table = torch.zeros(B, **f64)
+        self.lr = torch.zeros((), **f64)
+        self.head_offsets = torch.arange(H, **i64)
+        self.size_cap = self.policy.sizes - 1
+        # rollout batch
+        n = cfg.n_steps
+        self.b_obs = torch.zeros((n, T, H), **f64)
+        self.b_act = torch.zeros((n, H), **i64)
+        self.b_logp = torch.zeros(n, **f64)
+        self.b_value = torch.zeros(n, **f64)
+        self.b_reward = torch.zeros(n, **f64)
+        self.action = torch.zeros(H, **i64)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.opt = torch.optim.Adam(self.policy.parameters(), lr=self.lr, betas=(0.9, 0.999), eps=1e-8,
+                                    capturable=True, foreach=True)
+        self.use_graphs = use_graphs
+        self.stream = torch.cuda.Stream(device=dev)
+        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self._eager_rounds: dict[int, int] = {}
+        self._lib = _native.lib(require_gpu=True)
+        self.rounds = 0
+
+    # -- one round (graph-capturable: no host syncs, static shapes) ----------
+
+    def _sample_and_step(self, j: int) -> None:
+        pol, H = self.policy, self.H
+        obs = pol.observation(self.elite_vec, self.elite_reward)
+        with torch.no_grad():
+            log_probs, probs, value = pol(obs)
+            u = self.uniforms.index_select(0, self.spent * H + self.head_offsets)
+            act = sample_actions(probs, u, self.size_cap)
+            self.b_obs[j].copy_(obs)
+            self.b_act[j].copy_(act)
+            self.action.copy_(act)
+            self.b_logp[j:j + 1].copy_(log_probs.gather(1, act.unsqueeze(1)).sum().reshape(1))
+            self.b_value[j:j + 1].copy_(value.reshape(1))
+        _native.check(self._lib.ls_env_step(self.ev._ctx, ctypes.byref(self._state), ctypes.c_void_p(self.action.data_ptr()),
+                                            ctypes.c_void_p(self.b_reward.data_ptr() + 8 * j),
+                                            ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+        self.spent.add_(1)
+
+    def _update(self, n: int) -> torch.Tensor:
+        cfg, pol = self.cfg, self.policy
+        obs, act = self.b_obs[:n], self.b_act[:n]
+        logp_old, value_old, reward = self.b_logp[:n], self.b_value[:n], self.b_reward[:n]
+        bad = ~(torch.isfinite(reward) & torch.isfinite(value_old) & torch.isfinite(logp_old)).all()
+        for _ in range(cfg.epochs_per_update):
+            loss = ppo_loss(pol, obs, act, logp_old, value_old, reward, cfg)
+            loss.backward()
+            self.opt.step()
+            self.opt.zero_grad(set_to_none=False)
+            bad = bad | ~torch.isfinite(loss)
+        norms = torch._foreach_norm(list(pol.parameters()), float("inf"))
+        return bad | ~torch.isfinite(torch.stack(norms)).all()
+
+    def _round(self, n: int) -> None:
+        self.lr.copy_(self.lr_table.index_select(0, self.spent).reshape(()))
+        for j in range(n):
+            self._sample_and_step(j)
+        bad = self._update(n)
+        with torch.no_grad():
+            _, probs, _ = self.policy(self.policy.observation(self.elite_vec, self.elite_reward))
+            confident = (self.policy.confidence(probs) >= self.cfg.tau).all()
+        self.status.copy_((confident.int() * _CONFIDENT + bad.int() * _NONFINITE).reshape(1))
+
+    def _run_round(self, n: int) -> int:
+        """One round (replayed graph once warm); returns the status word."""
+        g = self._graphs.get(n)
+        if g is not None:
+            g.replay()
+        else:
+            self._round(n)
+            if self.use_graphs:
+                self._eager_rounds[n] = self._eager_rounds.get(n, 0) + 1
+                if self._eager_rounds[n] >= 3:  # warm (autograd, cuBLAS, Adam state) -> capture
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=self.stream):
+                        self._round(n)
+                    self._graphs[n] = g
+        self.rounds += 1
+        self.status_host.copy_(self.status, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return int(self.status_host[0])
+
+    # -- chunk protocol (reference run_chunk :330-359, run_search :466-528) ---
+
+    def _start_chunk(self, allowance: int) -> None:
+        self.policy.reset_parameters(self.rng)  # the reference's PolicyNetwork(rng=rng)
+        for st in self.opt.state.values():  # fresh optimizer
+            for v in st.values():
+                v.zero_()
+        self._rng_mark = self.rng.bit_generator.state
+        draws = self.rng.random(allowance * self.H)
+        self.uniforms[: draws.size].copy_(torch.from_numpy(draws))
+        lrs = np.array([cosine_decay(self.cfg.lr_initial, s / allowance) for s in range(allowance)])
+        self.lr_table[:allowance].copy_(torch.from_numpy(lrs))
+        self.spent.zero_()
+
+    def _end_chunk(self, spent: int) -> None:
+        self.rng.bit_generator.state = self._rng_mark
+        self.rng.random(spent * self.H)  # leave the generator where the reference's would be
+
+    def run_chunk(self, allowance: int) -> ChunkOutcome:
+        if allowance < 1:
+            raise ValueError("chunk allowance must be >= 1")
+        self._start_chunk(allowance)
+        spent = 0
+        outcome = ChunkExit.EXHAUSTED
+        while spent < allowance:
+            n = min(self.cfg.n_steps, allowance - spent)
+            status = self._run_round(n)
+            spent += n
+            if status & _NONFINITE:
+                raise NumericsError("non-finite loss or parameters in a PPO update")
+            if status & _CONFIDENT:
+                outcome = ChunkExit.EARLY_EXIT
+                break
+        self._end_chunk(spent)
+        return ChunkOutcome(outcome, spent)
+
+    def run(self) -> tuple[list[int], int]:
+        cfg = self.cfg
+        restarts, evals_done, carry = [], 0, 0
+        with torch.cuda.stream(self.stream):
+            for base in [cfg.budget // cfg.chunks] * cfg.chunks:
+                allowance = base + carry
+                restarts.append(evals_done)
+                out = self.run_chunk(allowance)
+                evals_done += out.evals_used
+                carry = allowance - out.evals_used
+            while carry > 0:  # early exit in the last chunk: extra restarts spend the rest
+                allowance = carry
+                restarts.append(evals_done)
+                out = self.run_chunk(allowance)
+                evals_done += out.evals_used
+                carry = allowance - out.evals_used
+        self.stream.synchronize()
+        return restarts, evals_done
+
+    def records(self, first_index: int, count: int) -> list[EvalRecord]:
+        vec = self.log_vec[:count].cpu().numpy()
+        raw = self.log_raw[:count].cpu().numpy()
+        rew = self.log_reward[:count].cpu().numpy()
+        why = self.log_reason[:count].cpu().numpy()
+        if (why == 255).any():
+            raise DecodingError(f"sampled vector {vec[int(np.argmax(why == 255))].tolist()} failed to decode")
+        return [EvalRecord(first_index + i, tuple(int(x) for x in vec[i]), float(raw[i]), float(rew[i]),
+                           bool(why[i] == 0), REASON_NAMES[int(why[i])]) for i in range(count)]
+
+
+def run_search(env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True) -> SearchReport:
+    """Full chunked-restart PPO search on the GPU; consumes exactly ``cfg.budget`` evals.
+
+    Appends the eval records to ``env`` (and its NDJSON sink) when the search
+    ends and leaves ``env.best_raw`` where the reference's would be.
+    """
+    start = time.perf_counter()
+    search = GpuSearch(env, cfg, seed, use_graphs=use_graphs)
+    restarts, evals_done = search.run()
+    first = env.evals_used
+    records = search.records(first, evals_done)
+    for r in records:
+        env._append(r)
+    env.best_raw = float(search.best.item())
+    return build_report("ppo", seed, records, restarts, cfg.budget, time.perf_counter() - start)
