@@ -257,6 +257,83 @@ typedef struct ls_search_state {
 
 int ls_env_step(ls_ctx* ctx, const ls_search_state* state, const int64_t* action, double* reward_out, void* stream);
 
+/* ---- Fused PPO search rounds ---------------------------------------------
+ * The reference's elite-conditioned policy (policy.py:213-499: embedding,
+ * one post-norm single-head attention block, mean pool, masked categorical
+ * heads, value head) and its chunked PPO loop (ppo.py:170-359) as float64
+ * device kernels: sampling (inverse CDF on caller-supplied uniforms,
+ * policy.py:205-210), the env step above, the clipped-surrogate loss with
+ * its exact gradient (ppo.py:203-294), backward, and Adam (ppo.py:130-161).
+ *
+ * Parameters live in ONE float64 arena in the layout ls_policy_layout_of
+ * returns (reference names in LS_PSEG_* order; q/k/v packed as [d, 3d],
+ * heads packed as [d, heads*kmax] with zero padding columns). Every pointer
+ * below is device memory owned by the caller. */
+enum {
+  LS_PSEG_EMBED_W = 0, LS_PSEG_EMBED_B, LS_PSEG_WQKV, LS_PSEG_BQKV, LS_PSEG_WO, LS_PSEG_BO,
+  LS_PSEG_LN1_G, LS_PSEG_LN1_B, LS_PSEG_FFN_W1, LS_PSEG_FFN_B1, LS_PSEG_FFN_W2, LS_PSEG_FFN_B2,
+  LS_PSEG_LN2_G, LS_PSEG_LN2_B, LS_PSEG_HEAD_W, LS_PSEG_HEAD_B, LS_PSEG_VALUE_W1, LS_PSEG_VALUE_B1,
+  LS_PSEG_VALUE_W2, LS_PSEG_VALUE_B2, LS_PSEG_COUNT
+};
+
+typedef struct ls_policy_dims {
+  int32_t obs_dim;     /* vector_length (= number of heads) */
+  int32_t width;       /* d */
+  int32_t ffn_width;   /* f */
+  int32_t history_len; /* T, observation rows */
+  int32_t num_heads;
+  int32_t kmax;        /* largest head size */
+  int32_t n_steps;     /* rollout samples per update */
+} ls_policy_dims;
+
+typedef struct ls_policy_layout {
+  int64_t off[LS_PSEG_COUNT]; /* element offsets into the arena */
+  int64_t total;              /* arena length in doubles */
+} ls_policy_layout;
+
+int ls_policy_layout_of(const ls_policy_dims* dims, ls_policy_layout* out);
+/* Scratch for activations and their gradients; 0 if dims are unsupported
+ * (n_steps * history_len > 16, or a stage's shared-memory staging > 160 KB). */
+size_t ls_ppo_workspace_bytes(const ls_policy_dims* dims);
+
+typedef struct ls_ppo_plan {
+  ls_policy_dims dims;
+  double* params;          /* arena */
+  double* adam_m;          /* arena-shaped first moments */
+  double* adam_v;          /* arena-shaped second moments */
+  double* grad_out;        /* optional arena-shaped gradient of the last epoch (tests) */
+  void* workspace;         /* ls_ppo_workspace_bytes */
+  const uint8_t* blocked;  /* [num_heads * kmax] 1 = inadmissible or padding */
+  const int32_t* head_size;/* [num_heads] */
+  const double* obs_denom; /* [obs_dim] max(k - 1, 1) */
+  ls_search_state env;
+  const double* uniforms;  /* chunk's draws, num_heads per sample, indexed by *spent */
+  const double* lr_table;  /* chunk's learning rate, indexed by samples spent before the update */
+  int64_t* spent;          /* [1] samples taken in this chunk */
+  int64_t* adam_step;      /* [1] Adam step count of this chunk's optimizer */
+  int32_t* status;         /* [1] bit 0 every head confident, bit 1 non-finite loss/params */
+  double* batch_obs;       /* [n_steps * history_len * obs_dim] */
+  int64_t* batch_action;   /* [n_steps * num_heads] */
+  double* batch_logp;      /* [n_steps] */
+  double* batch_value;     /* [n_steps] */
+  double* batch_reward;    /* [n_steps] */
+  double tau, clip_eps, value_coef, entropy_coef, beta1, beta2, adam_eps;
+  int32_t epochs;
+} ls_ppo_plan;
+
+/* Forward of the current observation into sample slot 0 (after a parameter
+ * reset: the next round's first sample reads it). */
+int ls_ppo_prime(ls_ctx* ctx, const ls_ppo_plan* plan, void* stream);
+/* One round (run_chunk loop body, ppo.py:350-358): n samples (each: sample,
+ * env step, elite offer), `epochs` PPO updates, then the confidence check of
+ * the new parameters on the current observation, which also primes the next
+ * round's first sample. Capturable in a CUDA graph. */
+int ls_ppo_round(ls_ctx* ctx, const ls_ppo_plan* plan, int n, void* stream);
+/* Tests: forward of batch_obs slots [0, n) -> log-probs [n, heads*kmax] and values [n]. */
+int ls_ppo_forward(ls_ctx* ctx, const ls_ppo_plan* plan, int n, double* logp_out, double* value_out, void* stream);
+/* Tests: `epochs` updates on the batch_* arrays as given (no sampling). */
+int ls_ppo_update(ls_ctx* ctx, const ls_ppo_plan* plan, int n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

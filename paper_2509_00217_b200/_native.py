@@ -73,6 +73,31 @@ class SearchState(ctypes.Structure):
     ]
 
 
+PSEG_COUNT = 20
+
+
+class PolicyDims(ctypes.Structure):
+    _fields_ = [("obs_dim", ctypes.c_int32), ("width", ctypes.c_int32), ("ffn_width", ctypes.c_int32),
+                ("history_len", ctypes.c_int32), ("num_heads", ctypes.c_int32), ("kmax", ctypes.c_int32),
+                ("n_steps", ctypes.c_int32)]
+
+
+class PolicyLayout(ctypes.Structure):
+    _fields_ = [("off", ctypes.c_int64 * PSEG_COUNT), ("total", ctypes.c_int64)]
+
+
+class PpoPlan(ctypes.Structure):
+    """ls_ppo_plan: every pointer is device memory."""
+
+    _fields_ = [("dims", PolicyDims)] + [(n, ctypes.c_void_p) for n in (
+        "params", "adam_m", "adam_v", "grad_out", "workspace", "blocked", "head_size", "obs_denom")] + [
+        ("env", SearchState)] + [(n, ctypes.c_void_p) for n in (
+            "uniforms", "lr_table", "spent", "adam_step", "status", "batch_obs", "batch_action", "batch_logp",
+            "batch_value", "batch_reward")] + [(n, ctypes.c_double) for n in (
+                "tau", "clip_eps", "value_coef", "entropy_coef", "beta1", "beta2", "adam_eps")] + [
+        ("epochs", ctypes.c_int32)]
+
+
 class EliteRec(ctypes.Structure):
     _fields_ = [
         ("key", ctypes.c_double),
@@ -117,6 +142,13 @@ _SIGS = {
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ls_env_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SearchState), ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p]),
+    "ls_policy_layout_of": (ctypes.c_int, [ctypes.POINTER(PolicyDims), ctypes.POINTER(PolicyLayout)]),
+    "ls_ppo_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(PolicyDims)]),
+    "ls_ppo_prime": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PpoPlan), ctypes.c_void_p]),
+    "ls_ppo_round": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PpoPlan), ctypes.c_int, ctypes.c_void_p]),
+    "ls_ppo_forward": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PpoPlan), ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]),
+    "ls_ppo_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PpoPlan), ctypes.c_int, ctypes.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -529,6 +529,76 @@ int ls_env_step(ls_ctx* c, const ls_search_state* st, const int64_t* action, dou
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "env_step launch");
 }
 
+int ls_policy_layout_of(const ls_policy_dims* dims, ls_policy_layout* out) {
+  g_err.clear();
+  if (!dims || !out || !ppo_layout(*dims, out)) return fail(LS_ERR_INVALID_ARGUMENT, "bad policy dims");
+  return LS_OK;
+}
+
+size_t ls_ppo_workspace_bytes(const ls_policy_dims* dims) { return dims ? ppo_workspace_bytes(*dims) : 0; }
+
+static int ppo_check(ls_ctx* c, const ls_ppo_plan* p, int n) {
+  if (!c || !p) return fail(LS_ERR_INVALID_ARGUMENT, "null context or plan");
+  if (ppo_workspace_bytes(p->dims) == 0)
+    return fail(LS_ERR_UNSUPPORTED, "policy dims unsupported by the fused kernels (n_steps*history_len > 16, "
+                                    "heads != obs_dim, or shared-memory staging too large)");
+  if (p->dims.obs_dim != c->desc.vector_length) return fail(LS_ERR_INVALID_ARGUMENT, "obs_dim != vector_length");
+  if (n < 1 || n > p->dims.n_steps) return fail(LS_ERR_INVALID_ARGUMENT, "n must be in [1, n_steps]");
+  if (!p->params || !p->adam_m || !p->adam_v || !p->workspace || !p->blocked || !p->head_size || !p->obs_denom ||
+      !p->spent || !p->adam_step || !p->status || !p->batch_obs || !p->batch_action || !p->batch_logp ||
+      !p->batch_value || !p->batch_reward || !p->lr_table || p->epochs < 1)
+    return fail(LS_ERR_INVALID_ARGUMENT, "incomplete ppo plan");
+  return LS_OK;
+}
+
+static PpoCtx ppo_ctx(const ls_ctx* c) {
+  PpoCtx x;
+  x.tab = c->d_tab;
+  x.L = c->L;
+  x.M = c->M;
+  x.neumaier = c->desc.sum_mode == LS_SUM_NEUMAIER;
+  return x;
+}
+
+int ls_ppo_prime(ls_ctx* c, const ls_ppo_plan* p, void* stream) {
+  g_err.clear();
+  int rc = ppo_check(c, p, 1);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  cudaError_t e = ppo_prime(*p, ppo_ctx(c), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "ppo_prime");
+}
+
+int ls_ppo_round(ls_ctx* c, const ls_ppo_plan* p, int n, void* stream) {
+  g_err.clear();
+  int rc = ppo_check(c, p, n);
+  if (rc) return rc;
+  if (!p->uniforms || !p->env.best_raw || !p->env.log_pos || !p->env.elite_vec || !p->env.elite_reward)
+    return fail(LS_ERR_INVALID_ARGUMENT, "incomplete search state");
+  DeviceGuard g(c->device);
+  cudaError_t e = ppo_round(*p, ppo_ctx(c), n, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "ppo_round");
+}
+
+int ls_ppo_forward(ls_ctx* c, const ls_ppo_plan* p, int n, double* logp_out, double* value_out, void* stream) {
+  g_err.clear();
+  int rc = ppo_check(c, p, n);
+  if (rc) return rc;
+  if (!logp_out || !value_out) return fail(LS_ERR_INVALID_ARGUMENT, "null output");
+  DeviceGuard g(c->device);
+  cudaError_t e = ppo_forward(*p, ppo_ctx(c), n, logp_out, value_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "ppo_forward");
+}
+
+int ls_ppo_update(ls_ctx* c, const ls_ppo_plan* p, int n, void* stream) {
+  g_err.clear();
+  int rc = ppo_check(c, p, n);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  cudaError_t e = ppo_update(*p, ppo_ctx(c), n, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "ppo_update");
+}
+
 uint64_t ls_stream_size(ls_ctx* c, int mode) {
   if (!c || mode < LS_GEN_UNIFORM || mode > LS_GEN_ENUM_ADMISSIBLE) return 0;
   std::lock_guard<std::mutex> lock(c->gen_mu);

@@ -89,4 +89,18 @@ cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, i
 cudaError_t launch_env_step(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
                             const ls_search_state& S, const int64_t* action, double* reward_out, cudaStream_t s);
 
+// Fused PPO rounds (ls_policy.cu)
+struct PpoCtx {
+  const uint64_t* tab;
+  TabLayout L;
+  EvalMeta M;
+  bool neumaier;
+};
+bool ppo_layout(const ls_policy_dims& D, ls_policy_layout* out);
+size_t ppo_workspace_bytes(const ls_policy_dims& D);
+cudaError_t ppo_prime(const ls_ppo_plan& p, const PpoCtx& c, cudaStream_t s);
+cudaError_t ppo_round(const ls_ppo_plan& p, const PpoCtx& c, int n, cudaStream_t s);
+cudaError_t ppo_forward(const ls_ppo_plan& p, const PpoCtx& c, int n, double* logp, double* value, cudaStream_t s);
+cudaError_t ppo_update(const ls_ppo_plan& p, const PpoCtx& c, int n, cudaStream_t s);
+
 }  // namespace ls

@@ -1,21 +1,8 @@
-// ls_search.cu — one environment step of a learning search, on the device.
-//
-// Fuses what the reference does in Python per sampled action:
-//   SearchEnv.step (env.py:152-180): score the strategy, Eq.-1 reward
-//     alpha*raw + beta*(raw - best) against the best raw seen strictly
-//     before, flat penalty when invalid, best update after the reward,
-//     eval-log append;
-//   EliteBuffer.offer (policy.py:86-102), valid strategies only: reject a
-//     duplicate vector, reject reward <= min when full, else insert after
-//     every entry with reward >= the newcomer's (the reference's stable sort).
-// One thread does the work: the step is strictly sequential (the next
-// action's observation depends on this step's elite update), and a single
-// candidate's gate + fp64 path is ~1 us. What matters is that the whole
-// search round stays on the device and can be graph-captured.
+// ls_search.cu — standalone launch of the search-loop environment step
+// (ls_envstep.cuh); the fused PPO round (ls_policy.cu) calls the same code.
 #include <cuda_runtime.h>
-#include <math.h>
 
-#include "ls_evaluate.cuh"
+#include "ls_envstep.cuh"
 #include "ls_kernels.h"
 
 namespace ls {
@@ -25,82 +12,7 @@ namespace {
 template <bool NEU>
 __global__ void env_step_kernel(const uint64_t* __restrict__ tab, const TabLayout L, const EvalMeta M,
                                 const ls_search_state S, const int64_t* __restrict__ action, double* reward_out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int A = M.A;
-  const int64_t pos = *S.log_pos;
-  if (pos < 0 || pos >= S.log_capacity) {  // budget guard: nothing scored
-    *reward_out = __longlong_as_double(0x7ff8000000000000LL);
-    return;
-  }
-  // decode the action (indices in range for its head) into (t, e, p, b, Y)
-  uint32_t bad = 0, Y = 0;
-  int idx[4] = {0, 0, 0, 0};
-  for (int h = 0; h < A; ++h) {
-    const int64_t v = action[h];
-    bad |= (v < 0 || v >= (int64_t)M.head_size[h]) ? 1u : 0u;
-    const uint32_t byte = (uint32_t)(v & 0xff);
-    if (h < 4) {
-      idx[h] = (int)byte;
-    } else {
-      const int slot = M.head_slot[h];
-      if (slot >= 0) Y |= (byte & 3u) << (2 * slot);
-    }
-  }
-  Verdict v;
-  v.thr = v.tpot = v.comp = v.comm = v.pipe = 0.0;
-  if (bad) {
-    v.reason = LS_REASON_DECODE_ERROR;
-  } else {
-    Decoded c;
-    c.t = idx[0];
-    c.e = idx[1];
-    c.p = idx[2];
-    c.b = idx[3];
-    c.Y = Y;
-    double mem = 0.0;
-    v.reason = gate(tab, L, M, c, mem);
-    if (v.reason == LS_REASON_NONE) full_path<NEU>(tab, L, M, c, v);
-  }
-  const bool valid = v.reason == LS_REASON_NONE;
-  const double best = *S.best_raw;
-  double raw = 0.0, reward;
-  if (valid) {
-    raw = v.thr;
-    reward = S.alpha * raw + S.beta * (raw - best);
-  } else {
-    reward = bad ? __longlong_as_double(0x7ff8000000000000LL) : S.penalty;
-  }
-  if (valid && raw > best) *S.best_raw = raw;
-  // eval-log append
-  for (int h = 0; h < A; ++h) S.log_vec[pos * A + h] = (uint8_t)(action[h] & 0xff);
-  S.log_raw[pos] = raw;
-  S.log_reward[pos] = reward;
-  S.log_reason[pos] = (uint8_t)v.reason;
-  *S.log_pos = pos + 1;
-  *reward_out = reward;
-  if (!valid) return;
-
-  // EliteBuffer.offer: entries are contiguous from slot 0, best first
-  const int T = S.elite_capacity;
-  int cnt = 0;
-  while (cnt < T && !isinf(S.elite_reward[cnt])) ++cnt;
-  for (int i = 0; i < cnt; ++i) {
-    bool same = true;
-    for (int h = 0; h < A; ++h) same &= S.elite_vec[(int64_t)i * A + h] == action[h];
-    if (same) return;  // duplicate vector
-  }
-  if (cnt >= T) {
-    if (reward <= S.elite_reward[T - 1]) return;
-    cnt = T - 1;  // the last entry is evicted
-  }
-  int at = cnt;  // stable: after every entry with reward >= the newcomer's
-  while (at > 0 && S.elite_reward[at - 1] < reward) {
-    S.elite_reward[at] = S.elite_reward[at - 1];
-    for (int h = 0; h < A; ++h) S.elite_vec[(int64_t)at * A + h] = S.elite_vec[(int64_t)(at - 1) * A + h];
-    --at;
-  }
-  S.elite_reward[at] = reward;
-  for (int h = 0; h < A; ++h) S.elite_vec[(int64_t)at * A + h] = action[h];
+  if (threadIdx.x == 0 && blockIdx.x == 0) env_step<NEU>(tab, L, M, S, action, reward_out);
 }
 
 }  // namespace

@@ -22,7 +22,7 @@ import torch
 from .strategy import ActionSpaceSpec, AxisChoice, FusedOpDescriptor
 
 __all__ = ["MASKED_LOGIT", "NumericsError", "Elite", "EliteBuffer", "build_observation", "head_masks", "TorchPolicy",
-           "sample_actions",
+           "sample_actions", "policy_shapes", "policy_layout",
            "CheckpointError", "save_checkpoint", "load_checkpoint"]
 
 MASKED_LOGIT = -1e30
@@ -94,6 +94,23 @@ def head_masks(space: ActionSpaceSpec, ops: Iterable[FusedOpDescriptor]) -> tupl
     return tuple(masks)
 
 
+def policy_shapes(a: int, d: int, f: int, hk: int) -> list[tuple[str, tuple[int, ...]]]:
+    """Packed parameter tensors in arena order (include/ls_eval.h LS_PSEG_*)."""
+    return [("embed_w", (a, d)), ("embed_b", (d,)), ("wqkv", (d, 3 * d)), ("bqkv", (3 * d,)), ("wo", (d, d)),
+            ("bo", (d,)), ("ln1_g", (d,)), ("ln1_b", (d,)), ("ffn_w1", (d, f)), ("ffn_b1", (f,)),
+            ("ffn_w2", (f, d)), ("ffn_b2", (d,)), ("ln2_g", (d,)), ("ln2_b", (d,)), ("head_w", (d, hk)),
+            ("head_b", (hk,)), ("value_w1", (d, d)), ("value_b1", (d,)), ("value_w2", (d, 1)), ("value_b2", (1,))]
+
+
+def policy_layout(shapes) -> tuple[list[int], int]:
+    """Element offsets of each tensor in the arena, 32-element aligned."""
+    offsets, off = [], 0
+    for _, shape in shapes:
+        offsets.append(off)
+        off = (off + int(np.prod(shape)) + 31) & ~31
+    return offsets, off
+
+
 class TorchPolicy(torch.nn.Module):
     """The reference network with packed parameters.
 
@@ -125,19 +142,18 @@ class TorchPolicy(torch.nn.Module):
         denom = np.maximum(np.asarray(self.head_sizes, dtype=np.float64) - 1.0, 1.0)
         self.register_buffer("obs_denom", torch.tensor(denom, dtype=dtype, device=dev))
         d, f, a = self.width, self.ffn_width, space.vector_length
-
-        def param(*shape):
-            return torch.nn.Parameter(torch.zeros(shape, dtype=dtype, device=dev))
-
-        self.embed_w, self.embed_b = param(a, d), param(d)
-        self.wqkv, self.bqkv = param(d, 3 * d), param(3 * d)
-        self.wo, self.bo = param(d, d), param(d)
-        self.ln1_g, self.ln1_b = param(d), param(d)
-        self.ffn_w1, self.ffn_b1, self.ffn_w2, self.ffn_b2 = param(d, f), param(f), param(f, d), param(d)
-        self.ln2_g, self.ln2_b = param(d), param(d)
-        self.head_w, self.head_b = param(d, nh * kmax), param(nh * kmax)
-        self.value_w1, self.value_b1, self.value_w2, self.value_b2 = param(d, d), param(d), param(d, 1), param(1)
-        self._views = self._name_views()
+        shapes = policy_shapes(a, d, f, nh * kmax)
+        offsets, total = policy_layout(shapes)
+        self.offsets = offsets
+        # one float64 arena in the C ABI's layout (ls_policy_layout_of); every
+        # parameter is a leaf over its slice, so the fused kernels and autograd
+        # see the same storage
+        self.flat = torch.zeros(total, dtype=dtype, device=dev)
+        for (attr, shape), off in zip(shapes, offsets):
+            n = int(np.prod(shape))
+            setattr(self, attr, torch.nn.Parameter(self.flat[off:off + n].view(shape)))
+        with torch.no_grad():  # plain aliases: no autograd node may be created outside the search's stream
+            self._views = self._name_views()
         self.names = list(self._views)
 
     def _name_views(self) -> dict:

@@ -85,7 +85,10 @@ def ppo_loss(pol: TorchPolicy, obs, act, logp_old, value_old, reward, cfg: PpoCo
 class GpuSearch:
     """Device-resident state of one PPO search over ``env``."""
 
-    def __init__(self, env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True) -> None:
+    def __init__(self, env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True,
+                 engine: str = "fused") -> None:
+        if engine not in ("fused", "torch"):
+            raise ValueError(f"unknown PPO engine {engine!r}")
         if env.budget_left < cfg.budget:
             raise ValueError(f"environment has {env.budget_left} evals left, need {cfg.budget}")
         self.env, self.cfg, self.seed = env, cfg, seed
@@ -138,6 +141,38 @@ class GpuSearch:
         self._eager_rounds: dict[int, int] = {}
         self._lib = _native.lib(require_gpu=True)
         self.rounds = 0
+        self.engine = engine
+        if engine == "fused":
+            self._init_fused()
+
+    def _init_fused(self) -> None:
+        """Buffers and the ls_ppo_plan of the fused-kernel engine (ls_policy.cu)."""
+        cfg, pol, dev = self.cfg, self.policy, self.device
+        dims = _native.PolicyDims(self.H, cfg.width, cfg.ffn_width, cfg.history_len, pol.num_heads, pol.kmax,
+                                  cfg.n_steps)
+        layout = _native.PolicyLayout()
+        _native.check(self._lib.ls_policy_layout_of(ctypes.byref(dims), ctypes.byref(layout)))
+        if list(layout.off) != pol.offsets or layout.total != pol.flat.numel():
+            raise RuntimeError("policy arena layout disagrees with ls_policy_layout_of")
+        ws = int(self._lib.ls_ppo_workspace_bytes(ctypes.byref(dims)))
+        if ws == 0:
+            raise _native.NativeError(4, "policy dims unsupported by the fused PPO kernels; use engine='torch'")
+        self.adam_m = torch.zeros_like(pol.flat)
+        self.adam_v = torch.zeros_like(pol.flat)
+        self.adam_step = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
+        self.blocked_u8 = pol.blocked.to(torch.uint8).contiguous()
+        self.head_size_i32 = pol.sizes.to(torch.int32).contiguous()
+        ptr = lambda t: t.data_ptr()  # noqa: E731
+        self.plan = _native.PpoPlan(
+            dims, ptr(pol.flat), ptr(self.adam_m), ptr(self.adam_v), None, ptr(self.workspace), ptr(self.blocked_u8),
+            ptr(self.head_size_i32), ptr(pol.obs_denom), self._state, ptr(self.uniforms), ptr(self.lr_table),
+            ptr(self.spent), ptr(self.adam_step), ptr(self.status), ptr(self.b_obs), ptr(self.b_act),
+            ptr(self.b_logp), ptr(self.b_value), ptr(self.b_reward), cfg.tau, cfg.clip_eps, cfg.value_coef,
+            cfg.entropy_coef, 0.9, 0.999, 1e-8, cfg.epochs_per_update)
+
+    def _stream_ptr(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     # -- one round (graph-capturable: no host syncs, static shapes) ----------
 
@@ -182,11 +217,23 @@ class GpuSearch:
             confident = (self.policy.confidence(probs) >= self.cfg.tau).all()
         self.status.copy_((confident.int() * _CONFIDENT + bad.int() * _NONFINITE).reshape(1))
 
+    def _fused_round(self, n: int) -> None:
+        _native.check(self._lib.ls_ppo_round(self.ev._ctx, ctypes.byref(self.plan), n, self._stream_ptr()))
+
     def _run_round(self, n: int) -> int:
         """One round (replayed graph once warm); returns the status word."""
         g = self._graphs.get(n)
         if g is not None:
             g.replay()
+        elif self.engine == "fused":
+            if self.use_graphs:  # kernels need no warm-up: capture at once, then replay
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._fused_round(n)
+                self._graphs[n] = g
+                g.replay()
+            else:
+                self._fused_round(n)
         else:
             self._round(n)
             if self.use_graphs:
@@ -208,12 +255,18 @@ class GpuSearch:
         for st in self.opt.state.values():  # fresh optimizer
             for v in st.values():
                 v.zero_()
+        if self.engine == "fused":
+            self.adam_m.zero_()
+            self.adam_v.zero_()
+            self.adam_step.zero_()
         self._rng_mark = self.rng.bit_generator.state
         draws = self.rng.random(allowance * self.H)
         self.uniforms[: draws.size].copy_(torch.from_numpy(draws))
         lrs = np.array([cosine_decay(self.cfg.lr_initial, s / allowance) for s in range(allowance)])
         self.lr_table[:allowance].copy_(torch.from_numpy(lrs))
         self.spent.zero_()
+        if self.engine == "fused":  # sample slot 0 <- forward of the current observation
+            _native.check(self._lib.ls_ppo_prime(self.ev._ctx, ctypes.byref(self.plan), self._stream_ptr()))
 
     def _end_chunk(self, spent: int) -> None:
         self.rng.bit_generator.state = self._rng_mark
@@ -267,14 +320,15 @@ class GpuSearch:
                            bool(why[i] == 0), REASON_NAMES[int(why[i])]) for i in range(count)]
 
 
-def run_search(env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True) -> SearchReport:
+def run_search(env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True,
+               engine: str = "fused") -> SearchReport:
     """Full chunked-restart PPO search on the GPU; consumes exactly ``cfg.budget`` evals.
 
     Appends the eval records to ``env`` (and its NDJSON sink) when the search
     ends and leaves ``env.best_raw`` where the reference's would be.
     """
     start = time.perf_counter()
-    search = GpuSearch(env, cfg, seed, use_graphs=use_graphs)
+    search = GpuSearch(env, cfg, seed, use_graphs=use_graphs, engine=engine)
     restarts, evals_done = search.run()
     first = env.evals_used
     records = search.records(first, evals_done)

@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--cases", default="")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--engine", default="fused")
     args = ap.parse_args()
     gold = np.load(ROOT / "tests" / "golden" / "ppo_reference.npz")
     meta = json.loads(str(gold["meta"]))
@@ -50,12 +51,13 @@ def main():
             env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, m["evals"], slo_tpot=wl.slo_tpot)
             env.evaluator  # build tables outside the timed search
             t0 = time.perf_counter()
-            report = run_search(env, PpoConfig(budget=m["evals"]), int(seed), use_graphs=not args.no_graphs)
+            report = run_search(env, PpoConfig(budget=m["evals"]), int(seed), use_graphs=not args.no_graphs,
+                                engine=args.engine)
             wall = time.perf_counter() - t0
             vecs = np.asarray([r.vector for r in env.eval_log], dtype=np.uint8)
             rews = np.asarray([r.reward for r in env.eval_log])
             k = common_prefix(vecs, rews, gold[case + "_vectors"], gold[case + "_rewards"])
-            print(json.dumps({"case": case, "rep": rep, "wall_s": round(wall, 4), "evals": report.evals,
+            print(json.dumps({"case": case, "engine": args.engine, "rep": rep, "wall_s": round(wall, 4), "evals": report.evals,
                               "match_prefix": k, "restarts": list(report.restarts), "ref_restarts": m["restarts"],
                               "best_raw": report.best_raw, "ref_best_raw": m["best_raw"],
                               "best_vector": list(report.best_vector), "ref_wall_s": round(m["wall_s"], 2)}),
