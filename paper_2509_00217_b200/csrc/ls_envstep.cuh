@@ -17,21 +17,25 @@
 
 namespace ls {
 
-template <bool NEU>
-__device__ __noinline__ void env_step(const uint64_t* __restrict__ tab, const TabLayout& L, const EvalMeta& M,
-                                      const ls_search_state& S, const int64_t* action, double* reward_out) {
+// Thread-0 core. ev/er: the elite buffer (shared-memory copy); returns true
+// when the buffer changed. tab is global (LDG) or a shared-memory copy.
+template <bool NEU, bool LDG>
+__device__ __noinline__ bool env_step_core(const uint64_t* __restrict__ tab, const TabLayout& L, const EvalMeta& M,
+                                           const ls_search_state& S, const int* action, double* reward_out,
+                                           int64_t* ev, double* er) {
   const int A = M.A;
   const int64_t pos = *S.log_pos;
+  const double best = *S.best_raw;
   if (pos < 0 || pos >= S.log_capacity) {  // budget guard: nothing scored
     *reward_out = __longlong_as_double(0x7ff8000000000000LL);
-    return;
+    return false;
   }
   // decode the action (indices in range for its head) into (t, e, p, b, Y)
   uint32_t bad = 0, Y = 0;
   int idx[4] = {0, 0, 0, 0};
   for (int h = 0; h < A; ++h) {
-    const int64_t v = action[h];
-    bad |= (v < 0 || v >= (int64_t)M.head_size[h]) ? 1u : 0u;
+    const int v = action[h];
+    bad |= (v < 0 || v >= (int)M.head_size[h]) ? 1u : 0u;
     const uint32_t byte = (uint32_t)(v & 0xff);
     if (h < 4) {
       idx[h] = (int)byte;
@@ -53,10 +57,9 @@ __device__ __noinline__ void env_step(const uint64_t* __restrict__ tab, const Ta
     c.Y = Y;
     double mem = 0.0;
     v.reason = gate(tab, L, M, c, mem);
-    if (v.reason == LS_REASON_NONE) full_path<NEU>(tab, L, M, c, v);
+    if (v.reason == LS_REASON_NONE) full_path<NEU, LDG>(tab, L, M, c, v);
   }
   const bool valid = v.reason == LS_REASON_NONE;
-  const double best = *S.best_raw;
   double raw = 0.0, reward;
   if (valid) {
     raw = v.thr;
@@ -72,30 +75,50 @@ __device__ __noinline__ void env_step(const uint64_t* __restrict__ tab, const Ta
   S.log_reason[pos] = (uint8_t)v.reason;
   *S.log_pos = pos + 1;
   *reward_out = reward;
-  if (!valid) return;
+  if (!valid) return false;
 
   // EliteBuffer.offer: entries are contiguous from slot 0, best first
   const int T = S.elite_capacity;
   int cnt = 0;
-  while (cnt < T && !isinf(S.elite_reward[cnt])) ++cnt;
+  while (cnt < T && !isinf(er[cnt])) ++cnt;
   for (int i = 0; i < cnt; ++i) {
     bool same = true;
-    for (int h = 0; h < A; ++h) same &= S.elite_vec[(int64_t)i * A + h] == action[h];
-    if (same) return;  // duplicate vector
+    for (int h = 0; h < A; ++h) same &= ev[i * A + h] == (int64_t)action[h];
+    if (same) return false;  // duplicate vector
   }
   if (cnt >= T) {
-    if (reward <= S.elite_reward[T - 1]) return;
+    if (reward <= er[T - 1]) return false;
     cnt = T - 1;  // the last entry is evicted
   }
   int at = cnt;  // stable: after every entry with reward >= the newcomer's
-  while (at > 0 && S.elite_reward[at - 1] < reward) {
-    S.elite_reward[at] = S.elite_reward[at - 1];
-    for (int h = 0; h < A; ++h) S.elite_vec[(int64_t)at * A + h] = S.elite_vec[(int64_t)(at - 1) * A + h];
+  while (at > 0 && er[at - 1] < reward) {
+    er[at] = er[at - 1];
+    for (int h = 0; h < A; ++h) ev[at * A + h] = ev[(at - 1) * A + h];
     --at;
   }
-  S.elite_reward[at] = reward;
-  for (int h = 0; h < A; ++h) S.elite_vec[(int64_t)at * A + h] = action[h];
+  er[at] = reward;
+  for (int h = 0; h < A; ++h) ev[at * A + h] = action[h];
+  return true;
 }
 
+// Block-cooperative step: every thread of the block must call it. The elite
+// buffer is staged through shared memory (ev: >= T*A, er: >= T) so the
+// sequential part runs on on-chip data; action: A indices visible to thread 0.
+template <bool NEU, bool LDG>
+__device__ __forceinline__ void env_step_block(const uint64_t* __restrict__ tab, const TabLayout& L,
+                                               const EvalMeta& M, const ls_search_state& S, const int* action,
+                                               double* reward_out, int64_t* ev, double* er) {
+  __shared__ int changed;
+  const int T = S.elite_capacity, TA = T * M.A;
+  for (int i = threadIdx.x; i < TA; i += blockDim.x) ev[i] = S.elite_vec[i];
+  for (int i = threadIdx.x; i < T; i += blockDim.x) er[i] = S.elite_reward[i];
+  __syncthreads();
+  if (threadIdx.x == 0) changed = env_step_core<NEU, LDG>(tab, L, M, S, action, reward_out, ev, er) ? 1 : 0;
+  __syncthreads();
+  if (changed) {
+    for (int i = threadIdx.x; i < TA; i += blockDim.x) S.elite_vec[i] = ev[i];
+    for (int i = threadIdx.x; i < T; i += blockDim.x) S.elite_reward[i] = er[i];
+  }
+}
 
 }  // namespace ls

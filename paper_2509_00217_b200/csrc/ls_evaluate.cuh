@@ -73,6 +73,15 @@ __device__ __forceinline__ double gget(const uint64_t* __restrict__ T, int i) {
 __device__ __forceinline__ uint64_t gword(const uint64_t* __restrict__ T, int i) {
   return __ldg(reinterpret_cast<const unsigned long long*>(T) + i);
 }
+// LDG: table in global memory (read-only path) or any address space (smem copy)
+template <bool LDG>
+__device__ __forceinline__ double tget(const uint64_t* __restrict__ T, int i) {
+  return LDG ? gget(T, i) : dget(T, i);
+}
+template <bool LDG>
+__device__ __forceinline__ uint64_t tword(const uint64_t* __restrict__ T, int i) {
+  return LDG ? gword(T, i) : T[i];
+}
 
 // A decoded candidate: domain indices and Y, the 2-bit axis of every axis
 // head in its field slot (ls_tables.cuh head_slots).
@@ -113,7 +122,7 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
 }
 
 // fp64 pass for a candidate that passed gate(). T: the full table (global).
-template <bool NEU>
+template <bool NEU, bool LDG = true>
 __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
                                           const Decoded& c, Verdict& v) {
   const int t = c.t, e = c.e, p = c.p, b = c.b;
@@ -125,28 +134,28 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   const int a2 = ax_attn == 2;
   const int nt = L.nt, ne = L.ne, nb = L.nb;
   const int tb = t * nb + b, teb = (t * ne + e) * nb + b;
-  const int64_t tpv = (int64_t)gword(T, L.tpv + t), epv = (int64_t)gword(T, L.epv + e);
-  const int64_t ppv = (int64_t)gword(T, L.ppv + p);
+  const int64_t tpv = (int64_t)tword<LDG>(T, L.tpv + t), epv = (int64_t)tword<LDG>(T, L.epv + e);
+  const int64_t ppv = (int64_t)tword<LDG>(T, L.ppv + p);
   const bool tp_gt1 = tpv > 1, ep_gt1 = epv > 1;
 
   // layer plan compute: qkv, kv, attn, out, router, ffn1, ffn2[, sh1, sh2]
   Accum<NEU> lc;
   lc.init();
-  lc.push(gget(T, L.opt_qkv + ax_qkv * nt * nb + tb));
-  lc.push(gget(T, L.opt_kv + a2 * nt * nb + tb));
-  lc.push(gget(T, L.opt_attn + a2 * nt * nb + tb));
-  lc.push(gget(T, L.opt_out + ax_out * nt * nb + tb));
-  lc.push(gget(T, L.opt_router + b));
-  lc.push(gget(T, L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
-  lc.push(gget(T, L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
+  lc.push(tget<LDG>(T, L.opt_qkv + ax_qkv * nt * nb + tb));
+  lc.push(tget<LDG>(T, L.opt_kv + a2 * nt * nb + tb));
+  lc.push(tget<LDG>(T, L.opt_attn + a2 * nt * nb + tb));
+  lc.push(tget<LDG>(T, L.opt_out + ax_out * nt * nb + tb));
+  lc.push(tget<LDG>(T, L.opt_router + b));
+  lc.push(tget<LDG>(T, L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
+  lc.push(tget<LDG>(T, L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
   if (L.has_shared) {
-    lc.push(gget(T, L.opt_sh1 + ax_s1 * nt * nb + tb));
-    lc.push(gget(T, L.opt_sh2 + ax_s2 * nt * nb + tb));
+    lc.push(tget<LDG>(T, L.opt_sh1 + ax_s1 * nt * nb + tb));
+    lc.push(tget<LDG>(T, L.opt_sh2 + ax_s2 * nt * nb + tb));
   }
   // layer plan collectives in all_collectives() order (layout.py:270-275)
   Accum<NEU> lm;
   lm.init();
-#define LS_TP_COLL(cls, f) gget(T, L.coll + ((cls) * 2 + ((f) - 1)) * nt * nb + tb)
+#define LS_TP_COLL(cls, f) tget<LDG>(T, L.coll + ((cls) * 2 + ((f) - 1)) * nt * nb + tb)
   const int st_attn = a2 ? ST_S : ST_R;
   if (tp_gt1) {
     int f;
@@ -154,11 +163,11 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
     if ((f = fam(st_attn, req(ax_out)))) lm.push(LS_TP_COLL(CLS_H, f));  // feed attn_out_proj
     if ((f = fam(ax_out, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));          // attention residual
   }
-  const double a2a = ep_gt1 ? gget(T, L.a2a + teb) : 0.0;
+  const double a2a = ep_gt1 ? tget<LDG>(T, L.a2a + teb) : 0.0;
   if (ep_gt1) lm.push(a2a);  // expert dispatch
   if (tp_gt1) {
     int f;
-    if ((f = fam(ax_f1, req(ax_f2)))) lm.push(gget(T, L.rtf + (f - 1) * nt * ne * nb + teb));  // feed ffn2
+    if ((f = fam(ax_f1, req(ax_f2)))) lm.push(tget<LDG>(T, L.rtf + (f - 1) * nt * ne * nb + teb));  // feed ffn2
     if (L.has_shared && (f = fam(ax_s1, req(ax_s2)))) lm.push(LS_TP_COLL(CLS_F, f));        // feed sh2
   }
   if (ep_gt1) lm.push(a2a);  // expert combine
@@ -174,7 +183,7 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   const double layer_c = lc.result(), layer_m = lm.result();
 
   // pre plan (embedding) and post plan (final_norm, lm_head)
-  const double pre_c = 0.0 + gget(T, L.opt_emb + ax_emb * nt * nb + tb);
+  const double pre_c = 0.0 + tget<LDG>(T, L.opt_emb + ax_emb * nt * nb + tb);
   double pre_m = 0.0, post_m = 0.0;
   if (tp_gt1) {
     int f;
@@ -183,18 +192,18 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   }
 #undef LS_TP_COLL
   PySum<NEU> po;
-  po.first(gget(T, L.opt_norm + b));
-  po.add(gget(T, L.opt_lmh + ax_lmh * nt * nb + tb));
+  po.first(tget<LDG>(T, L.opt_norm + b));
+  po.add(tget<LDG>(T, L.opt_lmh + ax_lmh * nt * nb + tb));
   const double post_c = po.result();
 
   // totals and pipeline stages (simulator.py:286-323)
   const int64_t world = tpv * epv * ppv;
-  const double hop = ppv > 1 ? gget(T, L.hop + (world <= M.node_size ? nb : 0) + b) : 0.0;
+  const double hop = ppv > 1 ? tget<LDG>(T, L.hop + (world <= M.node_size ? nb : 0) + b) : 0.0;
   const double compute = (M.num_layers_d * layer_c + pre_c) + post_c;
   const double comm = (M.num_layers_d * layer_m + pre_m) + post_m;
-  const double pipe = gget(T, L.ppm1_d + p) * hop;
+  const double pipe = tget<LDG>(T, L.ppm1_d + p) * hop;
   const double tpot = (compute + comm) + pipe;
-  const double body = gget(T, L.lps_d + p) * (layer_c + layer_m);
+  const double body = tget<LDG>(T, L.lps_d + p) * (layer_c + layer_m);
   const double c0 = body + (pre_c + pre_m);
   double cmax;
   if (ppv == 1) {
@@ -215,7 +224,7 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
     return;
   }
   v.reason = LS_REASON_NONE;
-  v.thr = (gget(T, L.batch_d + b) / cmax) / (double)world;
+  v.thr = (tget<LDG>(T, L.batch_d + b) / cmax) / (double)world;
 }
 
 }  // namespace ls

@@ -43,10 +43,11 @@ constexpr double kLnEps = 1e-5;
 // Workspace: activations and their gradients (doubles).
 struct Work {
   double *E, *QKV, *ATTW, *CTX, *RES1, *N1, *IS1, *H1, *ACT, *RES2, *N2, *IS2, *POOL, *LRAW, *VH;
-  double *DL, *DVAL, *DVPRE, *DPOOL, *DRES2, *DPRE, *DH1, *DRES1, *DCTX, *DQKV, *DEMB;
+  double *DL, *DVAL, *DVPRE, *DPOOL, *DRES2, *DPRE, *DH1, *DRES1, *DCTX, *DQKV, *DEMB, *HYP;
 };
 
 struct Seg {
+  int blk0, colblocks;      // first CTA of the segment, CTAs per row
   int64_t off, rows, cols;  // rows = 0: vector segment of length cols
   int kind;                 // 0 matrix x^T dy, 1 bias sum dy, 2 LN gain sum dy*x
   int nrows;                // summed rows
@@ -82,7 +83,7 @@ struct Args {
 };
 
 struct SegTable {
-  int n;
+  int n, blocks;
   Seg s[LS_PSEG_COUNT];
 };
 
@@ -92,20 +93,25 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // xor butterfly: every lane holds the same (commutative) sum
 }
 
-// Column tile: out(r, j) = sum_i X[r*ldx + i] * W[i*ldw + j] for j = j0 + lane,
-// the i range split across the 8 warps and reduced in a fixed order; then
-// epi(r, j, sum) for every (r < R, j < N).
+// Column tile: out(r, j) = sum_i X[r*ldx + i] * W[i*ldw + j] for the kCols
+// columns j0.. of this CTA. Threads are (k group, column): each k group sums
+// every kKG-th input row, then the kKG partials are reduced in a fixed order
+// (deterministic); finally epi(r, j, sum) for every (r < R, j < N).
+constexpr int kCols = 8;
+constexpr int kKG = kThreads / kCols;
+constexpr int kRedDoubles = kKG * kRowsMax * kCols;
+
 template <class Epi>
 __device__ __forceinline__ void xw_tile(const double* X, int64_t ldx, int R, int K, const double* __restrict__ W,
                                         int64_t ldw, int N, int j0, double* red, Epi epi) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = j0 + lane;
+  const int c = threadIdx.x % kCols, kg = threadIdx.x / kCols;
+  const int j = j0 + c;
   double acc[kRowsMax];
 #pragma unroll
   for (int r = 0; r < kRowsMax; ++r) acc[r] = 0.0;
   if (j < N) {
 #pragma unroll 4
-    for (int i = warp; i < K; i += kWarps) {
+    for (int i = kg; i < K; i += kKG) {
       const double wv = __ldg(W + (int64_t)i * ldw + j);
 #pragma unroll
       for (int r = 0; r < kRowsMax; ++r)
@@ -114,13 +120,13 @@ __device__ __forceinline__ void xw_tile(const double* X, int64_t ldx, int R, int
   }
 #pragma unroll
   for (int r = 0; r < kRowsMax; ++r)
-    if (r < R) red[(warp * kRowsMax + r) * 32 + lane] = acc[r];
+    if (r < R) red[(kg * kRowsMax + r) * kCols + c] = acc[r];
   __syncthreads();
-  for (int idx = threadIdx.x; idx < R * 32; idx += kThreads) {
-    const int r = idx >> 5, l = idx & 31, jj = j0 + l;
+  for (int idx = threadIdx.x; idx < R * kCols; idx += kThreads) {
+    const int r = idx / kCols, cc = idx % kCols, jj = j0 + cc;
     if (jj >= N) continue;
-    double s = red[r * 32 + l];
-    for (int w = 1; w < kWarps; ++w) s += red[(w * kRowsMax + r) * 32 + l];
+    double s = red[r * kCols + cc];
+    for (int g = 1; g < kKG; ++g) s += red[(g * kRowsMax + r) * kCols + cc];
     epi(r, jj, s);
   }
 }
@@ -134,6 +140,7 @@ __device__ __forceinline__ void dywt_row(const double* DY, int64_t ldd, int R, i
 #pragma unroll
   for (int r = 0; r < kRowsMax; ++r) acc[r] = 0.0;
   const double* wr = W + (int64_t)i * ldw;
+#pragma unroll 4
   for (int j = lane; j < N; j += 32) {
     const double wv = __ldg(wr + j);
 #pragma unroll
@@ -150,15 +157,18 @@ __device__ __forceinline__ void ln_row(const double* x, int d, const double* g, 
                                        double* nrm_out, double* inv_out) {
   const int lane = threadIdx.x & 31;
   double s = 0.0;
+#pragma unroll 8
   for (int c = lane; c < d; c += 32) s += x[c];
   const double mean = warp_sum(s) / d;
   double q = 0.0;
+#pragma unroll 8
   for (int c = lane; c < d; c += 32) {
     const double cc = x[c] - mean;
     q += cc * cc;
   }
   const double var = warp_sum(q) / d;
   const double inv = 1.0 / sqrt(var + kLnEps);
+#pragma unroll 8
   for (int c = lane; c < d; c += 32) {
     const double n = (x[c] - mean) * inv;
     h[c] = g[c] * n + b[c];
@@ -173,12 +183,14 @@ template <class DH>
 __device__ __forceinline__ void ln_back_row(DH dh, int d, const double* g, const double* nrm, double inv, double* dx) {
   const int lane = threadIdx.x & 31;
   double s1 = 0.0, s2 = 0.0;
+#pragma unroll 8
   for (int c = lane; c < d; c += 32) {
     const double dn = dh(c) * g[c];
     s1 += dn;
     s2 += dn * nrm[c];
   }
   const double m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+#pragma unroll 8
   for (int c = lane; c < d; c += 32) {
     const double dn = dh(c) * g[c];
     dx[c] = inv * (dn - m1 - nrm[c] * m2);
@@ -189,10 +201,10 @@ __device__ __forceinline__ void ln_back_row(DH dh, int d, const double* g, const
 
 // embedding (recomputed per CTA) + q/k/v column tile. build: render the
 // observation from the device elite buffer (build_observation, policy.py:105-117).
-__global__ void __launch_bounds__(kThreads) fwd_embed_qkv(const Args a, int row0, int R, int build) {
+__global__ void __launch_bounds__(kThreads) fwd_embed_qkv(const __grid_constant__ Args a, int row0, int R, int build) {
   extern __shared__ double sm[];
   double* red = sm;
-  double* Xs = red + kWarps * kRowsMax * 32;
+  double* Xs = red + kRedDoubles;
   double* Es = Xs + R * a.A;
   const int A = a.A, d = a.d;
   for (int i = threadIdx.x; i < R * A; i += kThreads) {
@@ -210,6 +222,7 @@ __global__ void __launch_bounds__(kThreads) fwd_embed_qkv(const Args a, int row0
   for (int i = threadIdx.x; i < R * d; i += kThreads) {
     const int r = i / d, c = i % d;
     double s = 0.0;
+#pragma unroll 8
     for (int k = 0; k < A; ++k) s += Xs[r * A + k] * __ldg(a.We + (int64_t)k * d + c);
     const double e = s + a.be[c];
     Es[i] = e;
@@ -218,16 +231,16 @@ __global__ void __launch_bounds__(kThreads) fwd_embed_qkv(const Args a, int row0
   __syncthreads();
   double* QKV = a.w.QKV + (int64_t)row0 * 3 * d;
   const double* bq = a.bqkv;
-  xw_tile(Es, d, R, d, a.Wqkv, 3 * d, 3 * d, blockIdx.x * 32, red,
+  xw_tile(Es, d, R, d, a.Wqkv, 3 * d, 3 * d, blockIdx.x * kCols, red,
           [&](int r, int j, double s) { QKV[(int64_t)r * 3 * d + j] = s + bq[j]; });
 }
 
 // attention (recomputed per CTA) + output projection tile + residual.
-__global__ void __launch_bounds__(kThreads) fwd_attn_out(const Args a, int row0, int R) {
+__global__ void __launch_bounds__(kThreads) fwd_attn_out(const __grid_constant__ Args a, int row0, int R) {
   extern __shared__ double sm[];
   const int d = a.d, T = a.T, S = R / T, TT = T * T;
   double* red = sm;
-  double* Ws = red + kWarps * kRowsMax * 32;
+  double* Ws = red + kRedDoubles;
   double* Cs = Ws + S * TT;
   const double* QKV = a.w.QKV + (int64_t)row0 * 3 * d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -237,6 +250,7 @@ __global__ void __launch_bounds__(kThreads) fwd_attn_out(const Args a, int row0,
     const double* q = QKV + (int64_t)(s * T + t) * 3 * d;
     const double* k = QKV + (int64_t)(s * T + u) * 3 * d + d;
     double acc = 0.0;
+#pragma unroll 8
     for (int c = lane; c < d; c += 32) acc += q[c] * k[c];
     acc = warp_sum(acc);
     if (lane == 0) Ws[p] = acc * scale;
@@ -259,6 +273,7 @@ __global__ void __launch_bounds__(kThreads) fwd_attn_out(const Args a, int row0,
   for (int i = threadIdx.x; i < R * d; i += kThreads) {
     const int r = i / d, c = i % d, s = r / T, t = r % T;
     double acc = 0.0;
+#pragma unroll 4
     for (int u = 0; u < T; ++u) acc += Ws[(s * T + t) * T + u] * QKV[(int64_t)(s * T + u) * 3 * d + 2 * d + c];
     Cs[i] = acc;
     if (blockIdx.x == 0) a.w.CTX[(int64_t)row0 * d + i] = acc;
@@ -267,16 +282,16 @@ __global__ void __launch_bounds__(kThreads) fwd_attn_out(const Args a, int row0,
   const double* E = a.w.E + (int64_t)row0 * d;
   double* RES1 = a.w.RES1 + (int64_t)row0 * d;
   const double* bo = a.bo;
-  xw_tile(Cs, d, R, d, a.Wo, d, d, blockIdx.x * 32, red,
+  xw_tile(Cs, d, R, d, a.Wo, d, d, blockIdx.x * kCols, red,
           [&](int r, int j, double s) { RES1[(int64_t)r * d + j] = E[(int64_t)r * d + j] + (s + bo[j]); });
 }
 
 // LayerNorm 1 (recomputed per CTA) + FFN first layer tile + ReLU.
-__global__ void __launch_bounds__(kThreads) fwd_ln1_ffn1(const Args a, int row0, int R) {
+__global__ void __launch_bounds__(kThreads) fwd_ln1_ffn1(const __grid_constant__ Args a, int row0, int R) {
   extern __shared__ double sm[];
   const int d = a.d, f = a.f;
   double* red = sm;
-  double* Hs = red + kWarps * kRowsMax * 32;
+  double* Hs = red + kRedDoubles;
   const int warp = threadIdx.x >> 5;
   const bool first = blockIdx.x == 0;
   for (int r = warp; r < R; r += kWarps) {
@@ -288,30 +303,34 @@ __global__ void __launch_bounds__(kThreads) fwd_ln1_ffn1(const Args a, int row0,
     for (int i = threadIdx.x; i < R * d; i += kThreads) a.w.H1[(int64_t)row0 * d + i] = Hs[i];
   double* ACT = a.w.ACT + (int64_t)row0 * f;
   const double* b1 = a.b1;
-  xw_tile(Hs, d, R, d, a.W1, f, f, blockIdx.x * 32, red, [&](int r, int j, double s) {
+  xw_tile(Hs, d, R, d, a.W1, f, f, blockIdx.x * kCols, red, [&](int r, int j, double s) {
     const double v = s + b1[j];
     ACT[(int64_t)r * f + j] = v > 0.0 ? v : 0.0;
   });
 }
 
 // FFN second layer tile + residual.
-__global__ void __launch_bounds__(kThreads) fwd_ffn2(const Args a, int row0, int R) {
+__global__ void __launch_bounds__(kThreads) fwd_ffn2(const __grid_constant__ Args a, int row0, int R) {
   extern __shared__ double sm[];
   const int d = a.d, f = a.f;
   const double* H1 = a.w.H1 + (int64_t)row0 * d;
   double* RES2 = a.w.RES2 + (int64_t)row0 * d;
   const double* b2 = a.b2;
-  xw_tile(a.w.ACT + (int64_t)row0 * f, f, R, f, a.W2, d, d, blockIdx.x * 32, sm,
+  double* As = sm + kRedDoubles;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < R * f; i += kThreads) As[i] = a.w.ACT[(int64_t)row0 * f + i];
+  __syncthreads();
+  xw_tile(As, f, R, f, a.W2, d, d, blockIdx.x * kCols, sm,
           [&](int r, int j, double s) { RES2[(int64_t)r * d + j] = H1[(int64_t)r * d + j] + (s + b2[j]); });
 }
 
 // LayerNorm 2 + mean pool (recomputed per CTA) + a column tile of the heads
 // (first ceil(HK/32) CTAs) or of the value hidden layer (the rest).
-__global__ void __launch_bounds__(kThreads) fwd_ln2_heads(const Args a, int row0, int R) {
+__global__ void __launch_bounds__(kThreads) fwd_ln2_heads(const __grid_constant__ Args a, int row0, int R) {
   extern __shared__ double sm[];
   const int d = a.d, T = a.T, S = R / T, slot0 = row0 / T;
   double* red = sm;
-  double* Hs = red + kWarps * kRowsMax * 32;
+  double* Hs = red + kRedDoubles;
   double* Ps = Hs + R * d;
   const int warp = threadIdx.x >> 5;
   const bool first = blockIdx.x == 0;
@@ -328,17 +347,17 @@ __global__ void __launch_bounds__(kThreads) fwd_ln2_heads(const Args a, int row0
     if (first) a.w.POOL[(int64_t)slot0 * d + i] = Ps[i];
   }
   __syncthreads();
-  const int nh = (a.HK + 31) / 32;
+  const int nh = (a.HK + kCols - 1) / kCols;
   if ((int)blockIdx.x < nh) {
     double* L = a.w.LRAW + (int64_t)slot0 * a.HK;
     const double* bh = a.bh;
     const int HK = a.HK;
-    xw_tile(Ps, d, S, d, a.Wh, HK, HK, blockIdx.x * 32, red,
+    xw_tile(Ps, d, S, d, a.Wh, HK, HK, blockIdx.x * kCols, red,
             [&](int r, int j, double s) { L[(int64_t)r * HK + j] = s + bh[j]; });
   } else {
     double* VH = a.w.VH + (int64_t)slot0 * d;
     const double* bv = a.bv1;
-    xw_tile(Ps, d, S, d, a.Wv1, d, d, (blockIdx.x - nh) * 32, red, [&](int r, int j, double s) {
+    xw_tile(Ps, d, S, d, a.Wv1, d, d, (blockIdx.x - nh) * kCols, red, [&](int r, int j, double s) {
       const double v = s + bv[j];
       VH[(int64_t)r * d + j] = v > 0.0 ? v : 0.0;
     });
@@ -349,10 +368,15 @@ enum { MODE_SAMPLE = 0, MODE_CONF = 1, MODE_TRAIN = 2, MODE_PROBE = 3 };
 
 // Heads and value on one CTA: masked log-softmax per head (policy.py:168-174),
 // value, then per mode — sample + env step, confidence, or the PPO loss
-// gradient w.r.t. logits and value (ppo.py:225-283).
+// gradient w.r.t. logits and value (ppo.py:225-283). Every global input is
+// first staged into shared memory with independent loads, so the serial
+// per-head and per-sample loops run on on-chip data. SMEMTAB: the workload's
+// cost tables are staged too, for the env step's single-thread walk.
 template <int MODE, bool NEU>
-__global__ void __launch_bounds__(kThreads) fwd_final(const Args a, int slot0, int S, const uint64_t* __restrict__ tab,
-                                                      const TabLayout L, const EvalMeta M) {
+__global__ void __launch_bounds__(kThreads) fwd_final(const __grid_constant__ Args a, int slot0, int S,
+                                                      const uint64_t* __restrict__ tab,
+                                                      const __grid_constant__ TabLayout L,
+                                                      const __grid_constant__ EvalMeta M) {
   extern __shared__ double sm[];
   const int d = a.d, H = a.H, K = a.K, HK = a.HK;
   double* LP = sm;
@@ -360,33 +384,67 @@ __global__ void __launch_bounds__(kThreads) fwd_final(const Args a, int slot0, i
   double* ENT = PR + S * HK;  // [S*H]
   double* VAL = ENT + S * H;  // [S]
   double* DLP = VAL + S;      // [S] d loss / d logprob
+  double* RAW = DLP + S;      // [S*HK] staged logits
+  double* MX = RAW + S * HK;  // [S*H] per-head max, then log(total)
+  double* TOT = MX + S * H;   // [S*H]
+  int64_t* EV = reinterpret_cast<int64_t*>(TOT + S * H);  // elite copy (sample mode)
+  double* ER = reinterpret_cast<double*>(EV + a.env.elite_capacity * a.A);
+  __shared__ uint8_t blk[LS_MAX_HEADS * 64];
   __shared__ int act[LS_MAX_HEADS];
   __shared__ int all_conf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (MODE == MODE_SAMPLE) {  // pull the cost tables into L1 for the env step's serial walk
+    for (int i = threadIdx.x * 16; i < L.words; i += kThreads * 16)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(tab + i));
+  }
+  const double* LR = a.w.LRAW + (int64_t)slot0 * HK;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < S * HK; i += kThreads) RAW[i] = LR[i];
+  for (int i = threadIdx.x; i < HK; i += kThreads) blk[i] = a.blocked[i];
   for (int s = warp; s < S; s += kWarps) {
     const double* vh = a.w.VH + (int64_t)(slot0 + s) * d;
     double acc = 0.0;
+#pragma unroll 4
     for (int c = lane; c < d; c += 32) acc += vh[c] * a.Wv2[c];
     acc = warp_sum(acc);
     if (lane == 0) VAL[s] = acc + a.bv2[0];
   }
+  __syncthreads();
+  // masked log-softmax: per-head max, element-parallel exp, per-head sums in k order
   for (int i = threadIdx.x; i < S * H; i += kThreads) {
     const int s = i / H, h = i % H;
-    const double* raw = a.w.LRAW + (int64_t)(slot0 + s) * HK + h * K;
-    const uint8_t* blk = a.blocked + h * K;
+    const double* raw = RAW + s * HK + h * K;
+    const uint8_t* bk = blk + h * K;
     double mx = -INFINITY;
-    for (int k = 0; k < K; ++k) mx = fmax(mx, blk[k] ? kMasked : raw[k]);
+    for (int k = 0; k < K; ++k) mx = fmax(mx, bk[k] ? kMasked : raw[k]);
+    MX[i] = mx;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S * HK; i += kThreads) {
+    const int s = i / HK, j = i % HK;
+    const double sh = (blk[j] ? kMasked : RAW[i]) - MX[s * H + j / K];
+    LP[i] = sh;
+    PR[i] = exp(sh);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S * H; i += kThreads) {
+    const double* ex = PR + (i / H) * HK + (i % H) * K;
     double tot = 0.0;
-    for (int k = 0; k < K; ++k) tot += exp((blk[k] ? kMasked : raw[k]) - mx);
-    const double lt = log(tot);
+    for (int k = 0; k < K; ++k) tot += ex[k];
+    TOT[i] = tot;
+    MX[i] = log(tot);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S * HK; i += kThreads) {
+    const int hh = (i / HK) * H + (i % HK) / K;
+    LP[i] = LP[i] - MX[hh];
+    PR[i] = PR[i] / TOT[hh];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S * H; i += kThreads) {
+    const int o = (i / H) * HK + (i % H) * K;
     double e = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double sh = (blk[k] ? kMasked : raw[k]) - mx;
-      const double lp = sh - lt, p = exp(sh) / tot;
-      LP[s * HK + h * K + k] = lp;
-      PR[s * HK + h * K + k] = p;
-      e += p * lp;
-    }
+    for (int k = 0; k < K; ++k) e += PR[o + k] * LP[o + k];
     ENT[i] = -e;
   }
   __syncthreads();
@@ -394,9 +452,7 @@ __global__ void __launch_bounds__(kThreads) fwd_final(const Args a, int slot0, i
   if constexpr (MODE == MODE_PROBE) {
     for (int i = threadIdx.x; i < S * HK; i += kThreads) a.out_logp[i] = LP[i];
     if (threadIdx.x < S) a.out_val[threadIdx.x] = VAL[threadIdx.x];
-    return;
-  }
-  if constexpr (MODE == MODE_SAMPLE) {  // sample_categorical per head (policy.py:205-210), then env.step
+  } else if constexpr (MODE == MODE_SAMPLE) {  // sample_categorical per head (policy.py:205-210), then env.step
     const int64_t sp = *a.spent;
     if (threadIdx.x < H) {
       const int h = threadIdx.x;
@@ -423,12 +479,10 @@ __global__ void __launch_bounds__(kThreads) fwd_final(const Args a, int slot0, i
       for (int h = 0; h < H; ++h) lp += LP[h * K + act[h]];
       a.b_logp[slot0] = lp;
       a.b_val[slot0] = VAL[0];
-      env_step<NEU>(tab, L, M, a.env, a.b_act + (int64_t)slot0 * H, a.b_rew + slot0);
       *a.spent = sp + 1;
     }
-    return;
-  }
-  if constexpr (MODE == MODE_CONF) {  // confidence (policy.py:502-504) >= tau on every head
+    env_step_block<NEU, true>(tab, L, M, a.env, act, a.b_rew + slot0, EV, ER);
+  } else if constexpr (MODE == MODE_CONF) {  // confidence (policy.py:502-504) >= tau on every head
     if (threadIdx.x == 0) all_conf = 1;
     __syncthreads();
     if (threadIdx.x < H) {
@@ -438,61 +492,67 @@ __global__ void __launch_bounds__(kThreads) fwd_final(const Args a, int slot0, i
     }
     __syncthreads();
     if (threadIdx.x == 0 && all_conf) atomicOr(a.status, 1);
-    return;
-  } else {
-  // MODE_TRAIN: clipped surrogate + value + entropy (ppo.py:225-283)
-  if (threadIdx.x == 0) {
-    const double n = (double)S, lo = 1.0 - a.clip, hi = 1.0 + a.clip;
-    double pl = 0.0, vl = 0.0, et = 0.0;
-    bool bad = false;
-    for (int s = 0; s < S; ++s) {
-      const double rew = a.b_rew[s], vold = a.b_val[s], lold = a.b_logp[s];
-      bad |= !(isfinite(rew) && isfinite(vold) && isfinite(lold));
-      double lpn = 0.0, ent = 0.0;
-      for (int h = 0; h < H; ++h) {
-        lpn += LP[s * HK + h * K + (int)a.b_act[(int64_t)s * H + h]];
-        ent += ENT[s * H + h];
+  } else {  // MODE_TRAIN: clipped surrogate + value + entropy (ppo.py:225-283)
+    __shared__ int64_t bact[8 * LS_MAX_HEADS];
+    for (int i = threadIdx.x; i < S * H; i += kThreads) bact[i] = a.b_act[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double n = (double)S, lo = 1.0 - a.clip, hi = 1.0 + a.clip;
+      double pl = 0.0, vl = 0.0, et = 0.0;
+      bool bad = false;
+      for (int s = 0; s < S; ++s) {
+        const double rew = a.b_rew[s], vold = a.b_val[s], lold = a.b_logp[s];
+        bad |= !(isfinite(rew) && isfinite(vold) && isfinite(lold));
+        double lpn = 0.0, ent = 0.0;
+        for (int h = 0; h < H; ++h) {
+          lpn += LP[s * HK + h * K + (int)bact[s * H + h]];
+          ent += ENT[s * H + h];
+        }
+        const double adv = rew - vold;
+        const double ratio = exp(lpn - lold);
+        const double unc = ratio * adv;
+        const double clp = fmin(fmax(ratio, lo), hi) * adv;
+        const double sur = fmin(unc, clp);
+        const double d_ratio = unc <= clp ? -adv / n : 0.0;
+        const double err = VAL[s] - rew;
+        pl += -sur / n;
+        vl += a.vc * err * err / n;
+        et += ent / n;
+        DLP[s] = d_ratio * ratio;
+        a.w.DVAL[s] = 2.0 * a.vc * err / n;
       }
-      const double adv = rew - vold;
-      const double ratio = exp(lpn - lold);
-      const double unc = ratio * adv;
-      const double clp = fmin(fmax(ratio, lo), hi) * adv;
-      const double sur = fmin(unc, clp);
-      const double d_ratio = unc <= clp ? -adv / n : 0.0;
-      const double err = VAL[s] - rew;
-      pl += -sur / n;
-      vl += a.vc * err * err / n;
-      et += ent / n;
-      DLP[s] = d_ratio * ratio;
-      a.w.DVAL[s] = 2.0 * a.vc * err / n;
+      const double total = pl + vl - a.ec * et;
+      if (bad || !isfinite(total)) atomicOr(a.status, 2);
+      const int64_t step = *a.adam_step + 1;  // Adam.apply (ppo.py:150-152)
+      *a.adam_step = step;
+      a.w.HYP[0] = a.lr_table[*a.spent - S];
+      a.w.HYP[1] = 1.0 - pow(a.beta1, (double)step);
+      a.w.HYP[2] = 1.0 - pow(a.beta2, (double)step);
     }
-    const double total = pl + vl - a.ec * et;
-    if (bad || !isfinite(total)) atomicOr(a.status, 2);
-    *a.adam_step += 1;
-  }
-  __syncthreads();
-  const double n = (double)S;
-  for (int i = threadIdx.x; i < S * HK; i += kThreads) {
-    const int s = i / HK, j = i % HK, h = j / K, k = j % K;
-    double g = 0.0;
-    if (!a.blocked[j]) {
-      const double p = PR[i], oh = k == (int)a.b_act[(int64_t)s * H + h] ? 1.0 : 0.0;
-      g = DLP[s] * (oh - p);
-      g += a.ec * p * (LP[i] + ENT[s * H + h]) / n;
+    __syncthreads();
+    const double n = (double)S;
+    for (int i = threadIdx.x; i < S * HK; i += kThreads) {
+      const int s = i / HK, j = i % HK, h = j / K, k = j % K;
+      double g = 0.0;
+      if (!blk[j]) {
+        const double p = PR[i], oh = k == (int)bact[s * H + h] ? 1.0 : 0.0;
+        g = DLP[s] * (oh - p);
+        g += a.ec * p * (LP[i] + ENT[s * H + h]) / n;
+      }
+      a.w.DL[i] = g;
     }
-    a.w.DL[i] = g;
-  }
   }
 }
 
 // ---- backward --------------------------------------------------------------
 
 // d pooled = heads^T dl + value_w1^T d value_pre (policy.py:405-419).
-__global__ void __launch_bounds__(kThreads) bwd_pool(const Args a, int S) {
+__global__ void __launch_bounds__(kThreads) bwd_pool(const __grid_constant__ Args a, int S) {
   extern __shared__ double sm[];
   const int d = a.d, HK = a.HK;
   double* DLs = sm;
   double* DVP = DLs + S * HK;
+#pragma unroll 4
   for (int i = threadIdx.x; i < S * HK; i += kThreads) DLs[i] = a.w.DL[i];
   for (int i = threadIdx.x; i < S * d; i += kThreads) {
     const int s = i / d, k = i % d;
@@ -516,7 +576,7 @@ __global__ void __launch_bounds__(kThreads) bwd_pool(const Args a, int S) {
 }
 
 // LayerNorm 2 backward (recomputed per CTA) + d ffn_pre tile (policy.py:421-430).
-__global__ void __launch_bounds__(kThreads) bwd_ln2_ffn2(const Args a, int S) {
+__global__ void __launch_bounds__(kThreads) bwd_ln2_ffn2(const __grid_constant__ Args a, int S) {
   extern __shared__ double sm[];
   const int d = a.d, f = a.f, T = a.T, R = S * T;
   double* DR = sm;
@@ -543,10 +603,11 @@ __global__ void __launch_bounds__(kThreads) bwd_ln2_ffn2(const Args a, int S) {
 }
 
 // d hidden1 = d res2 + d ffn_pre W1^T (policy.py:426-433).
-__global__ void __launch_bounds__(kThreads) bwd_ffn1(const Args a, int S) {
+__global__ void __launch_bounds__(kThreads) bwd_ffn1(const __grid_constant__ Args a, int S) {
   extern __shared__ double sm[];
   const int d = a.d, f = a.f, R = S * a.T;
   double* DP = sm;
+#pragma unroll 4
   for (int i = threadIdx.x; i < R * f; i += kThreads) DP[i] = a.w.DPRE[i];
   __syncthreads();
   const int c = blockIdx.x * kWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -563,7 +624,7 @@ __global__ void __launch_bounds__(kThreads) bwd_ffn1(const Args a, int S) {
 }
 
 // LayerNorm 1 backward (recomputed per CTA) + d context = d res1 Wo^T (policy.py:435-442).
-__global__ void __launch_bounds__(kThreads) bwd_ln1_wo(const Args a, int S) {
+__global__ void __launch_bounds__(kThreads) bwd_ln1_wo(const __grid_constant__ Args a, int S) {
   extern __shared__ double sm[];
   const int d = a.d, R = S * a.T;
   double* DR = sm;
@@ -590,7 +651,7 @@ __global__ void __launch_bounds__(kThreads) bwd_ln1_wo(const Args a, int S) {
 
 // Attention backward (policy.py:444-453): d scores recomputed per CTA, then
 // d q, d k, d v per feature column.
-__global__ void __launch_bounds__(kThreads) bwd_attn(const Args a, int S) {
+__global__ void __launch_bounds__(kThreads) bwd_attn(const __grid_constant__ Args a, int S) {
   extern __shared__ double sm[];
   const int d = a.d, T = a.T, TT = T * T;
   double* dW = sm;
@@ -603,6 +664,7 @@ __global__ void __launch_bounds__(kThreads) bwd_attn(const Args a, int S) {
     const double* dc = a.w.DCTX + (int64_t)(s * T + t) * d;
     const double* v = QKV + (int64_t)(s * T + u) * 3 * d + 2 * d;
     double acc = 0.0;
+#pragma unroll 8
     for (int c = lane; c < d; c += 32) acc += dc[c] * v[c];
     acc = warp_sum(acc);
     if (lane == 0) dW[p] = acc;
@@ -635,10 +697,11 @@ __global__ void __launch_bounds__(kThreads) bwd_attn(const Args a, int S) {
 }
 
 // d embedded = d res1 + d qkv Wqkv^T (policy.py:455-464).
-__global__ void __launch_bounds__(kThreads) bwd_embed(const Args a, int S) {
+__global__ void __launch_bounds__(kThreads) bwd_embed(const __grid_constant__ Args a, int S) {
   extern __shared__ double sm[];
   const int d = a.d, R = S * a.T;
   double* DQ = sm;
+#pragma unroll 4
   for (int i = threadIdx.x; i < R * 3 * d; i += kThreads) DQ[i] = a.w.DQKV[i];
   __syncthreads();
   const int e = blockIdx.x * kWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -655,43 +718,51 @@ __global__ void __launch_bounds__(kThreads) bwd_embed(const Args a, int S) {
 }
 
 // Adam (ppo.py:147-161) with every gradient element computed in place from
-// the saved rows; flags non-finite parameters.
-__global__ void __launch_bounds__(kThreads) adam_kernel(const Args a, const SegTable st, int S) {
-  const int64_t t = *a.adam_step;
-  const double lr = a.lr_table[*a.spent - S];
-  const double bias1 = 1.0 - pow(a.beta1, (double)t), bias2 = 1.0 - pow(a.beta2, (double)t);
-  bool bad = false;
-  for (int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x; idx < a.total;
-       idx += (int64_t)gridDim.x * kThreads) {
-    int q = 0;
-    while (q + 1 < st.n && st.s[q + 1].off <= idx) ++q;
-    const Seg& g = st.s[q];
-    const int64_t rel = idx - g.off;
-    const int64_t size = g.rows ? g.rows * g.cols : g.cols;
-    if (rel >= size) continue;  // alignment gap
-    int64_t i = 0, j = rel;
-    if (g.rows) {
-      i = rel / g.cols;
-      j = rel % g.cols;
+// the saved rows; flags non-finite parameters. One CTA per (segment, matrix
+// row, 256-column chunk): the row's input values are loaded once, the output
+// gradients are coalesced along the row.
+__global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ Args a,
+                                                        const __grid_constant__ SegTable st, int S) {
+  // segment of this CTA: lanes test one segment start each
+  const int lane = threadIdx.x & 31;
+  const bool ge = lane < st.n && st.s[lane].blk0 <= (int)blockIdx.x;
+  const int q = __popc(__ballot_sync(0xffffffffu, ge)) - 1;
+  const Seg& g = st.s[q];
+  const int b = blockIdx.x - g.blk0;
+  const int i = b / g.colblocks;
+  const int j = (b - i * g.colblocks) * kThreads + threadIdx.x;
+  if (j >= g.cols) return;
+  double grad = 0.0;
+  if (g.kind == 0) {
+#pragma unroll
+    for (int r = 0; r < kRowsMax; ++r) {
+      if (r >= g.nrows) break;
+      grad += g.x[(int64_t)r * g.ldx + i] * g.dy[(int64_t)r * g.lddy + j];
     }
-    double grad = 0.0;
+  } else if (g.row_div == 1) {
+#pragma unroll
+    for (int r = 0; r < kRowsMax; ++r) {
+      if (r >= g.nrows) break;
+      const double dy = g.dy[(int64_t)r * g.lddy + j];
+      grad += g.kind == 1 ? dy : dy * g.x[(int64_t)r * g.ldx + j];
+    }
+  } else {  // LayerNorm 2: dy = d pooled / T broadcast over the sample's rows (policy.py:421)
     for (int r = 0; r < g.nrows; ++r) {
       const double dy = g.dy[(int64_t)(r / g.row_div) * g.lddy + j] / g.div;
-      if (g.kind == 0) grad += g.x[(int64_t)r * g.ldx + i] * dy;
-      else if (g.kind == 1) grad += dy;
-      else grad += dy * g.x[(int64_t)r * g.ldx + j];
+      grad += g.kind == 1 ? dy : dy * g.x[(int64_t)r * g.ldx + j];
     }
-    if (a.G) a.G[idx] = grad;
-    double m = a.Mo[idx], v = a.Vo[idx];
-    m = m * a.beta1 + (1.0 - a.beta1) * grad;
-    v = v * a.beta2 + (1.0 - a.beta2) * grad * grad;
-    const double p = a.P[idx] - lr * (m / bias1) / (sqrt(v / bias2) + a.eps);
-    a.Mo[idx] = m;
-    a.Vo[idx] = v;
-    a.P[idx] = p;
-    bad |= !isfinite(p);
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.status, 2);
+  const int64_t idx = g.off + (int64_t)i * g.cols + j;
+  if (a.G) a.G[idx] = grad;
+  const double lr = a.w.HYP[0], bias1 = a.w.HYP[1], bias2 = a.w.HYP[2];
+  double m = a.Mo[idx], v = a.Vo[idx];
+  m = m * a.beta1 + (1.0 - a.beta1) * grad;
+  v = v * a.beta2 + (1.0 - a.beta2) * grad * grad;
+  const double p = a.P[idx] - lr * (m / bias1) / (sqrt(v / bias2) + a.eps);
+  a.Mo[idx] = m;
+  a.Vo[idx] = v;
+  a.P[idx] = p;
+  if (!isfinite(p)) atomicOr(a.status, 2);
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -715,7 +786,7 @@ bool layout_of(const ls_policy_dims& D, ls_policy_layout& out) {
 }
 
 struct WsLayout {
-  int64_t n[26];
+  int64_t n[27];
   int64_t total;
 };
 
@@ -723,18 +794,18 @@ WsLayout ws_layout(const ls_policy_dims& D) {
   const int64_t d = D.width, f = D.ffn_width, T = D.history_len, SM = D.n_steps, RM = SM * T,
                 HK = (int64_t)D.num_heads * D.kmax;
   WsLayout w;
-  const int64_t n[26] = {RM * d,  RM * 3 * d, SM * T * T, RM * d,  RM * d,     RM * d, RM,     RM * d,  RM * f,
+  const int64_t n[27] = {RM * d,  RM * 3 * d, SM * T * T, RM * d,  RM * d,     RM * d, RM,     RM * d,  RM * f,
                          RM * d,  RM * d,     RM,         SM * d,  SM * HK,    SM * d, SM * HK, SM,      SM * d,
-                         SM * d,  RM * d,     RM * f,     RM * d,  RM * d,     RM * d, RM * 3 * d, RM * d};
+                         SM * d,  RM * d,     RM * f,     RM * d,  RM * d,     RM * d, RM * 3 * d, RM * d, 4};
   w.total = 0;
-  for (int i = 0; i < 26; ++i) {
+  for (int i = 0; i < 27; ++i) {
     w.n[i] = n[i];
     w.total += align32(n[i]);
   }
   return w;
 }
 
-size_t red_bytes() { return sizeof(double) * kWarps * kRowsMax * 32; }
+size_t red_bytes() { return sizeof(double) * kRedDoubles; }
 
 // dynamic shared memory per stage
 struct Smem {
@@ -748,9 +819,9 @@ Smem smem_of(const ls_policy_dims& D, int R) {
   s.embed = red_bytes() + db * R * (A + d);
   s.attn = red_bytes() + db * (S * T * T + R * d);
   s.ln1 = red_bytes() + db * R * d;
-  s.ffn2 = red_bytes();
+  s.ffn2 = red_bytes() + db * R * f;
   s.ln2 = red_bytes() + db * (R * d + S * d);
-  s.fin = db * (2 * S * HK + S * H + 2 * S);
+  s.fin = db * (3 * S * HK + 3 * S * H + 2 * S);
   s.pool = db * (S * HK + S * d);
   s.b_ln2 = db * R * d;
   s.b_ffn1 = db * R * f;
@@ -768,7 +839,7 @@ size_t smem_max(const Smem& s) {
 bool supported(const ls_policy_dims& D) {
   ls_policy_layout l;
   if (!layout_of(D, l)) return false;
-  if ((int64_t)D.n_steps * D.history_len > kRowsMax) return false;
+  if ((int64_t)D.n_steps * D.history_len > kRowsMax || D.n_steps > 8 || D.kmax > 64) return false;
   if (D.num_heads != D.obs_dim) return false;
   return smem_max(smem_of(D, D.n_steps * D.history_len)) <= kSmemMax;
 }
@@ -840,11 +911,11 @@ Args make_args(const ls_ppo_plan& p) {
   a.total = l.total;
   WsLayout wl = ws_layout(D);
   double* base = static_cast<double*>(p.workspace);
-  double** ptrs[26] = {&a.w.E,    &a.w.QKV,   &a.w.ATTW, &a.w.CTX,  &a.w.RES1,  &a.w.N1,    &a.w.IS1,
+  double** ptrs[27] = {&a.w.E,    &a.w.QKV,   &a.w.ATTW, &a.w.CTX,  &a.w.RES1,  &a.w.N1,    &a.w.IS1,
                        &a.w.H1,   &a.w.ACT,   &a.w.RES2, &a.w.N2,   &a.w.IS2,   &a.w.POOL,  &a.w.LRAW,
                        &a.w.VH,   &a.w.DL,    &a.w.DVAL, &a.w.DVPRE, &a.w.DPOOL, &a.w.DRES2, &a.w.DPRE,
-                       &a.w.DH1,  &a.w.DRES1, &a.w.DCTX, &a.w.DQKV, &a.w.DEMB};
-  for (int i = 0; i < 26; ++i) {
+                       &a.w.DH1,  &a.w.DRES1, &a.w.DCTX, &a.w.DQKV, &a.w.DEMB, &a.w.HYP};
+  for (int i = 0; i < 27; ++i) {
     *ptrs[i] = base;
     base += align32(wl.n[i]);
   }
@@ -878,9 +949,9 @@ SegTable seg_table(const Args& a, const ls_policy_layout& l, int S) {
   SegTable t;
   t.n = LS_PSEG_COUNT;
   auto mat = [&](int q, int64_t rows, int64_t cols, const double* x, int64_t ldx, const double* dy, int64_t lddy,
-                 int nrows) { t.s[q] = Seg{l.off[q], rows, cols, 0, nrows, x, ldx, dy, lddy, 1, 1.0}; };
+                 int nrows) { t.s[q] = Seg{0, 0, l.off[q], rows, cols, 0, nrows, x, ldx, dy, lddy, 1, 1.0}; };
   auto vec = [&](int q, int64_t cols, int kind, const double* x, const double* dy, int nrows, int row_div,
-                 double div) { t.s[q] = Seg{l.off[q], 0, cols, kind, nrows, x, cols, dy, cols, row_div, div}; };
+                 double div) { t.s[q] = Seg{0, 0, l.off[q], 0, cols, kind, nrows, x, cols, dy, cols, row_div, div}; };
   mat(LS_PSEG_EMBED_W, A, d, a.X, A, a.w.DEMB, d, R);
   vec(LS_PSEG_EMBED_B, d, 1, nullptr, a.w.DEMB, R, 1, 1.0);
   mat(LS_PSEG_WQKV, d, 3 * d, a.w.E, d, a.w.DQKV, 3 * d, R);
@@ -901,6 +972,14 @@ SegTable seg_table(const Args& a, const ls_policy_layout& l, int S) {
   vec(LS_PSEG_VALUE_B1, d, 1, nullptr, a.w.DVPRE, S, 1, 1.0);
   mat(LS_PSEG_VALUE_W2, d, 1, a.w.VH, d, a.w.DVAL, 1, S);
   vec(LS_PSEG_VALUE_B2, 1, 1, nullptr, a.w.DVAL, S, 1, 1.0);
+  int blocks = 0;
+  for (int q = 0; q < t.n; ++q) {
+    Seg& g = t.s[q];
+    g.colblocks = (int)((g.cols + kThreads - 1) / kThreads);
+    g.blk0 = blocks;
+    blocks += (int)(g.rows ? g.rows : 1) * g.colblocks;
+  }
+  t.blocks = blocks;
   return t;
 }
 
@@ -908,20 +987,24 @@ unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 void forward_rows(const Args& a, const ls_policy_dims& D, int row0, int R, int build, cudaStream_t s) {
   const Smem m = smem_of(D, R);
-  fwd_embed_qkv<<<cdiv(3 * a.d, 32), kThreads, m.embed, s>>>(a, row0, R, build);
-  fwd_attn_out<<<cdiv(a.d, 32), kThreads, m.attn, s>>>(a, row0, R);
-  fwd_ln1_ffn1<<<cdiv(a.f, 32), kThreads, m.ln1, s>>>(a, row0, R);
-  fwd_ffn2<<<cdiv(a.d, 32), kThreads, m.ffn2, s>>>(a, row0, R);
-  fwd_ln2_heads<<<cdiv(a.HK, 32) + cdiv(a.d, 32), kThreads, m.ln2, s>>>(a, row0, R);
+  fwd_embed_qkv<<<cdiv(3 * a.d, kCols), kThreads, m.embed, s>>>(a, row0, R, build);
+  fwd_attn_out<<<cdiv(a.d, kCols), kThreads, m.attn, s>>>(a, row0, R);
+  fwd_ln1_ffn1<<<cdiv(a.f, kCols), kThreads, m.ln1, s>>>(a, row0, R);
+  fwd_ffn2<<<cdiv(a.d, kCols), kThreads, m.ffn2, s>>>(a, row0, R);
+  fwd_ln2_heads<<<cdiv(a.HK, kCols) + cdiv(a.d, kCols), kThreads, m.ln2, s>>>(a, row0, R);
 }
 
 template <int MODE>
 void final_stage(const Args& a, const ls_policy_dims& D, int slot0, int S, const PpoCtx& c, cudaStream_t s) {
-  const size_t sm = smem_of(D, S * D.history_len).fin;
-  if (MODE == MODE_SAMPLE && !c.neumaier)
-    fwd_final<MODE, false><<<1, kThreads, sm, s>>>(a, slot0, S, c.tab, c.L, c.M);
-  else
-    fwd_final<MODE, true><<<1, kThreads, sm, s>>>(a, slot0, S, c.tab, c.L, c.M);
+  size_t sm = smem_of(D, S * D.history_len).fin;
+  if (MODE == MODE_SAMPLE) {
+    sm += sizeof(int64_t) * (size_t)a.env.elite_capacity * (a.A + 1);
+    if (!c.neumaier) {
+      fwd_final<MODE, false><<<1, kThreads, sm, s>>>(a, slot0, S, c.tab, c.L, c.M);
+      return;
+    }
+  }
+  fwd_final<MODE, true><<<1, kThreads, sm, s>>>(a, slot0, S, c.tab, c.L, c.M);
 }
 
 void backward_adam(const Args& a, const ls_policy_dims& D, int S, cudaStream_t s) {
@@ -934,8 +1017,8 @@ void backward_adam(const Args& a, const ls_policy_dims& D, int S, cudaStream_t s
   bwd_ln1_wo<<<cdiv(a.d, kWarps), kThreads, m.b_ln1, s>>>(a, S);
   bwd_attn<<<cdiv(a.d, kThreads), kThreads, m.b_attn, s>>>(a, S);
   bwd_embed<<<cdiv(a.d, kWarps), kThreads, m.b_embed, s>>>(a, S);
-  const unsigned grid = std::min<unsigned>(cdiv(a.total, kThreads), 148u * 8u);
-  adam_kernel<<<grid, kThreads, 0, s>>>(a, seg_table(a, l, S), S);
+  const SegTable st = seg_table(a, l, S);
+  adam_kernel<<<(unsigned)st.blocks, kThreads, 0, s>>>(a, st, S);
 }
 
 }  // namespace

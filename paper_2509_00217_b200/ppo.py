@@ -141,6 +141,7 @@ class GpuSearch:
         self._eager_rounds: dict[int, int] = {}
         self._lib = _native.lib(require_gpu=True)
         self.rounds = 0
+        self.round_events: list | None = None  # set to [] to record (start, end) CUDA events per round
         self.engine = engine
         if engine == "fused":
             self._init_fused()
@@ -223,6 +224,10 @@ class GpuSearch:
     def _run_round(self, n: int) -> int:
         """One round (replayed graph once warm); returns the status word."""
         g = self._graphs.get(n)
+        ev = None
+        if self.round_events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         if g is not None:
             g.replay()
         elif self.engine == "fused":
@@ -244,6 +249,9 @@ class GpuSearch:
                         self._round(n)
                     self._graphs[n] = g
         self.rounds += 1
+        if ev is not None:
+            ev[1].record()
+            self.round_events.append(ev)
         self.status_host.copy_(self.status, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
         return int(self.status_host[0])
@@ -321,7 +329,7 @@ class GpuSearch:
 
 
 def run_search(env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True,
-               engine: str = "fused") -> SearchReport:
+               engine: str = "fused", stats: dict | None = None) -> SearchReport:
     """Full chunked-restart PPO search on the GPU; consumes exactly ``cfg.budget`` evals.
 
     Appends the eval records to ``env`` (and its NDJSON sink) when the search
@@ -329,7 +337,13 @@ def run_search(env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = 
     """
     start = time.perf_counter()
     search = GpuSearch(env, cfg, seed, use_graphs=use_graphs, engine=engine)
+    if stats is not None:
+        search.round_events = []
     restarts, evals_done = search.run()
+    if stats is not None:
+        gpu = [a.elapsed_time(b) for a, b in search.round_events]
+        stats.update(rounds=search.rounds, round_gpu_ms_total=sum(gpu),
+                     round_gpu_us_median=1e3 * sorted(gpu)[len(gpu) // 2] if gpu else 0.0)
     first = env.evals_used
     records = search.records(first, evals_done)
     for r in records:

@@ -45,33 +45,34 @@ def prefix(env, case):
 @pytest.mark.parametrize("engine", ["fused", "torch"])
 def test_tiny_search_reproduces_reference_trajectory(case, engine):
     """Same PCG64 stream, same reward arithmetic: the GPU search walks the
-    reference's trajectory (float64 policy math differs only in rounding)."""
+    reference's trajectory. The fused kernels reproduce the whole eval log;
+    the autograd engine's float64 rounding (cuBLAS order) lets it drift after
+    a while, so it only has to agree on the opening stretch."""
     name, seed = case.rsplit("_", 1)
     m = META[case]
     env, _ = make_env(name, m["evals"])
     rep = run_search(env, PpoConfig(budget=m["evals"]), int(seed), engine=engine)
     assert rep.evals == m["evals"] == len(env.eval_log)
     k = prefix(env, case)
-    assert k >= 40, f"trajectory diverged from the reference after {k} evals"
-    if k == m["evals"]:
-        assert list(rep.restarts) == m["restarts"]
-        assert rep.best_raw == m["best_raw"] and list(rep.best_vector) == m["best_vector"]
+    if engine == "torch":
+        assert k >= 40, f"trajectory diverged from the reference after {k} evals"
+        return
+    assert k == m["evals"], f"trajectory diverged from the reference after {k} evals"
+    assert list(rep.restarts) == m["restarts"]
+    assert rep.best_raw == m["best_raw"] and list(rep.best_vector) == m["best_vector"]
+    np.testing.assert_array_equal(np.asarray([r.raw for r in env.eval_log]), GOLD[case + "_raws"])
 
 
-def test_flagship_search_matches_reference_quality():
-    """1.2T, budget 4000, seed 0: the reference's trajectory (or one of equal quality)."""
-    case = "moe_1p2t_h100_0"
+@pytest.mark.parametrize("case", ["moe_1p2t_h100_0", "moe_1p2t_h100_3"])
+def test_flagship_search_reproduces_reference_run(case):
+    """1.2T, budget 4000: the reference's full eval log, restarts and winner."""
     m = META[case]
     env, _ = make_env("moe_1p2t_h100", m["evals"])
-    rep = run_search(env, PpoConfig(budget=m["evals"]), 0)
+    rep = run_search(env, PpoConfig(budget=m["evals"]), int(case.rsplit("_", 1)[1]))
     assert rep.evals == 4000
-    k = prefix(env, case)
-    if k < 4000:
-        # diverged late: the search must still be a healthy PPO run
-        assert k >= 500, f"diverged after {k} evals"
-        assert rep.best_raw >= 0.8 * m["best_raw"]
-    else:
-        assert rep.best_raw == m["best_raw"]
+    assert prefix(env, case) == 4000
+    assert list(rep.restarts) == m["restarts"]
+    assert rep.best_raw == m["best_raw"] and list(rep.best_vector) == m["best_vector"]
 
 
 def test_records_rewards_and_best_are_consistent():
@@ -152,7 +153,7 @@ def _randomize(search, seed=0):
         pol.head_b.copy_(torch.from_numpy(rng.normal(0, 0.3, tuple(pol.head_b.shape))))
         pol.value_w2.copy_(torch.from_numpy(rng.normal(0, 0.3, tuple(pol.value_w2.shape))))
         for t in (pol.ln1_g, pol.ln2_g):
-            t.add_(torch.from_numpy(rng.normal(0, 0.1, tuple(t.shape))))
+            t.add_(torch.from_numpy(rng.normal(0, 0.1, tuple(t.shape))).to(t.device))
     return rng
 
 
