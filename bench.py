@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--e2e-n", type=int, default=1 << 26, help="candidates per GPU per e2e step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-search", action="store_true", help="skip the PPO search wall-time line")
     return ap.parse_args()
 
 
@@ -176,6 +177,37 @@ class Clocks:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+# reference run_search on moe_1p2t_h100, budget 4000, seed 0, in this image's CPU
+# container (BASELINE.md "Search-level reference points")
+REF_SEARCH_WALL_S = 105.8
+REF_SEARCH_BEST_RAW = 41.90363518619595
+
+
+def ppo_search_line():
+    """Wall time of one full PPO search through the public
+    API: ppo.run_search on the flagship 1.2T config, budget 4000, seed 0."""
+    from paper_2509_00217_b200.config import load_workload
+    from paper_2509_00217_b200.env import SearchEnv
+    from paper_2509_00217_b200.knobs import PpoConfig
+    from paper_2509_00217_b200.ppo import run_search
+
+    wl = load_workload("moe_1p2t_h100")
+
+    def one(budget):
+        env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, budget, slo_tpot=wl.slo_tpot)
+        env.evaluator
+        t0 = time.perf_counter()
+        rep = run_search(env, PpoConfig(budget=budget), 0)
+        return time.perf_counter() - t0, rep
+
+    one(200)  # loads kernels, first graph captures
+    wall, rep = one(4000)
+    return {"workload": "moe_1p2t_h100 PPO run_search, budget 4000, seed 0 (fused policy kernels + CUDA graphs)",
+            "wall_s": wall, "evals": rep.evals, "evals_per_s": rep.evals / wall, "best_raw": rep.best_raw,
+            "reference_wall_s": REF_SEARCH_WALL_S, "reference_best_raw": REF_SEARCH_BEST_RAW,
+            "same_best_as_reference": rep.best_raw == REF_SEARCH_BEST_RAW}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -311,6 +343,8 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
         "elite_best": {"vector": list(elite[0].vector), "raw": elite[0].raw, "index": elite[0].index} if elite else None,
     }
+    if not args.no_search:
+        line["search"] = ppo_search_line()
     if not args.no_cpu:
         rate, cores, done = cpu_rate(wl, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",

@@ -133,8 +133,10 @@ class GpuSearch:
         self.action = torch.zeros(H, **i64)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
-        self.opt = torch.optim.Adam(self.policy.parameters(), lr=self.lr, betas=(0.9, 0.999), eps=1e-8,
-                                    capturable=True, foreach=True)
+        self.opt = None  # torch engine only (importing torch.optim costs seconds)
+        if engine == "torch":
+            self.opt = torch.optim.Adam(self.policy.parameters(), lr=self.lr, betas=(0.9, 0.999), eps=1e-8,
+                                        capturable=True, foreach=True)
         self.use_graphs = use_graphs
         self.stream = torch.cuda.Stream(device=dev)
         self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
@@ -260,9 +262,10 @@ class GpuSearch:
 
     def _start_chunk(self, allowance: int) -> None:
         self.policy.reset_parameters(self.rng)  # the reference's PolicyNetwork(rng=rng)
-        for st in self.opt.state.values():  # fresh optimizer
-            for v in st.values():
-                v.zero_()
+        if self.opt is not None:  # fresh optimizer
+            for st in self.opt.state.values():
+                for v in st.values():
+                    v.zero_()
         if self.engine == "fused":
             self.adam_m.zero_()
             self.adam_v.zero_()
