@@ -20,6 +20,13 @@
 
 using namespace ls;
 
+// ABI layouts the Python ctypes mirrors (_native.py) and tests rely on
+static_assert(sizeof(ls_workload_desc) == 2280, "ls_workload_desc layout");
+static_assert(sizeof(ls_elite_rec) == 32, "ls_elite_rec layout");
+static_assert(sizeof(ls_search_state) == 104, "ls_search_state layout");
+static_assert(sizeof(ls_policy_layout) == 168, "ls_policy_layout layout");
+static_assert(sizeof(ls_ppo_plan) == 344, "ls_ppo_plan layout");
+
 namespace {
 
 thread_local std::string g_err;

@@ -35,7 +35,7 @@ from .strategy import (
 from .workload import LS_MAX_DOMAIN, Workload
 
 __all__ = ["InvalidReason", "SimRequest", "TimeBreakdown", "SimResult", "simulate", "simulate_vector",
-           "result_from_row", "layout_error_detail"]
+           "result_from_row", "layout_error_detail", "explain"]
 
 
 class InvalidReason(str, Enum):
@@ -223,3 +223,32 @@ def _eval_one(ev: Evaluator, vec) -> dict:
 def simulate_vector(ev: Evaluator, vector, model=None, hw=None, strategy=None, slo=None) -> SimResult:
     """Score one index vector of ``ev``'s action space."""
     return result_from_row(_eval_one(ev, vector), 0, model, hw, strategy, slo)
+
+
+def explain(req: SimRequest) -> str:
+    """Human-readable account of one strategy (reference simulator.py:344-374):
+    verdict and times from the GPU evaluator, per-layer plan from the host
+    planner (plan.py)."""
+    from .plan import plan_layer
+
+    model, hw, s = req.model, req.hw, req.strategy
+    result = simulate(req)
+    lines = [f"strategy: tp={s.tp} ep={s.ep} pp={s.pp} batch={s.batch} world_size={s.world_size}",
+             "fine dims: " + " ".join(f"{n}={AxisChoice(a).name.lower()}" for n, a in zip(s.op_names, s.op_dims)),
+             f"valid: {result.valid}" + ("" if result.valid else f" ({result.invalid_reason.value}: {result.detail})")]
+    if result.invalid_reason in (InvalidReason.OVER_DEVICE_BUDGET, InvalidReason.LAYOUT_ERROR):
+        return "\n".join(lines)
+    lines.append(f"memory per device: {result.memory_bytes / 1e9:.3f} GB")
+    if result.invalid_reason is InvalidReason.OOM:
+        return "\n".join(lines)
+    lines.append(f"tpot: {result.tpot_s * 1e3:.4f} ms")
+    b = result.breakdown
+    lines.append(f"breakdown: compute {b.compute_s * 1e3:.4f} ms, comm {b.comm_s * 1e3:.4f} ms, "
+                 f"pipeline {b.pipeline_s * 1e3:.4f} ms")
+    if result.valid:
+        lines.append(f"throughput: {result.throughput:.4f} tokens/s/chip")
+    layer_ops = tuple(op for op in canonical_fused_ops(model) if op.per_layer)
+    plan = plan_layer(model, layer_ops, s, s.batch, hw.node_size)
+    lines.append("per-layer plan:")
+    lines.extend("  " + ln for ln in plan.describe().splitlines())
+    return "\n".join(lines)

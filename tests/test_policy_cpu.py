@@ -192,3 +192,37 @@ def test_checkpoint_round_trip_and_errors(wl, tmp_path):
         load_checkpoint(str(tmp_path / "short"))
     with pytest.raises(ValueError):
         other.load_state({k: v for k, v in back.items() if k != "ln1.g"})
+
+
+def test_arena_layout_matches_the_c_abi(wl):
+    """TorchPolicy's flat parameter arena is the layout ls_policy_layout_of
+    documents, so the fused kernels and autograd share storage."""
+    import ctypes
+
+    from paper_2509_00217_b200 import _native
+
+    lib = _native.lib()
+    for width, ffn, hist, steps in ((16, 8, 3, 2), (256, 256, 3, 2), (64, 64, 4, 4)):
+        pol = make_policy(wl, width=width, ffn=ffn)
+        dims = _native.PolicyDims(wl.space.vector_length, width, ffn, hist, pol.num_heads, pol.kmax, steps)
+        lay = _native.PolicyLayout()
+        assert lib.ls_policy_layout_of(ctypes.byref(dims), ctypes.byref(lay)) == 0
+        assert list(lay.off) == pol.offsets
+        assert lay.total == pol.flat.numel()
+        assert lib.ls_ppo_workspace_bytes(ctypes.byref(dims)) > 0
+    too_many_rows = _native.PolicyDims(wl.space.vector_length, 16, 8, 9, 16, 11, 2)
+    assert lib.ls_ppo_workspace_bytes(ctypes.byref(too_many_rows)) == 0
+    bad = _native.PolicyDims(0, 16, 8, 3, 16, 11, 2)
+    assert lib.ls_policy_layout_of(ctypes.byref(bad), ctypes.byref(_native.PolicyLayout())) != 0
+
+
+def test_search_structs_have_the_header_layout():
+    import ctypes
+
+    from paper_2509_00217_b200 import _native
+
+    assert ctypes.sizeof(_native.SearchState) == 104
+    assert ctypes.sizeof(_native.PolicyDims) == 28
+    assert ctypes.sizeof(_native.PolicyLayout) == 8 * 21
+    # dims (28, padded to 32) + 8 pointers + state + 10 pointers + 7 doubles + int (padded)
+    assert ctypes.sizeof(_native.PpoPlan) == 32 + 64 + 104 + 80 + 56 + 8
