@@ -161,6 +161,18 @@ int ls_evaluate(ls_ctx* ctx, const uint8_t* planes, int64_t n, int64_t plane_str
 int ls_evaluate_host(ls_ctx* ctx, const uint8_t* host_planes, int64_t n, int64_t plane_stride,
                      const ls_result_soa* host_out);
 
+/* Packed candidates (vectors of <= 16 heads): one uint64 word per candidate,
+ * axis head h in bits [2(h-4), 2(h-4)+2), then the tp/ep/pp/batch indices
+ * from bit 24 in the widths ls_packed_layout reports (8 B per candidate
+ * instead of A bytes of planes: the hot loop is HBM-bound, so fewer bytes
+ * is more candidates per second). Malformed words (bits outside the
+ * layout, an axis field of 3, an index past its domain) evaluate to
+ * LS_REASON_DECODE_ERROR, like out-of-range plane bytes. */
+int ls_packed_layout(ls_ctx* ctx, int32_t shift_out[4], int32_t bits_out[4]);
+int ls_pack(ls_ctx* ctx, const uint8_t* planes, int64_t plane_stride, int64_t n, uint64_t* words, void* stream);
+int ls_evaluate_packed(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, void* stream);
+int ls_evaluate_host_packed(ls_ctx* ctx, const uint64_t* host_words, int64_t n, const ls_result_soa* host_out);
+
 /* Pinned host memory helpers for ls_evaluate_host callers. */
 int ls_host_alloc(size_t bytes, void** out);
 int ls_host_free(void* ptr);
@@ -229,6 +241,10 @@ int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int
  * into the global top-k with the same ordering and dedupe rule. */
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                   ls_elite_rec* out, int32_t* count_out, void* stream);
+/* ls_evaluate_topk over packed words (fused path only: k <= 32). */
+int ls_evaluate_packed_topk(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
+                            int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                            void* stream);
 
 /* ---- Search-loop step (device-resident environment state) ---------------
  * One sequential environment step of a learning search, entirely on the

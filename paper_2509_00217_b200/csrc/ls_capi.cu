@@ -252,6 +252,25 @@ uint64_t stream_size(const GenMeta& g) {
 
 }  // namespace
 
+namespace ls {
+PackMeta pack_meta(const ls_workload_desc& d) {
+  PackMeta pk{};
+  uint32_t sh = 24;
+  for (int h = 0; h < 4; ++h) {
+    uint32_t bits = 1;
+    while ((1u << bits) < (uint32_t)d.domain_len[h]) ++bits;
+    pk.shift[h] = sh;
+    pk.mask[h] = (1u << bits) - 1u;
+    sh += bits;
+  }
+  const int A = d.vector_length;
+  pk.axis_mask = A > 4 ? (uint32_t)((1ull << (2 * (A - 4))) - 1ull) : 0u;
+  pk.used = pk.axis_mask;
+  for (int h = 0; h < 4; ++h) pk.used |= (uint64_t)pk.mask[h] << pk.shift[h];
+  return pk;
+}
+}  // namespace ls
+
 extern "C" {
 
 const char* ls_last_error(void) { return g_err.c_str(); }
@@ -325,13 +344,14 @@ uint64_t ls_space_size(const ls_ctx* c) { return c ? c->space_size : 0; }
 
 
 static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stride, const ls_result_soa* out,
-                       cudaStream_t s) {
+                       cudaStream_t s, const uint64_t* words = nullptr) {
   if (n < 0 || !out) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate arguments");
   if (n == 0) return LS_OK;
-  if (!out->reason || !planes) return fail(LS_ERR_INVALID_ARGUMENT, "null planes or reason buffer");
-  if (stride < n) return fail(LS_ERR_INVALID_ARGUMENT, "plane_stride must be >= n");
-  EvalArgs a;
+  if (!out->reason || (!planes && !words)) return fail(LS_ERR_INVALID_ARGUMENT, "null candidates or reason buffer");
+  if (!words && stride < n) return fail(LS_ERR_INVALID_ARGUMENT, "plane_stride must be >= n");
+  EvalArgs a{};
   a.planes = planes;
+  a.words = words;
   a.n = n;
   a.stride = stride;
   a.reason = out->reason;
@@ -345,7 +365,14 @@ static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stri
   lp.tma = tma_eligible(a, c->M.A) && c->blocks_tma > 0;
   lp.smem_gate = c->smem_gate;
   lp.max_blocks = lp.tma ? c->blocks_tma : c->blocks_generic;
-  cudaError_t e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, s);
+  PackMeta pk;
+  if (words) {
+    if (!lp.tma)
+      return fail(LS_ERR_UNSUPPORTED, "packed candidates need vectors of <= 16 heads and 16-byte aligned buffers");
+    pk = pack_meta(c->desc);
+  }
+  cudaError_t e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, s,
+                                  words ? &pk : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "evaluate launch");
   return LS_OK;
 }
@@ -358,6 +385,50 @@ int ls_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_strid
   return do_evaluate(c, planes, n, plane_stride, out, static_cast<cudaStream_t>(stream));
 }
 
+
+int ls_packed_layout(ls_ctx* c, int32_t* shift_out, int32_t* bits_out) {
+  g_err.clear();
+  if (!c || !shift_out || !bits_out) return fail(LS_ERR_INVALID_ARGUMENT, "null argument");
+  if (c->desc.vector_length > 16) return fail(LS_ERR_UNSUPPORTED, "packed candidates need vectors of <= 16 heads");
+  const PackMeta pk = pack_meta(c->desc);
+  for (int h = 0; h < 4; ++h) {
+    shift_out[h] = (int32_t)pk.shift[h];
+    bits_out[h] = __builtin_popcount(pk.mask[h]);
+  }
+  return LS_OK;
+}
+
+int ls_pack(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, int64_t n, uint64_t* words, void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || (n > 0 && (!planes || !words)) || plane_stride < n)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad pack arguments");
+  if (c->desc.vector_length > 16) return fail(LS_ERR_UNSUPPORTED, "packed candidates need vectors of <= 16 heads");
+  DeviceGuard g(c->device);
+  cudaError_t e = launch_pack(pack_meta(c->desc), c->desc.vector_length, planes, plane_stride, n, words,
+                              static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "pack launch");
+}
+
+int ls_evaluate_packed(ls_ctx* c, const uint64_t* words, int64_t n, const ls_result_soa* out, void* stream) {
+  g_err.clear();
+  if (!c) return fail(LS_ERR_INVALID_ARGUMENT, "null context");
+  if (n > 0 && !words) return fail(LS_ERR_INVALID_ARGUMENT, "null words");
+  DeviceGuard g(c->device);
+  return do_evaluate(c, nullptr, n, n, out, static_cast<cudaStream_t>(stream), words);
+}
+
+static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_stride, const uint64_t* host_words,
+                         int64_t n, const ls_result_soa* host_out);
+
+int ls_evaluate_host_packed(ls_ctx* c, const uint64_t* host_words, int64_t n, const ls_result_soa* host_out) {
+  g_err.clear();
+  if (!c || !host_out || n < 0) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host_packed arguments");
+  if (n == 0) return LS_OK;
+  if (!host_out->reason || !host_words) return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host_packed arguments");
+  if (c->desc.vector_length > 16) return fail(LS_ERR_UNSUPPORTED, "packed candidates need vectors of <= 16 heads");
+  return host_pipeline(c, nullptr, 0, host_words, n, host_out);
+}
+
 int ls_evaluate_host(ls_ctx* c, const uint8_t* host_planes, int64_t n, int64_t plane_stride,
                      const ls_result_soa* host_out) {
   g_err.clear();
@@ -365,6 +436,12 @@ int ls_evaluate_host(ls_ctx* c, const uint8_t* host_planes, int64_t n, int64_t p
   if (n == 0) return LS_OK;
   if (!host_out->reason || !host_planes || plane_stride < n)
     return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host arguments");
+  return host_pipeline(c, host_planes, plane_stride, nullptr, n, host_out);
+}
+
+// Chunked H2D -> evaluate -> D2H, double-buffered over two streams.
+static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_stride, const uint64_t* host_words,
+                         int64_t n, const ls_result_soa* host_out) {
   std::lock_guard<std::mutex> lock(c->host_mu);
   DeviceGuard g(c->device);
   const int A = c->desc.vector_length;
@@ -388,14 +465,20 @@ int ls_evaluate_host(ls_ctx* c, const uint8_t* host_planes, int64_t n, int64_t p
     const int s = (int)(chunk & 1);
     const int64_t cnt = std::min<int64_t>(kHostChunk, n - off);
     cudaStream_t st = c->hs[s];
-    if ((e = cudaMemcpy2DAsync(c->h_planes[s], (size_t)cnt, host_planes + off, (size_t)plane_stride, (size_t)cnt, A,
+    if (host_words) {
+      if ((e = cudaMemcpyAsync(c->h_planes[s], host_words + off, sizeof(uint64_t) * (size_t)cnt,
                                cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "H2D words");
+    } else if ((e = cudaMemcpy2DAsync(c->h_planes[s], (size_t)cnt, host_planes + off, (size_t)plane_stride,
+                                      (size_t)cnt, A, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
       return cuda_fail(e, "H2D planes");
+    }
     ls_result_soa dev;
     dev.reason = c->h_reason[s];
     double** dv[6] = {&dev.throughput, &dev.tpot_s, &dev.memory_bytes, &dev.compute_s, &dev.comm_s, &dev.pipeline_s};
     for (int f = 0; f < 6; ++f) *dv[f] = hf[f] ? c->h_f[s][f] : nullptr;
-    int rc = do_evaluate(c, c->h_planes[s], cnt, cnt, &dev, st);
+    int rc = host_words ? do_evaluate(c, nullptr, cnt, cnt, &dev, st, reinterpret_cast<const uint64_t*>(c->h_planes[s]))
+                        : do_evaluate(c, c->h_planes[s], cnt, cnt, &dev, st);
     if (rc) return rc;
     if ((e = cudaMemcpyAsync(host_out->reason + off, dev.reason, (size_t)cnt, cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)
@@ -457,16 +540,37 @@ size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
   return std::max(fused, topk_scratch_bytes(n, k, 0));
 }
 
+static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
+                              int64_t plane_stride, const ls_result_soa* out, int k, int64_t index_base,
+                              ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream);
+
 int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_stride, const ls_result_soa* out,
                      int k, int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
                      void* stream) {
   g_err.clear();
   if (!c || n < 0 || k < 1 || !topk_out || !count_out || !scratch || (n > 0 && !planes) || plane_stride < n)
     return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_topk arguments");
+  return evaluate_topk_impl(c, planes, nullptr, n, plane_stride, out, k, index_base, topk_out, count_out, scratch,
+                            stream);
+}
+
+int ls_evaluate_packed_topk(ls_ctx* c, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
+                            int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                            void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || k < 1 || !topk_out || !count_out || !scratch || (n > 0 && !words))
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_packed_topk arguments");
+  return evaluate_topk_impl(c, nullptr, words, n, n, out, k, index_base, topk_out, count_out, scratch, stream);
+}
+
+static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
+                              int64_t plane_stride, const ls_result_soa* out, int k, int64_t index_base,
+                              ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream) {
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   EvalArgs a{};
   a.planes = planes;
+  a.words = words;
   a.n = n;
   a.stride = plane_stride;
   if (out) {
@@ -493,14 +597,16 @@ int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_
     }
     if ((e = cudaMemsetAsync(tk.floor, 0, sizeof(unsigned long long), s)) != cudaSuccess)
       return cuda_fail(e, "floor reset");
-    if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s)) !=
-        cudaSuccess)
+    const PackMeta pk = pack_meta(c->desc);
+    if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s,
+                                  words ? &pk : nullptr)) != cudaSuccess)
       return cuda_fail(e, "evaluate_topk launch");
     if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, tk.floor, topk_out, count_out, s)) !=
         cudaSuccess)
       return cuda_fail(e, "topk merge launch");
     return LS_OK;
   }
+  if (words) return fail(LS_ERR_UNSUPPORTED, "packed candidates need k <= 32 and 16-byte aligned buffers");
   if (!a.reason || !a.thr)
     return fail(LS_ERR_UNSUPPORTED,
                 "unaligned planes, k > 32 or vectors longer than 16 heads need per-candidate reason + throughput "

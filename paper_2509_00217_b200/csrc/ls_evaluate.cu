@@ -53,6 +53,9 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ void lds_u64x2(uint32_t addr, uint64_t& x, uint64_t& y) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(addr));
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -145,6 +148,21 @@ __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, in
   // Y = q0.byte j | q1.byte j << 8 | q2.byte j << 16
   const uint32_t y01 = __byte_perm(q[0], q[1], 0x4440u | ((4u + j) << 4) | (uint32_t)j);
   c.Y = __byte_perm(y01, q[2], 0x4000u | ((4u + j) << 8) | 0x10u) & 0x00ffffffu;
+}
+
+// Packed candidate word -> fields (A <= 16, head slot = h - 4, so the axis
+// bits ARE the Y word). Nonzero return: malformed word or index out of range
+// (the planes path's decode error, strategy.py:247-254).
+__device__ __forceinline__ uint32_t word_decode(uint64_t w, const PackMeta& pk, const EvalMeta& M, Decoded& c) {
+  const uint32_t Y = (uint32_t)w & pk.axis_mask;
+  c.Y = Y;
+  c.t = (int)((uint32_t)(w >> pk.shift[0]) & pk.mask[0]);
+  c.e = (int)((uint32_t)(w >> pk.shift[1]) & pk.mask[1]);
+  c.p = (int)((uint32_t)(w >> pk.shift[2]) & pk.mask[2]);
+  c.b = (int)((uint32_t)(w >> pk.shift[3]) & pk.mask[3]);
+  const bool bad = (w & ~pk.used) != 0 || (Y & (Y >> 1) & 0x555555u) != 0 || c.t >= M.head_size[0] ||
+                   c.e >= M.head_size[1] || c.p >= M.head_size[2] || c.b >= M.head_size[3];
+  return bad ? 1u : 0u;
 }
 
 // ---- on-device candidate streams (ls_sweep) ----------------------------
@@ -267,9 +285,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t ring_base = smem_u32(S.ring);
   // plane slices >= A are never written by the TMA: zero them once so the
   // gate warps can load all 16 unconditionally (zero = in range, UNSHARDED)
-  for (int s = 0; s < kStages; ++s)
-    for (int o = A * kTile + 16 * (int)threadIdx.x; o < (int)kStageBytes; o += 16 * kThreads)
-      *reinterpret_cast<uint4*>(S.ring + s * kStageBytes + o) = make_uint4(0, 0, 0, 0);
+  if (MODE == GEN_PLANES)
+    for (int s = 0; s < kStages; ++s)
+      for (int o = A * kTile + 16 * (int)threadIdx.x; o < (int)kStageBytes; o += 16 * kThreads)
+        *reinterpret_cast<uint4*>(S.ring + s * kStageBytes + o) = make_uint4(0, 0, 0, 0);
   if (threadIdx.x < kWorkWarps) list_count[threadIdx.x] = 0;
   if (threadIdx.x < kGateWarps * kSlots) mb_state[threadIdx.x / kSlots][threadIdx.x % kSlots] = 0;
   if (threadIdx.x == 0) {
@@ -291,13 +310,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         bulk_g2s(S.gate, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
       }
       int i = 0;
-      for (int64_t tile = blockIdx.x; MODE == GEN_PLANES && tile < ntiles; tile += gridDim.x, ++i) {
+      for (int64_t tile = blockIdx.x; (MODE == GEN_PLANES || MODE == GEN_WORDS) && tile < ntiles;
+           tile += gridDim.x, ++i) {
         const int s = i % kStages, k = i / kStages;
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
-        mbar_expect_tx(&full_bar[s], stage_bytes);
-        const uint8_t* src = a.planes + tile * kTile;
         uint8_t* dst = S.ring + s * kStageBytes;
-        for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
+        if (MODE == GEN_WORDS) {  // one contiguous 8 KB tile of candidate words
+          mbar_expect_tx(&full_bar[s], 8u * kTile);
+          bulk_g2s(dst, a.words + tile * kTile, 8u * kTile, &full_bar[s]);
+        } else {
+          mbar_expect_tx(&full_bar[s], stage_bytes);
+          const uint8_t* src = a.planes + tile * kTile;
+          for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
+        }
       }
     }
     return;
@@ -479,6 +504,33 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
         pass_a(cs, badb, base, count);
       }
+    } else if (MODE == GEN_WORDS) {  // 4 consecutive 8-byte candidate words per lane
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i % kStages;
+        mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
+        uint64_t w[4];
+        const uint32_t st = ring_base + (uint32_t)s * kStageBytes + 8u * (uint32_t)lane_off;
+        lds_u64x2(st, w[0], w[1]);
+        lds_u64x2(st + 16, w[2], w[3]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        Decoded cs[4];
+        uint32_t badb = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) badb |= word_decode(w[j], gm.pk, M, cs[j]) << (8 * j);
+        pass_a(cs, badb, tile * kTile + lane_off, 4);
+      }
+      const int64_t tail0 = ntiles * kTile;
+      if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
+        const int64_t base = tail0 + lane_off;
+        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+        Decoded cs[4];
+        uint32_t badb = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, M, cs[j]) << (8 * j);
+        pass_a(cs, badb, base, count);
+      }
     } else {  // candidates generated in registers: nothing read from HBM
       const int64_t gtiles = (a.n + kTile - 1) / kTile;
       for (int64_t tile = blockIdx.x; tile < gtiles; tile += gridDim.x) {
@@ -555,6 +607,8 @@ void set_attr(size_t smem) {
   const int b = (int)smem;
   cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, false, GEN_PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
   cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, true, GEN_PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, false, GEN_WORDS>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(eval_ws_kernel<NEU, FULL, SG, true, GEN_WORDS>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
   if (!FULL) {
     cudaFuncSetAttribute(eval_ws_kernel<NEU, false, SG, true, GEN_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          b);
@@ -567,7 +621,7 @@ void set_attr(size_t smem) {
 template <bool NEU, bool FULL, bool TOPK, int MODE = GEN_PLANES>
 void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, const EvalArgs& a,
                  const TopkArgs& tk, cudaStream_t s, const GenMeta& gm = GenMeta{}) {
-  const int64_t ntiles = MODE == GEN_PLANES ? a.n / kTile : (a.n + kTile - 1) / kTile;
+  const int64_t ntiles = (MODE == GEN_PLANES || MODE == GEN_WORDS) ? a.n / kTile : (a.n + kTile - 1) / kTile;
   const size_t smem = ws_dynamic_bytes(M.A, L.gate_words, lp.smem_gate);
   int64_t blocks = ntiles > 0 ? ntiles : 1;
   if (blocks > lp.max_blocks) blocks = lp.max_blocks;
@@ -594,7 +648,19 @@ __global__ void generate_kernel(const GenMeta gm, int64_t n, int A, const EvalMe
 
 template <bool TOPK>
 void launch_ws(const LaunchPlan& lp, bool neumaier, bool full, const uint64_t* tab, const TabLayout& L,
-               const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
+               const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s, const PackMeta* pk) {
+  if (pk) {
+    GenMeta gm{};
+    gm.pk = *pk;
+    if (neumaier) {
+      if (full) launch_ws_t<true, true, TOPK, GEN_WORDS>(lp, tab, L, M, a, tk, s, gm);
+      else launch_ws_t<true, false, TOPK, GEN_WORDS>(lp, tab, L, M, a, tk, s, gm);
+    } else {
+      if (full) launch_ws_t<false, true, TOPK, GEN_WORDS>(lp, tab, L, M, a, tk, s, gm);
+      else launch_ws_t<false, false, TOPK, GEN_WORDS>(lp, tab, L, M, a, tk, s, gm);
+    }
+    return;
+  }
   if (neumaier) {
     if (full) launch_ws_t<true, true, TOPK>(lp, tab, L, M, a, tk, s);
     else launch_ws_t<true, false, TOPK>(lp, tab, L, M, a, tk, s);
@@ -604,12 +670,35 @@ void launch_ws(const LaunchPlan& lp, bool neumaier, bool full, const uint64_t* t
   }
 }
 
+// SoA planes -> packed candidate words (A <= 16). Out-of-range heads pack
+// to a malformed word (all used bits of the field set plus an unused bit),
+// so they still evaluate to LS_REASON_DECODE_ERROR.
+__global__ void pack_kernel(const PackMeta pk, int A, const uint8_t* __restrict__ planes, int64_t stride, int64_t n,
+                            uint64_t* __restrict__ words) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w = 0;
+    bool bad = false;
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t v = planes[(int64_t)h * stride + i];
+      bad |= v > pk.mask[h];
+      w |= (uint64_t)(v & pk.mask[h]) << pk.shift[h];
+    }
+    for (int h = 4; h < A; ++h) {
+      const uint32_t v = planes[(int64_t)h * stride + i];
+      bad |= v > 3;
+      w |= (uint64_t)(v & 3u) << (2 * (h - 4));
+    }
+    words[i] = bad ? ~0ull : w;
+  }
+}
+
 }  // namespace
 
 size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) { return ws_dynamic_bytes(A, L.gate_words, smem_gate); }
 
 bool tma_eligible(const EvalArgs& a, int A) {
-  const bool al16 = ((uintptr_t)a.planes % 16) == 0 && a.stride % 16 == 0;
+  const bool al16 = a.words ? ((uintptr_t)a.words % 16) == 0
+                            : ((uintptr_t)a.planes % 16) == 0 && a.stride % 16 == 0;
   bool out_al = ((uintptr_t)a.reason % 4) == 0;
   const double* fs[6] = {a.thr, a.tpot, a.mem, a.comp, a.comm, a.pipe};
   for (const double* f : fs) out_al = out_al && ((uintptr_t)f % 16) == 0;
@@ -658,12 +747,21 @@ int64_t ws_grid(const LaunchPlan& lp, int64_t n) {
 
 int fused_k_max() { return kFusedK; }
 
+cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
+                        cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  pack_kernel<<<(unsigned)blocks, 256, 0, s>>>(pk, A, planes, stride, n, words);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
-                            const EvalMeta& M, const EvalArgs& a, cudaStream_t s) {
+                            const EvalMeta& M, const EvalArgs& a, cudaStream_t s, const PackMeta* pk) {
   if (a.n <= 0) return cudaSuccess;
   const bool full = a.tpot || a.mem || a.comp || a.comm || a.pipe;
-  if (lp.tma) {
-    launch_ws<false>(lp, neumaier, full, tab, L, M, a, TopkArgs{}, s);
+  if (lp.tma || pk) {
+    launch_ws<false>(lp, neumaier, full, tab, L, M, a, TopkArgs{}, s, pk);
   } else {
     int64_t blocks = (a.n + kGenericThreads - 1) / kGenericThreads;
     if (blocks > lp.max_blocks) blocks = lp.max_blocks;
@@ -674,9 +772,10 @@ cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t*
 }
 
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
-                                 const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s) {
+                                 const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s,
+                                 const PackMeta* pk) {
   const bool full = a.reason && (a.tpot || a.mem || a.comp || a.comm || a.pipe);
-  launch_ws<true>(lp, neumaier, full, tab, L, M, a, tk, s);
+  launch_ws<true>(lp, neumaier, full, tab, L, M, a, tk, s, pk);
   return cudaGetLastError();
 }
 

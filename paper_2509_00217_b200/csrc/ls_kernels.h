@@ -10,6 +10,7 @@ namespace ls {
 
 struct EvalArgs {
   const uint8_t* planes;
+  const uint64_t* words;  // packed candidate words (GEN_WORDS) instead of planes
   int64_t n;
   int64_t stride;
   uint8_t* reason;
@@ -35,7 +36,17 @@ struct TopkArgs {
 };
 
 // Candidate sources of eval_ws_kernel.
-enum : int { GEN_PLANES = 0, GEN_UNIFORM = 1, GEN_ENUM = 2, GEN_ENUM_ADMISSIBLE = 3 };
+enum : int { GEN_PLANES = 0, GEN_UNIFORM = 1, GEN_ENUM = 2, GEN_ENUM_ADMISSIBLE = 3, GEN_WORDS = 4 };
+
+// Packed candidate word (A <= 16): axis head h in bits [2(h-4), 2(h-4)+2),
+// then t, e, p, b from bit 24 in the minimal widths of their domains.
+struct PackMeta {
+  uint32_t shift[4];
+  uint32_t mask[4];
+  uint32_t axis_mask;  // low 2(A-4) bits
+  uint64_t used;       // every bit a valid word may set
+};
+PackMeta pack_meta(const ls_workload_desc& d);
 
 // On-device candidate stream: index -> (coarse rank, axis rank) -> decoded
 // candidate. Axis ranks split into a high and a low group of axis heads whose
@@ -48,6 +59,7 @@ struct GenMeta {
   uint64_t nb, np, ne;
   const uint32_t* hi_tab;  // [axis_size / lo_size] packed Y of the high group
   const uint32_t* lo_tab;  // [lo_size] packed Y of the low group
+  PackMeta pk;             // GEN_WORDS field layout
 };
 
 bool tma_eligible(const EvalArgs& a, int A);
@@ -55,16 +67,19 @@ cudaError_t launch_sweep(const LaunchPlan& lp, bool neumaier, int mode, const ui
                          const EvalMeta& M, int64_t n, const TopkArgs& tk, const GenMeta& gm, cudaStream_t s);
 cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8_t* planes, int64_t stride,
                             cudaStream_t s);
+cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
+                        cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n);
 int fused_k_max();
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
-                                 const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s);
+                                 const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s,
+                                 const PackMeta* pk = nullptr);
 cudaError_t prepare_eval_kernels(const TabLayout& L, int A, bool smem_gate);
 int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate);
 int generic_blocks_per_sm();
 size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate);
 cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
-                            const EvalMeta& M, const EvalArgs& a, cudaStream_t s);
+                            const EvalMeta& M, const EvalArgs& a, cudaStream_t s, const PackMeta* pk = nullptr);
 
 // Reward scan (ls_select.cu)
 size_t scan_scratch_bytes(int64_t n);

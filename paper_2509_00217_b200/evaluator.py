@@ -258,6 +258,81 @@ class Evaluator:
                                          _ptr(recs), _ptr(count), _ptr(self._scratch), self._stream()))
         return (out if verdicts else None), recs, count
 
+    # -- packed candidate words (8 B per candidate) ---------------------------
+
+    def packed_layout(self) -> tuple[tuple[int, ...], tuple[int, ...]]:
+        sh, bits = (ctypes.c_int32 * 4)(), (ctypes.c_int32 * 4)()
+        check(self._lib.ls_packed_layout(self._ctx, sh, bits))
+        return tuple(sh), tuple(bits)
+
+    def pack(self, planes: torch.Tensor) -> torch.Tensor:
+        """Device SoA planes -> packed uint64 words (as int64 storage)."""
+        n, stride = self._check_planes(planes)
+        words = torch.empty(n, dtype=torch.int64, device=self.device)
+        check(self._lib.ls_pack(self._ctx, ctypes.c_void_p(planes.data_ptr()), stride, n, _ptr(words),
+                                self._stream()))
+        return words
+
+    def _check_words(self, words: torch.Tensor) -> int:
+        if words.device != self.device:
+            raise ValueError(f"words live on {words.device}, evaluator on {self.device}")
+        if words.dtype not in (torch.int64, torch.uint64) or words.dim() != 1 or not words.is_contiguous():
+            raise ValueError("packed candidates must be a contiguous 1-D 64-bit tensor")
+        return words.shape[0]
+
+    def _alloc(self, n: int, fields) -> BatchResult:
+        out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=self.device))
+        for f in (FIELDS if fields == "all" else fields):
+            setattr(out, f, torch.empty(n, dtype=torch.float64, device=self.device))
+        return out
+
+    def evaluate_packed(self, words: torch.Tensor, fields=("throughput",), out: BatchResult | None = None) -> BatchResult:
+        """Score packed candidate words resident on the device."""
+        n = self._check_words(words)
+        if out is None:
+            out = self._alloc(n, fields)
+        soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS))
+        check(self._lib.ls_evaluate_packed(self._ctx, ctypes.c_void_p(words.data_ptr()), n, ctypes.byref(soa),
+                                           self._stream()))
+        return out
+
+    def evaluate_packed_topk(self, words: torch.Tensor, k: int = 3, index_base: int = 0,
+                             out: BatchResult | None = None, fields=("throughput",), verdicts: bool = True):
+        """Fused evaluate + top-k by raw over packed words. Returns (out, records, count)."""
+        n = self._check_words(words)
+        if verdicts and out is None:
+            out = self._alloc(n, fields)
+        soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
+        recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+        count = torch.empty(1, dtype=torch.int32, device=self.device)
+        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
+        if self._scratch is None or self._scratch.numel() < nbytes:
+            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        check(self._lib.ls_evaluate_packed_topk(self._ctx, ctypes.c_void_p(words.data_ptr()), n,
+                                                ctypes.byref(soa) if soa is not None else None, int(k),
+                                                int(index_base), _ptr(recs), _ptr(count), _ptr(self._scratch),
+                                                self._stream()))
+        return (out if verdicts else None), recs, count
+
+    def evaluate_host_packed(self, words: np.ndarray, fields=("throughput",), out: dict | None = None) -> dict:
+        """Score host-resident packed words (pinned for full PCIe speed); numpy results."""
+        arr = np.ascontiguousarray(words)
+        if arr.dtype not in (np.uint64, np.int64) or arr.ndim != 1:
+            raise ValueError("packed candidates must be a 1-D 64-bit array")
+        n = arr.shape[0]
+        if fields == "all":
+            fields = FIELDS
+        if out is None:
+            out = {"reason": np.empty(n, dtype=np.uint8)}
+            for f in fields:
+                out[f] = np.empty(n, dtype=np.float64)
+        elif any(len(v) < n for v in out.values()):
+            raise ValueError("out arrays are shorter than the batch")
+        soa = ResultSoA(ctypes.c_void_p(out["reason"].ctypes.data),
+                        *(ctypes.c_void_p(out[f].ctypes.data) if f in out else None for f in FIELDS))
+        check(self._lib.ls_evaluate_host_packed(self._ctx, ctypes.c_void_p(arr.ctypes.data), n, ctypes.byref(soa)))
+        return out
+
     # -- on-device candidate streams ----------------------------------------
 
     def stream_size(self, mode: int) -> int:

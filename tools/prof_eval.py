@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--fields", default="raw")
     ap.add_argument("--topk", type=int, default=0, help="fused evaluate + elite of this size")
     ap.add_argument("--no-verdicts", action="store_true")
+    ap.add_argument("--packed", action="store_true", help="8-byte candidate words instead of planes")
     args = ap.parse_args()
     wl = load_workload(args.config)
     ev = Evaluator(wl, device=0)
@@ -38,11 +39,18 @@ def main():
         planes[h] = torch.randint(0, k, (args.n,), generator=g, device="cuda", dtype=torch.uint8)
     fields = ("throughput",) if args.fields == "raw" else "all"
     out = ev.evaluate(planes, fields=fields)
+    words = ev.pack(planes) if args.packed else None
+    if words is not None:
+        del planes
     torch.cuda.synchronize()
     for _ in range(args.reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        if args.topk:
+        if words is not None and args.topk:
+            ev.evaluate_packed_topk(words, k=args.topk, out=out, verdicts=not args.no_verdicts)
+        elif words is not None:
+            ev.evaluate_packed(words, fields=fields, out=out)
+        elif args.topk:
             ev.evaluate_topk(planes, k=args.topk, out=out, verdicts=not args.no_verdicts)
         else:
             ev.evaluate(planes, fields=fields, out=out)
