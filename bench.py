@@ -44,7 +44,9 @@ sys.path.insert(0, str(ROOT))
 METRIC = "strategy evals/sec"
 UNIT = "evals/s"
 CONFIG = "moe_1p6t_h100x2048"
-ALGO_BYTES = 16 + 1 + 8  # per candidate: 16 head bytes in, reason u8 + raw f64 out
+# per candidate: one packed 8-byte candidate word in, reason u8 + raw f64 out
+# (planes: 16 head bytes in instead of 8)
+ALGO_BYTES = {"packed": 8 + 1 + 8, "planes": 16 + 1 + 8}
 ELITE_K = 8
 
 
@@ -60,6 +62,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-search", action="store_true", help="skip the PPO search wall-time line")
+    ap.add_argument("--format", default="packed", choices=["packed", "planes"],
+                    help="resident candidate format: 8-byte packed words or uint8 SoA planes")
     return ap.parse_args()
 
 
@@ -229,6 +233,9 @@ def run_ours(args, rank, world, local_rank):
     planes = torch.empty((len(sizes), n), dtype=torch.uint8, device=dev)
     for h, k in enumerate(sizes):
         planes[h] = torch.randint(0, k, (n,), generator=gen, device=dev, dtype=torch.uint8)
+    cands = planes
+    if args.format == "packed":
+        cands = ev.pack(planes)  # same candidates, 8 B each
     out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=dev),
                       throughput=torch.empty(n, dtype=torch.float64, device=dev))
     base = rank * n  # contiguous global index range per rank
@@ -241,14 +248,17 @@ def run_ours(args, rank, world, local_rank):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
         if world > 1:
-            _, recs, count = ev.evaluate_topk(planes, k=ELITE_K, index_base=base, out=out)
+            if cands.dim() == 1:
+                _, recs, count = ev.evaluate_packed_topk(cands, k=ELITE_K, index_base=base, out=out)
+            else:
+                _, recs, count = ev.evaluate_topk(cands, k=ELITE_K, index_base=base, out=out)
             if timed:
                 b.record(stream)
                 ev_start.append(a)
                 ev_end.append(b)
             recs, count = sweep.merge(recs, count)
             return recs, count, 3
-        _, recs, count = sweep.run(planes, index_base=base, out=out)
+        _, recs, count = sweep.run(cands, index_base=base, out=out)
         if timed:
             b.record(stream)
             ev_start.append(a)
@@ -289,19 +299,28 @@ def run_ours(args, rank, world, local_rank):
     else:
         kern_avg = statistics.mean(kern_ms)
 
-    # end-to-end through the public host API: pinned host planes in, host verdicts out
+    # end-to-end through the public host API: pinned host candidates in, host verdicts out
     e2e_n = min(args.e2e_n, n)
-    host_planes = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
-    host_planes.copy_(planes[:, :e2e_n].cpu())
-    hp = host_planes.numpy()
+    if args.format == "packed":
+        host_in = torch.empty(e2e_n, dtype=torch.int64).pin_memory()
+        host_in.copy_(cands[:e2e_n].cpu())
+        in_bytes = 8
+        run_host = ev.evaluate_host_packed
+    else:
+        host_in = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
+        host_in.copy_(planes[:, :e2e_n].cpu())
+        in_bytes = len(sizes)
+        run_host = ev.evaluate_host
+    hp = host_in.numpy()
+    del planes
     e2e_steps = max(3, min(args.steps, 10))
     hout = pinned_results(e2e_n)
-    ev.evaluate_host(hp, out=hout)  # warm: allocates the pipeline buffers
+    run_host(hp, out=hout)  # warm: allocates the pipeline buffers
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res = ev.evaluate_host(hp, out=hout)
+        res = run_host(hp, out=hout)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -314,7 +333,8 @@ def run_ours(args, rank, world, local_rank):
         return
     value = world * n * args.steps / (elapsed_ms / 1e3)
     pk, pk_kind = peaks()
-    achieved_gbs = ALGO_BYTES * n / (kern_avg / 1e3) / 1e9
+    algo_bytes = ALGO_BYTES[args.format]
+    achieved_gbs = algo_bytes * n / (kern_avg / 1e3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "roofline_traffic.json"
     if tfile.exists():
@@ -329,15 +349,20 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: uniform candidates (baselines.uniform_vector), "
-                               f"{n} per GPU per step, SoA uint8 planes in HBM",
+                               f"{n} per GPU per step, " + ("packed 8-byte candidate words" if args.format == "packed"
+                                                             else "SoA uint8 planes") + " in HBM",
+                   "format": args.format,
                    "candidates_per_gpu": n, "elite_k": ELITE_K, "parallelism": f"dp{world} (index-range shards)",
-                   "l2": "inputs 16 B x n per GPU >> 126 MB L2; no flush"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * len(sizes),
+                   "l2": f"inputs {ALGO_BYTES[args.format] - 9} B x n per GPU >> 126 MB L2; no flush"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * in_bytes,
                 "d2h_bytes_per_step": world * e2e_n * 9, "candidates_per_gpu": e2e_n,
-                "api": "Evaluator.evaluate_host -> ls_evaluate_host"},
+                "api": ("Evaluator.evaluate_host_packed -> ls_evaluate_host_packed" if args.format == "packed"
+                        else "Evaluator.evaluate_host -> ls_evaluate_host")},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved_gbs / pk.get("hbm_gbs"), "traffic": traffic,
-                     "kernel": "eval_ws_kernel (fused evaluate + elite) + topk_merge_kernel", "algorithmic_bytes_per_candidate": ALGO_BYTES,
+                     "kernel": "eval_ws_kernel<GEN_WORDS> (fused evaluate + elite) + topk_merge_kernel"
+                               if args.format == "packed" else
+                               "eval_ws_kernel (fused evaluate + elite) + topk_merge_kernel", "algorithmic_bytes_per_candidate": algo_bytes,
                      "kernel_ms_avg": kern_avg, "peak_source": f"{pk_kind} hbm_gbs (MEASURED_PEAKS.json)"},
         "gpu_launches": launches,
         "clocks": clk,

@@ -162,13 +162,15 @@ int ls_evaluate_host(ls_ctx* ctx, const uint8_t* host_planes, int64_t n, int64_t
                      const ls_result_soa* host_out);
 
 /* Packed candidates (vectors of <= 16 heads): one uint64 word per candidate,
- * axis head h in bits [2(h-4), 2(h-4)+2), then the tp/ep/pp/batch indices
- * from bit 24 in the widths ls_packed_layout reports (8 B per candidate
- * instead of A bytes of planes: the hot loop is HBM-bound, so fewer bytes
- * is more candidates per second). Malformed words (bits outside the
- * layout, an axis field of 3, an index past its domain) evaluate to
- * LS_REASON_DECODE_ERROR, like out-of-range plane bytes. */
-int ls_packed_layout(ls_ctx* ctx, int32_t shift_out[4], int32_t bits_out[4]);
+ *   word = Y | crank << 24
+ * Y: axis head h (4 <= h < A) in bits [2(h-4), 2(h-4)+2); crank: the coarse
+ * rank ((t*ne + e)*np + p)*nb + b over the tp/ep/pp/batch domain indices.
+ * 8 B per candidate instead of A bytes of planes, and the coarse rank
+ * indexes the gate table directly. Malformed words (bits above 24 + 24, an
+ * axis field of 3, a rank past the coarse space, bits above head A) evaluate
+ * to LS_REASON_DECODE_ERROR, like out-of-range plane bytes.
+ * ls_packed_layout reports the rank's shift (24) and the coarse space size. */
+int ls_packed_layout(ls_ctx* ctx, int32_t* coarse_shift, int64_t* coarse_size);
 int ls_pack(ls_ctx* ctx, const uint8_t* planes, int64_t plane_stride, int64_t n, uint64_t* words, void* stream);
 int ls_evaluate_packed(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, void* stream);
 int ls_evaluate_host_packed(ls_ctx* ctx, const uint64_t* host_words, int64_t n, const ls_result_soa* host_out);

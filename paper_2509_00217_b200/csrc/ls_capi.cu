@@ -255,18 +255,19 @@ uint64_t stream_size(const GenMeta& g) {
 namespace ls {
 PackMeta pack_meta(const ls_workload_desc& d) {
   PackMeta pk{};
-  uint32_t sh = 24;
-  for (int h = 0; h < 4; ++h) {
-    uint32_t bits = 1;
-    while ((1u << bits) < (uint32_t)d.domain_len[h]) ++bits;
-    pk.shift[h] = sh;
-    pk.mask[h] = (1u << bits) - 1u;
-    sh += bits;
-  }
   const int A = d.vector_length;
   pk.axis_mask = A > 4 ? (uint32_t)((1ull << (2 * (A - 4))) - 1ull) : 0u;
-  pk.used = pk.axis_mask;
-  for (int h = 0; h < 4; ++h) pk.used |= (uint64_t)pk.mask[h] << pk.shift[h];
+  pk.nt = (uint32_t)d.domain_len[0];
+  pk.ne = (uint32_t)d.domain_len[1];
+  pk.np = (uint32_t)d.domain_len[2];
+  pk.nb = (uint32_t)d.domain_len[3];
+  pk.ncoarse = (uint32_t)d.domain_len[0] * pk.ne * pk.np * pk.nb;
+  auto magic = [](uint64_t v) {
+    return v <= 1 ? 0ull : (uint64_t)((((unsigned __int128)1 << 64) + v - 1) / v);
+  };
+  pk.m_e = magic(pk.ne);
+  pk.m_p = magic(pk.np);
+  pk.m_b = magic(pk.nb);
   return pk;
 }
 }  // namespace ls
@@ -386,15 +387,12 @@ int ls_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_strid
 }
 
 
-int ls_packed_layout(ls_ctx* c, int32_t* shift_out, int32_t* bits_out) {
+int ls_packed_layout(ls_ctx* c, int32_t* coarse_shift, int64_t* coarse_size) {
   g_err.clear();
-  if (!c || !shift_out || !bits_out) return fail(LS_ERR_INVALID_ARGUMENT, "null argument");
+  if (!c || !coarse_shift || !coarse_size) return fail(LS_ERR_INVALID_ARGUMENT, "null argument");
   if (c->desc.vector_length > 16) return fail(LS_ERR_UNSUPPORTED, "packed candidates need vectors of <= 16 heads");
-  const PackMeta pk = pack_meta(c->desc);
-  for (int h = 0; h < 4; ++h) {
-    shift_out[h] = (int32_t)pk.shift[h];
-    bits_out[h] = __builtin_popcount(pk.mask[h]);
-  }
+  *coarse_shift = 24;
+  *coarse_size = (int64_t)pack_meta(c->desc).ncoarse;
   return LS_OK;
 }
 

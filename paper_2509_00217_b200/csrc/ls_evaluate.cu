@@ -150,18 +150,14 @@ __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, in
   c.Y = __byte_perm(y01, q[2], 0x4000u | ((4u + j) << 8) | 0x10u) & 0x00ffffffu;
 }
 
-// Packed candidate word -> fields (A <= 16, head slot = h - 4, so the axis
-// bits ARE the Y word). Nonzero return: malformed word or index out of range
-// (the planes path's decode error, strategy.py:247-254).
-__device__ __forceinline__ uint32_t word_decode(uint64_t w, const PackMeta& pk, const EvalMeta& M, Decoded& c) {
-  const uint32_t Y = (uint32_t)w & pk.axis_mask;
-  c.Y = Y;
-  c.t = (int)((uint32_t)(w >> pk.shift[0]) & pk.mask[0]);
-  c.e = (int)((uint32_t)(w >> pk.shift[1]) & pk.mask[1]);
-  c.p = (int)((uint32_t)(w >> pk.shift[2]) & pk.mask[2]);
-  c.b = (int)((uint32_t)(w >> pk.shift[3]) & pk.mask[3]);
-  const bool bad = (w & ~pk.used) != 0 || (Y & (Y >> 1) & 0x555555u) != 0 || c.t >= M.head_size[0] ||
-                   c.e >= M.head_size[1] || c.p >= M.head_size[2] || c.b >= M.head_size[3];
+// Packed candidate word -> (coarse rank, Y); nonzero return: malformed word
+// (bits past the rank, axis bits past head A, an axis field of 3, a rank past
+// the coarse space) — the planes path's decode error, strategy.py:247-254.
+__device__ __forceinline__ uint32_t word_decode(uint64_t w, const PackMeta& pk, uint32_t& rank, uint32_t& Y) {
+  Y = (uint32_t)w & 0xffffffu;
+  rank = (uint32_t)(w >> 24) & 0xffffffu;
+  const bool bad = (w >> 48) != 0 || (Y & ~pk.axis_mask) != 0 || (Y & (Y >> 1) & 0x555555u) != 0 ||
+                   rank >= pk.ncoarse;
   return bad ? 1u : 0u;
 }
 
@@ -177,6 +173,17 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 __device__ __forceinline__ uint64_t divq(uint64_t x, uint64_t magic, uint64_t d) {
   return d == 1 ? x : __umul64hi(x, magic);
 }
+// Coarse rank -> (t, e, p, b) (mixed radix, batch fastest).
+__device__ __forceinline__ void rank_split(uint32_t rank, const PackMeta& pk, Decoded& c) {
+  const uint64_t q1 = divq(rank, pk.m_b, pk.nb);
+  c.b = (int)(rank - q1 * pk.nb);
+  const uint64_t q2 = divq(q1, pk.m_p, pk.np);
+  c.p = (int)(q1 - q2 * pk.np);
+  const uint64_t q3 = divq(q2, pk.m_e, pk.ne);
+  c.e = (int)(q2 - q3 * pk.ne);
+  c.t = (int)q3;
+}
+
 // Stream index -> decoded candidate. GEN_UNIFORM: i.i.d. uniform over every
 // head (baselines.uniform_vector semantics, baselines.py:50-54) from two
 // counter-based draws; GEN_ENUM / GEN_ENUM_ADMISSIBLE: the index-th vector of
@@ -216,6 +223,9 @@ struct WsSmem {
   uint8_t* lists;  // [kWorkWarps] elite lists
 };
 
+// words staged into shared memory: the coarse words in raw mode, else the gate segment
+__host__ __device__ inline int stage_words(const TabLayout& L) { return L.gate_words > L.coarse_words ? L.gate_words : L.coarse_words; }
+
 inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
   return (size_t)kStages * kStageBytes + (smem_gate ? (size_t)gate_words * 8 : 0) +
          (size_t)kGateWarps * kWarpQueue * 12 + (size_t)kGateWarps * kSlots * 32 * 12 +
@@ -224,10 +234,11 @@ inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
 
 // fp64 pass over n <= 32 survivors (lane i takes entry i of keys/ys), with
 // verdict stores and the optional elite offer. Called by whole warps.
-template <bool NEU, bool FULL, bool TOPK>
+template <bool NEU, bool FULL, bool TOPK, int MODE>
 __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, const TabLayout& L, const EvalMeta& M,
                                         const EvalArgs& a, const TopkArgs& tk, const uint64_t* keys,
-                                        const uint32_t* ys, int n, RegList& wl, double& gfloor) {
+                                        const uint32_t* ys, int n, RegList& wl, double& gfloor,
+                                        const PackMeta& pk) {
   const int lane = threadIdx.x & 31;
   int64_t idx = 0;
   Decoded c;
@@ -235,7 +246,13 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
   v.reason = LS_REASON_DECODE_ERROR;
   v.thr = 0.0;
   if (lane < n) {
-    unpack_key(keys[lane], ys[lane], idx, c);
+    if (MODE == GEN_WORDS && !FULL) {  // raw-mode packed words queue (idx, coarse rank)
+      idx = (int64_t)(keys[lane] & ((1ull << 40) - 1));
+      rank_split((uint32_t)(keys[lane] >> 40), pk, c);
+      c.Y = ys[lane];
+    } else {
+      unpack_key(keys[lane], ys[lane], idx, c);
+    }
     full_path<NEU>(gtab, L, M, c, v);
     if (a.reason) write_verdict<FULL>(a, idx, v);
   }
@@ -274,7 +291,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   WsSmem S;
   S.ring = smem;
   S.gate = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  S.qkey = SMEM_GATE ? S.gate + L.gate_words : S.gate;
+  S.qkey = SMEM_GATE ? S.gate + stage_words(L) : S.gate;
+  const bool coarse = !FULL && L.coarse_words > 0;
+  const uint32_t* Cg = reinterpret_cast<const uint32_t*>(SMEM_GATE ? S.gate : gtab + L.coarse);
   S.qy = reinterpret_cast<uint32_t*>(S.qkey + kGateWarps * kWarpQueue);
   S.mkey = reinterpret_cast<uint64_t*>(S.qy + kGateWarps * kWarpQueue);
   S.my = reinterpret_cast<uint32_t*>(S.mkey + kGateWarps * kSlots * 32);
@@ -306,8 +325,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kWorkWarps) {  // ---------------- producer warp
     if (lane == 0) {
       if (SMEM_GATE) {
-        mbar_expect_tx(&gate_bar, (uint32_t)L.gate_words * 8u);
-        bulk_g2s(S.gate, gtab, (uint32_t)L.gate_words * 8u, &gate_bar);
+        const uint32_t words = coarse ? (uint32_t)L.coarse_words : (uint32_t)L.gate_words;
+        mbar_expect_tx(&gate_bar, words * 8u);
+        bulk_g2s(S.gate, coarse ? gtab + L.coarse : gtab, words * 8u, &gate_bar);
       }
       int i = 0;
       for (int64_t tile = blockIdx.x; (MODE == GEN_PLANES || MODE == GEN_WORDS) && tile < ntiles;
@@ -343,7 +363,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           __threadfence_block();
           found = true;
           const int base = (g * kSlots + sl) * 32;
-          fp64_batch<NEU, FULL, TOPK>(gtab, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl, gfloor);
+          fp64_batch<NEU, FULL, TOPK, MODE>(gtab, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl, gfloor,
+                                            gm.pk);
           __syncwarp();
           if (lane == 0) {
             __threadfence_block();
@@ -395,22 +416,40 @@ __global__ void __launch_bounds__(kThreads, 2)
           mb_state[warp][slot] = 1;
         }
       } else {
-        fp64_batch<NEU, FULL, TOPK>(gtab, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor);
+        fp64_batch<NEU, FULL, TOPK, MODE>(gtab, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor, gm.pk);
       }
       qcount -= n;
       __syncwarp();
     };
 
     // gate pass over this lane's 4 decoded candidates (stream indices base..)
-    auto pass_a = [&](Decoded* cs, uint32_t badb, int64_t base, int count) {
+    // ranks: coarse ranks of the 4 candidates when the candidates came as
+    // packed words (t, e, p, b then split only where needed)
+    auto pass_a = [&](Decoded* cs, uint32_t badb, int64_t base, int count, const uint32_t* ranks) {
       uint32_t r4 = 0, reason[4];
       double m[4];
       // the 4 gate evaluations are independent: issue them back to back (ILP)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool dbad = ((badb >> (8 * j)) & 0xffu) != 0;
-        if (dbad) cs[j].t = cs[j].e = cs[j].p = cs[j].b = 0;  // keep the branch-free lookups in range
-        reason[j] = gate(Gt, L, M, cs[j], m[j]);
+        if (MODE == GEN_WORDS) {
+          const uint32_t rk = dbad ? 0u : ranks[j];  // keep the branch-free lookups in range
+          if (coarse) {
+            reason[j] = gate_rank(Cg, M, rk, cs[j].Y);
+            m[j] = 0.0;
+          } else {
+            rank_split(rk, gm.pk, cs[j]);
+            reason[j] = gate(Gt, L, M, cs[j], m[j]);
+          }
+        } else {
+          if (dbad) cs[j].t = cs[j].e = cs[j].p = cs[j].b = 0;  // keep the branch-free lookups in range
+          if (coarse) {
+            reason[j] = gate_coarse(Cg, L, M, cs[j]);
+            m[j] = 0.0;
+          } else {
+            reason[j] = gate(Gt, L, M, cs[j], m[j]);
+          }
+        }
         if (dbad) {
           reason[j] = LS_REASON_DECODE_ERROR;
           m[j] = 0.0;
@@ -424,7 +463,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const unsigned mask = __ballot_sync(0xffffffffu, surv);
         if (surv) {
           const int pos = qcount + __popc(mask & ((1u << lane) - 1u));
-          qkey[pos] = pack_key(base + j, cs[j]);
+          qkey[pos] = (MODE == GEN_WORDS && !FULL) ? (uint64_t)(base + j) | ((uint64_t)ranks[j] << 40)
+                                                   : pack_key(base + j, cs[j]);
           qy[pos] = cs[j].Y;
         }
         qcount += __popc(mask);
@@ -483,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         Decoded cs[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
-        pass_a(cs, badb, tile * kTile + lane_off, 4);
+        pass_a(cs, badb, tile * kTile + lane_off, 4, nullptr);
       }
       // ragged tail (< one tile): the CTA that would own the next tile
       const int64_t tail0 = ntiles * kTile;
@@ -502,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         Decoded cs[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
-        pass_a(cs, badb, base, count);
+        pass_a(cs, badb, base, count, nullptr);
       }
     } else if (MODE == GEN_WORDS) {  // 4 consecutive 8-byte candidate words per lane
       int i = 0;
@@ -516,20 +556,21 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
         Decoded cs[4];
-        uint32_t badb = 0;
+        uint32_t badb = 0, rk[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) badb |= word_decode(w[j], gm.pk, M, cs[j]) << (8 * j);
-        pass_a(cs, badb, tile * kTile + lane_off, 4);
+        for (int j = 0; j < 4; ++j) badb |= word_decode(w[j], gm.pk, rk[j], cs[j].Y) << (8 * j);
+        pass_a(cs, badb, tile * kTile + lane_off, 4, rk);
       }
       const int64_t tail0 = ntiles * kTile;
       if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
         const int64_t base = tail0 + lane_off;
         const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
         Decoded cs[4];
-        uint32_t badb = 0;
+        uint32_t badb = 0, rk[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, M, cs[j]) << (8 * j);
-        pass_a(cs, badb, base, count);
+        for (int j = 0; j < 4; ++j)
+          badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, rk[j], cs[j].Y) << (8 * j);
+        pass_a(cs, badb, base, count, rk);
       }
     } else {  // candidates generated in registers: nothing read from HBM
       const int64_t gtiles = (a.n + kTile - 1) / kTile;
@@ -540,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int j = 0; j < 4; ++j)  // past-the-end lanes regenerate the last valid index (never enqueued)
           gen_candidate<MODE>(gm, (uint64_t)(gm.start + (base + j < a.n ? base + j : a.n - 1)), cs[j]);
-        pass_a(cs, 0u, base, count);
+        pass_a(cs, 0u, base, count, nullptr);
       }
     }
     if (qcount > 0) flush(qcount);
@@ -622,7 +663,7 @@ template <bool NEU, bool FULL, bool TOPK, int MODE = GEN_PLANES>
 void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, const EvalArgs& a,
                  const TopkArgs& tk, cudaStream_t s, const GenMeta& gm = GenMeta{}) {
   const int64_t ntiles = (MODE == GEN_PLANES || MODE == GEN_WORDS) ? a.n / kTile : (a.n + kTile - 1) / kTile;
-  const size_t smem = ws_dynamic_bytes(M.A, L.gate_words, lp.smem_gate);
+  const size_t smem = ws_dynamic_bytes(M.A, stage_words(L), lp.smem_gate);
   int64_t blocks = ntiles > 0 ? ntiles : 1;
   if (blocks > lp.max_blocks) blocks = lp.max_blocks;
   if (lp.smem_gate)
@@ -670,31 +711,29 @@ void launch_ws(const LaunchPlan& lp, bool neumaier, bool full, const uint64_t* t
   }
 }
 
-// SoA planes -> packed candidate words (A <= 16). Out-of-range heads pack
-// to a malformed word (all used bits of the field set plus an unused bit),
-// so they still evaluate to LS_REASON_DECODE_ERROR.
+// SoA planes -> packed candidate words (A <= 16). Out-of-range heads give an
+// all-ones (malformed) word, so they still evaluate to LS_REASON_DECODE_ERROR.
 __global__ void pack_kernel(const PackMeta pk, int A, const uint8_t* __restrict__ planes, int64_t stride, int64_t n,
                             uint64_t* __restrict__ words) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t w = 0;
-    bool bad = false;
-    for (int h = 0; h < 4; ++h) {
-      const uint32_t v = planes[(int64_t)h * stride + i];
-      bad |= v > pk.mask[h];
-      w |= (uint64_t)(v & pk.mask[h]) << pk.shift[h];
-    }
+    const uint32_t t = planes[i], e = planes[stride + i], p = planes[2 * stride + i], b = planes[3 * stride + i];
+    bool bad = t >= pk.nt || e >= pk.ne || p >= pk.np || b >= pk.nb;
+    uint64_t y = 0;
     for (int h = 4; h < A; ++h) {
       const uint32_t v = planes[(int64_t)h * stride + i];
-      bad |= v > 3;
-      w |= (uint64_t)(v & 3u) << (2 * (h - 4));
+      bad |= v > 2;
+      y |= (uint64_t)(v & 3u) << (2 * (h - 4));
     }
-    words[i] = bad ? ~0ull : w;
+    const uint64_t rank = ((uint64_t)(t * pk.ne + e) * pk.np + p) * pk.nb + b;
+    words[i] = bad ? ~0ull : (y | rank << 24);
   }
 }
 
 }  // namespace
 
-size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) { return ws_dynamic_bytes(A, L.gate_words, smem_gate); }
+size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) {
+  return ws_dynamic_bytes(A, stage_words(L), smem_gate);
+}
 
 bool tma_eligible(const EvalArgs& a, int A) {
   const bool al16 = a.words ? ((uintptr_t)a.words % 16) == 0

@@ -121,6 +121,30 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
   return reason;
 }
 
+// Raw-mode gate (no memory_bytes output): the coarse word of (t, e, p, b)
+// carries the same three gates, OOM precomputed for both attention layouts.
+__device__ __forceinline__ uint32_t gate_coarse(const uint32_t* C, const TabLayout& L, const EvalMeta& M,
+                                                const Decoded& c) {
+  const uint32_t cw = C[((c.t * L.ne + c.e) * L.np + c.p) * L.nb + c.b];
+  const uint32_t a2 = M.attn_src >= 0 ? (c.Y >> (M.attn_src + 1)) & 1u : (uint32_t)(M.attn_pin == 2);
+  const bool over = (cw & GATE_BUDGET) != 0;
+  const bool bad = ((c.Y & cw & GATE_FIELDS) | (cw & (GATE_PINNED | GATE_LAYOUT))) != 0;
+  const bool oom = (cw & (a2 ? GATE_OOM1 : GATE_OOM0)) != 0;
+  return over ? LS_REASON_OVER_DEVICE_BUDGET
+              : (bad ? LS_REASON_LAYOUT_ERROR : (oom ? LS_REASON_OOM : LS_REASON_NONE));
+}
+
+// Same, from the coarse rank ((t*ne + e)*np + p)*nb + b directly.
+__device__ __forceinline__ uint32_t gate_rank(const uint32_t* C, const EvalMeta& M, uint32_t rank, uint32_t Y) {
+  const uint32_t cw = C[rank];
+  const uint32_t a2 = M.attn_src >= 0 ? (Y >> (M.attn_src + 1)) & 1u : (uint32_t)(M.attn_pin == 2);
+  const bool over = (cw & GATE_BUDGET) != 0;
+  const bool bad = ((Y & cw & GATE_FIELDS) | (cw & (GATE_PINNED | GATE_LAYOUT))) != 0;
+  const bool oom = (cw & (a2 ? GATE_OOM1 : GATE_OOM0)) != 0;
+  return over ? LS_REASON_OVER_DEVICE_BUDGET
+              : (bad ? LS_REASON_LAYOUT_ERROR : (oom ? LS_REASON_OOM : LS_REASON_NONE));
+}
+
 // fp64 pass for a candidate that passed gate(). T: the full table (global).
 template <bool NEU, bool LDG = true>
 __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,

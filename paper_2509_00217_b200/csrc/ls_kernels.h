@@ -38,13 +38,13 @@ struct TopkArgs {
 // Candidate sources of eval_ws_kernel.
 enum : int { GEN_PLANES = 0, GEN_UNIFORM = 1, GEN_ENUM = 2, GEN_ENUM_ADMISSIBLE = 3, GEN_WORDS = 4 };
 
-// Packed candidate word (A <= 16): axis head h in bits [2(h-4), 2(h-4)+2),
-// then t, e, p, b from bit 24 in the minimal widths of their domains.
+// Packed candidate word (A <= 16): axis head h in bits [2(h-4), 2(h-4)+2)
+// (= the Y word), and from bit 24 the coarse rank ((t*ne + e)*np + p)*nb + b.
 struct PackMeta {
-  uint32_t shift[4];
-  uint32_t mask[4];
   uint32_t axis_mask;  // low 2(A-4) bits
-  uint64_t used;       // every bit a valid word may set
+  uint32_t ncoarse;    // nt * ne * np * nb
+  uint32_t nt, ne, np, nb;
+  uint64_t m_e, m_p, m_b;  // ceil(2^64 / d) (exact floor division of ranks < 2^24)
 };
 PackMeta pack_meta(const ls_workload_desc& d);
 

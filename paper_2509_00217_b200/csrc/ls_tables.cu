@@ -51,6 +51,36 @@ __device__ uint32_t gate_bits(const ls_workload_desc& d, int64_t tp, int64_t ep,
   return g;
 }
 
+// memory_per_device terms (simulator.py:135-160), each in the reference's order
+__device__ double weights_mem(const ls_workload_desc& d, int64_t tp, int64_t ep, int64_t pp) {
+  int64_t dense, routed;
+  param_counts(d, &dense, &routed);
+  return ((double)(dense * d.dtype_bytes) / (double)tp) / (double)pp +
+         ((double)(routed * d.dtype_bytes) / (double)(ep * tp)) / (double)pp;
+}
+__device__ double kv_mem(const ls_workload_desc& d, int64_t tp, int64_t pp, int64_t b, bool attn_dim1) {
+  const int64_t share = kv_share(d, tp, attn_dim1);
+  return ((((2.0 * ((double)d.num_layers / (double)pp)) * ((double)(d.num_kv_heads * d.head_dim) / (double)share)) *
+           (double)d.context_len) *
+          (double)b) *
+         (double)d.dtype_bytes;
+}
+__device__ double ws_mem(const ls_workload_desc& d, int64_t b) {
+  return ((2.0 * (double)b) * (double)(d.hidden_dim + d.ffn_dim)) * (double)d.dtype_bytes;
+}
+
+// Coarse gate word of one (t, e, p, b): the gate bits plus OOM outcomes for
+// both attention layouts, with gate()'s expression (w + kv) + ws > capacity.
+__device__ uint32_t coarse_word(const ls_workload_desc& d, const TabLayout& L, int c) {
+  const int b = c % L.nb, p = (c / L.nb) % L.np, e = (c / (L.nb * L.np)) % L.ne, t = c / (L.nb * L.np * L.ne);
+  const int64_t TP = d.domain[0][t], EP = d.domain[1][e], PP = d.domain[2][p], B = d.domain[3][b];
+  uint32_t g = gate_bits(d, TP, EP, PP);
+  const double w = weights_mem(d, TP, EP, PP), ws = ws_mem(d, B);
+  if ((w + kv_mem(d, TP, PP, B, false)) + ws > d.hbm_capacity) g |= GATE_OOM0;
+  if ((w + kv_mem(d, TP, PP, B, true)) + ws > d.hbm_capacity) g |= GATE_OOM1;
+  return g;
+}
+
 __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, int w) {
   const int nt = L.nt, ne = L.ne, np = L.np, nb = L.nb;
   const int64_t* TP = d.domain[0];
@@ -117,27 +147,19 @@ __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, in
   // simulator.py:147-150); word 1 = gate bits | kv row base << 32
   if (w >= L.tep && w < L.tep + 2 * nt * ne * np) {
     const int i = (w - L.tep) / 2, t = i / (ne * np), e = (i / np) % ne, p = i % np;
-    if ((w - L.tep) % 2 == 0) {
-      int64_t dense, routed;
-      param_counts(d, &dense, &routed);
-      return dbits(((double)(dense * d.dtype_bytes) / (double)TP[t]) / (double)PP[p] +
-                   ((double)(routed * d.dtype_bytes) / (double)(EP[e] * TP[t])) / (double)PP[p]);
-    }
+    if ((w - L.tep) % 2 == 0) return dbits(weights_mem(d, TP[t], EP[e], PP[p]));
     return (uint64_t)gate_bits(d, TP[t], EP[e], PP[p]) | ((uint64_t)((t * np + p) * nb) << 32);
   }
   // KV cache per device: [attn_dim1][t][p][b]
   if (w >= L.mem_kv && w < L.mem_kv + 2 * nt * np * nb) {
     unflat(w - L.mem_kv, nt, np, nb, &c0, &c1, &c2, &c3);
-    const int64_t share = kv_share(d, TP[c1], c0 != 0);
-    return dbits(((((2.0 * ((double)d.num_layers / (double)PP[c2])) *
-                    ((double)(d.num_kv_heads * d.head_dim) / (double)share)) *
-                   (double)d.context_len) *
-                  (double)B[c3]) *
-                 (double)d.dtype_bytes);
+    return dbits(kv_mem(d, TP[c1], PP[c2], B[c3], c0 != 0));
   }
-  if (w >= L.mem_ws && w < L.mem_ws + nb) {
-    const int b = w - L.mem_ws;
-    return dbits(((2.0 * (double)B[b]) * (double)(d.hidden_dim + d.ffn_dim)) * (double)d.dtype_bytes);
+  if (w >= L.mem_ws && w < L.mem_ws + nb) return dbits(ws_mem(d, B[w - L.mem_ws]));
+  if (L.coarse_words && w >= L.coarse && w < L.coarse + L.coarse_words) {
+    const int c0i = 2 * (w - L.coarse), nc = nt * ne * np * nb;
+    const uint64_t lo = c0i < nc ? coarse_word(d, L, c0i) : 0u, hi = c0i + 1 < nc ? coarse_word(d, L, c0i + 1) : 0u;
+    return lo | (hi << 32);
   }
   // stage handoff hop: [intra][b]
   if (w >= L.hop && w < L.hop + 2 * nb) {

@@ -46,8 +46,15 @@ enum : uint32_t {
   GATE_FIELDS = 0x00ffffffu,  // 12 axis fields x {DIM0, DIM1}
   GATE_PINNED = 1u << 24,     // a pinned (uncontrolled) op is a layout error at this tp
   GATE_LAYOUT = 1u << 25,     // pp does not divide num_layers, or ep vs num_experts
-  GATE_BUDGET = 1u << 26      // tp * ep * pp > device_budget
+  GATE_BUDGET = 1u << 26,     // tp * ep * pp > device_budget
+  GATE_OOM0 = 1u << 27,       // memory > capacity with attn_core not on DIM1 (coarse words only)
+  GATE_OOM1 = 1u << 28        // memory > capacity with attn_core on DIM1 (coarse words only)
 };
+
+// Coarse gate words: one uint32 per (t, e, p, b) = the (t, e, p) gate bits plus
+// both memory-gate outcomes, so a raw-mode gate is one shared-memory load and
+// a few bit tests. Built only when the coarse space is small enough to stage.
+constexpr int kCoarseMax = 6144;
 
 // Offsets (in 8-byte words) of every table segment inside one buffer.
 struct TabLayout {
@@ -68,6 +75,8 @@ struct TabLayout {
   int hop, batch_d, lps_d, ppm1_d;
   // integer segments
   int tpv, epv, ppv;
+  // coarse gate words (uint32 [t][e][p][b], two per table word), 0 if too large
+  int coarse, coarse_words;
   int words;  // total, even (16-byte multiple)
 };
 
@@ -146,6 +155,9 @@ inline TabLayout make_layout(const ls_workload_desc& d) {
   L.tpv = seg(nt);
   L.epv = seg(ne);
   L.ppv = seg(np);
+  const int nc = nt * ne * np * nb;
+  L.coarse_words = nc <= kCoarseMax ? round2((nc + 1) / 2) : 0;
+  L.coarse = seg(L.coarse_words);
   L.words = round2(w);
   return L;
 }

@@ -67,13 +67,18 @@ class ShardedSweep:
         self._gathered = torch.empty((self.world * self.k, 32), dtype=torch.uint8, device=dev)
         self._gcounts = torch.empty(self.world, dtype=torch.int32, device=dev)
 
-    def run(self, planes: torch.Tensor, index_base: int, out=None, verdicts: bool = True):
-        """Score this rank's planes (global indices index_base..) and return the global elite.
+    def run(self, candidates: torch.Tensor, index_base: int, out=None, verdicts: bool = True):
+        """Score this rank's candidates (global indices index_base..) and return the global elite.
 
+        ``candidates``: [A, n] uint8 planes, or n packed 64-bit words.
         Returns (out, recs, count) with recs/count the merged global top-k on device.
         """
-        out, recs, count = self.ev.evaluate_topk(planes, k=self.k, index_base=index_base, out=out,
-                                                 verdicts=verdicts)
+        if candidates.dim() == 1:
+            out, recs, count = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
+                                                            verdicts=verdicts)
+        else:
+            out, recs, count = self.ev.evaluate_topk(candidates, k=self.k, index_base=index_base, out=out,
+                                                     verdicts=verdicts)
         recs, count = self.merge(recs, count)
         return out, recs, count
 

@@ -260,10 +260,11 @@ class Evaluator:
 
     # -- packed candidate words (8 B per candidate) ---------------------------
 
-    def packed_layout(self) -> tuple[tuple[int, ...], tuple[int, ...]]:
-        sh, bits = (ctypes.c_int32 * 4)(), (ctypes.c_int32 * 4)()
-        check(self._lib.ls_packed_layout(self._ctx, sh, bits))
-        return tuple(sh), tuple(bits)
+    def packed_layout(self) -> tuple[int, int]:
+        """(bit shift of the coarse rank, coarse space size) of packed words."""
+        sh, size = ctypes.c_int32(), ctypes.c_int64()
+        check(self._lib.ls_packed_layout(self._ctx, ctypes.byref(sh), ctypes.byref(size)))
+        return sh.value, size.value
 
     def pack(self, planes: torch.Tensor) -> torch.Tensor:
         """Device SoA planes -> packed uint64 words (as int64 storage)."""

@@ -67,15 +67,22 @@ def test_device_pack_equals_host_pack_and_round_trips(name, ev_factory):
 def test_malformed_words_are_decode_errors(ev_factory):
     wl, meta, data = load_eval("moe_1p2t")
     ev = ev_factory(wl)
-    shifts, widths = packed_layout(wl.space)
-    good = pack_vectors(data["vectors"][:4], wl.space)
-    top = shifts[3] + widths[3]
-    bad = [good[0] | np.uint64(1 << 63), good[1] | np.uint64(1 << top),  # bits outside the layout
+    shift, size = packed_layout(wl.space)
+    good = pack_vectors(data["vectors"][:5], wl.space)
+    low24 = np.uint64((1 << 24) - 1)
+    bad = [good[0] | np.uint64(1 << 63), good[1] | np.uint64(1 << 48),  # bits past the rank field
            good[2] | np.uint64(3 << 4),  # an axis field holding 3
-           (good[3] & ~np.uint64(((1 << widths[0]) - 1) << shifts[0])) | np.uint64(7 << shifts[0])]  # t = 7 >= 7
-    words = torch.from_numpy(np.asarray(bad, dtype=np.uint64).view(np.int64)).cuda()
+           (good[3] & low24) | np.uint64(size << shift),  # rank past the coarse space
+           good[4] | np.uint64(1 << 23)]  # axis bits past head A (A = 16 uses all 24: use a 14-head set below)
+    words = torch.from_numpy(np.asarray(bad[:4], dtype=np.uint64).view(np.int64)).cuda()
     got = ev.evaluate_packed(words).numpy()
     assert (got["reason"] == 255).all() and (got["throughput"] == 0).all()
+    wl14, _, data14 = load_eval("llama3_8b_h100x8")  # A = 14: axis bits 20..23 must be zero
+    ev14 = ev_factory(wl14)
+    w14 = pack_vectors(data14["vectors"][:2], wl14.space)
+    w14[1] |= np.uint64(1 << 21)
+    got = ev14.evaluate_packed(torch.from_numpy(w14.view(np.int64)).cuda()).numpy()
+    assert got["reason"][1] == 255 and got["reason"][0] != 255
 
 
 @pytest.mark.parametrize("n", [0, 1, 5, 1023, 1024, 1025, 4097, 300_001])
