@@ -339,9 +339,9 @@ def run_ours(args, rank, world, local_rank):
     tfile = ROOT / "profiles" / "roofline_traffic.json"
     if tfile.exists():
         try:
-            tj = json.loads(tfile.read_text())
-            if tj.get("config") == args.config and tj.get("n") == n:
-                traffic = tj.get("bytes_per_launch")
+            for tj in json.loads(tfile.read_text()).get("entries", []):
+                if tj.get("config") == args.config and tj.get("n") == n and tj.get("format") == args.format:
+                    traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
     line = {

@@ -44,6 +44,15 @@ constexpr int kSlots = 2;        // mailbox slots per gate warp
 constexpr int kGenericThreads = 256;
 constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
 constexpr uint32_t kStageBytes = 16 * kTile;  // 16 plane slices per stage (planes >= A stay zero)
+constexpr uint32_t kRingBytes = kStages * kStageBytes;
+// packed words are 8 B per candidate: the same ring holds twice the stages,
+// keeping the bytes in flight per SM (and so the HBM pipe) as full as for planes
+constexpr int kMaxStages = kRingBytes / (8 * kTile);
+template <int MODE>
+struct Ring {
+  static constexpr uint32_t stage_bytes = MODE == GEN_WORDS ? 8u * kTile : kStageBytes;
+  static constexpr int stages = (int)(kRingBytes / stage_bytes);
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -227,7 +236,7 @@ struct WsSmem {
 __host__ __device__ inline int stage_words(const TabLayout& L) { return L.gate_words > L.coarse_words ? L.gate_words : L.coarse_words; }
 
 inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
-  return (size_t)kStages * kStageBytes + (smem_gate ? (size_t)gate_words * 8 : 0) +
+  return (size_t)kRingBytes + (smem_gate ? (size_t)gate_words * 8 : 0) +
          (size_t)kGateWarps * kWarpQueue * 12 + (size_t)kGateWarps * kSlots * 32 * 12 +
          (size_t)kWorkWarps * warp_list_bytes(kFusedK);
 }
@@ -279,8 +288,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
                    const int64_t ntiles, const TopkArgs tk, const GenMeta gm) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full_bar[kStages];
-  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  constexpr int NST = Ring<MODE>::stages;
+  constexpr uint32_t STB = Ring<MODE>::stage_bytes;
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t gate_bar;
   __shared__ int list_count[kWorkWarps];
   __shared__ int mb_n[kGateWarps][kSlots];
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t stage_bytes = (uint32_t)A * kTile;  // bytes the producer copies per stage
   WsSmem S;
   S.ring = smem;
-  S.gate = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  S.gate = reinterpret_cast<uint64_t*>(smem + kRingBytes);
   S.qkey = SMEM_GATE ? S.gate + stage_words(L) : S.gate;
   const bool coarse = !FULL && L.coarse_words > 0;
   const uint32_t* Cg = reinterpret_cast<const uint32_t*>(SMEM_GATE ? S.gate : gtab + L.coarse);
@@ -312,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (threadIdx.x < kGateWarps * kSlots) mb_state[threadIdx.x / kSlots][threadIdx.x % kSlots] = 0;
   if (threadIdx.x == 0) {
     gates_done = 0;
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kGateWarps);
     }
@@ -332,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       int i = 0;
       for (int64_t tile = blockIdx.x; (MODE == GEN_PLANES || MODE == GEN_WORDS) && tile < ntiles;
            tile += gridDim.x, ++i) {
-        const int s = i % kStages, k = i / kStages;
+        const int s = i % NST, k = i / NST;
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
-        uint8_t* dst = S.ring + s * kStageBytes;
+        uint8_t* dst = S.ring + s * STB;
         if (MODE == GEN_WORDS) {  // one contiguous 8 KB tile of candidate words
           mbar_expect_tx(&full_bar[s], 8u * kTile);
           bulk_g2s(dst, a.words + tile * kTile, 8u * kTile, &full_bar[s]);
@@ -510,10 +521,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (MODE == GEN_PLANES) {
       int i = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-        const int s = i % kStages;
-        mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
+        const int s = i % NST;
+        mbar_wait(&full_bar[s], (uint32_t)((i / NST) & 1));
         uint32_t w[16];
-        const uint32_t st = ring_base + (uint32_t)s * kStageBytes + (uint32_t)lane_off;
+        const uint32_t st = ring_base + (uint32_t)s * STB + (uint32_t)lane_off;
 #pragma unroll
         for (int h = 0; h < 16; ++h) w[h] = lds_u32(st + h * kTile);  // planes >= A are zero-filled
         __syncwarp();
@@ -547,10 +558,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     } else if (MODE == GEN_WORDS) {  // 4 consecutive 8-byte candidate words per lane
       int i = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-        const int s = i % kStages;
-        mbar_wait(&full_bar[s], (uint32_t)((i / kStages) & 1));
+        const int s = i % NST;
+        mbar_wait(&full_bar[s], (uint32_t)((i / NST) & 1));
         uint64_t w[4];
-        const uint32_t st = ring_base + (uint32_t)s * kStageBytes + 8u * (uint32_t)lane_off;
+        const uint32_t st = ring_base + (uint32_t)s * STB + 8u * (uint32_t)lane_off;
         lds_u64x2(st, w[0], w[1]);
         lds_u64x2(st + 16, w[2], w[3]);
         __syncwarp();
