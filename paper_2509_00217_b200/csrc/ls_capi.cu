@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -52,7 +53,13 @@ struct DeviceGuard {
   }
 };
 
-constexpr int kHostChunk = 1 << 22;  // candidates per pipelined host chunk
+// Host pipeline: chunks of 2^kHostChunkLog2 candidates, up to kPipe in flight on
+// their own streams, so the H2D of later chunks overlaps the D2H of earlier
+// ones (two copy engines). LS_HOST_CHUNK_LOG2 / LS_HOST_PIPE override the
+// defaults (tuning knobs, read at context creation).
+constexpr int kHostChunkLog2 = 22;
+constexpr int kPipe = 8;  // capacity; the depth in use is ls_ctx::pipe
+constexpr int kPipeDefault = 2;
 
 }  // namespace
 
@@ -74,10 +81,12 @@ struct ls_ctx {
   uint32_t* gen_tabs[4] = {};
   // host pipeline
   std::mutex host_mu;
-  cudaStream_t hs[2] = {nullptr, nullptr};
-  uint8_t* h_planes[2] = {nullptr, nullptr};
-  uint8_t* h_reason[2] = {nullptr, nullptr};
-  double* h_f[2][6] = {};
+  int64_t host_chunk = int64_t(1) << kHostChunkLog2;
+  int pipe = kPipeDefault;
+  cudaStream_t hs[kPipe] = {};
+  uint8_t* h_planes[kPipe] = {};
+  uint8_t* h_reason[kPipe] = {};
+  double* h_f[kPipe][6] = {};
 };
 
 namespace {
@@ -158,6 +167,8 @@ void build_meta(ls_ctx* c) {
   }
   M.attn_src = M.op_src[LS_OP_ATTN_CORE];
   M.attn_pin = M.op_pin[LS_OP_ATTN_CORE];
+  M.attn_shift = M.attn_src >= 0 ? M.attn_src + 1 : 31;
+  M.attn_or = M.attn_src >= 0 ? 0u : (M.attn_pin == 2 ? 0x80000000u : 0u);
   M.node_size = d.node_size;
   M.num_layers_d = (double)d.num_layers;
   M.slo_tpot = d.slo_tpot;
@@ -322,6 +333,14 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
     delete c;
     return cuda_fail(e, "kernel setup");
   }
+  if (const char* v = getenv("LS_HOST_CHUNK_LOG2")) {
+    const int l = atoi(v);
+    if (l >= 16 && l <= 26) c->host_chunk = int64_t(1) << l;
+  }
+  if (const char* v = getenv("LS_HOST_PIPE")) {
+    const int p = atoi(v);
+    if (p >= 2 && p <= kPipe) c->pipe = p;
+  }
   *out = c;
   return LS_OK;
 }
@@ -329,7 +348,7 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
 int ls_ctx_destroy(ls_ctx* c) {
   if (!c) return LS_OK;
   DeviceGuard g(c->device);
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < kPipe; ++s) {
     if (c->hs[s]) cudaStreamDestroy(c->hs[s]);
     cudaFree(c->h_planes[s]);
     cudaFree(c->h_reason[s]);
@@ -437,7 +456,7 @@ int ls_evaluate_host(ls_ctx* c, const uint8_t* host_planes, int64_t n, int64_t p
   return host_pipeline(c, host_planes, plane_stride, nullptr, n, host_out);
 }
 
-// Chunked H2D -> evaluate -> D2H, double-buffered over two streams.
+// Chunked H2D -> evaluate -> D2H, kPipe chunks in flight on kPipe streams.
 static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_stride, const uint64_t* host_words,
                          int64_t n, const ls_result_soa* host_out) {
   std::lock_guard<std::mutex> lock(c->host_mu);
@@ -446,22 +465,23 @@ static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_st
   double* hf[6] = {host_out->throughput, host_out->tpot_s, host_out->memory_bytes,
                    host_out->compute_s,  host_out->comm_s, host_out->pipeline_s};
   cudaError_t e;
-  for (int s = 0; s < 2; ++s) {
+  const int64_t chunk_n = c->host_chunk;
+  for (int s = 0; s < c->pipe; ++s) {
     if (!c->hs[s] && (e = cudaStreamCreateWithFlags(&c->hs[s], cudaStreamNonBlocking)) != cudaSuccess)
       return cuda_fail(e, "stream create");
     if (!c->h_planes[s]) {
-      if ((e = cudaMalloc(&c->h_planes[s], (size_t)LS_MAX_HEADS * kHostChunk)) != cudaSuccess ||
-          (e = cudaMalloc(&c->h_reason[s], kHostChunk)) != cudaSuccess)
+      if ((e = cudaMalloc(&c->h_planes[s], (size_t)LS_MAX_HEADS * chunk_n)) != cudaSuccess ||
+          (e = cudaMalloc(&c->h_reason[s], chunk_n)) != cudaSuccess)
         return cuda_fail(e, "pipeline buffers");
     }
     for (int f = 0; f < 6; ++f)
-      if (hf[f] && !c->h_f[s][f] && (e = cudaMalloc(&c->h_f[s][f], sizeof(double) * kHostChunk)) != cudaSuccess)
+      if (hf[f] && !c->h_f[s][f] && (e = cudaMalloc(&c->h_f[s][f], sizeof(double) * chunk_n)) != cudaSuccess)
         return cuda_fail(e, "pipeline buffers");
   }
   int64_t chunk = 0;
-  for (int64_t off = 0; off < n; off += kHostChunk, ++chunk) {
-    const int s = (int)(chunk & 1);
-    const int64_t cnt = std::min<int64_t>(kHostChunk, n - off);
+  for (int64_t off = 0; off < n; off += chunk_n, ++chunk) {
+    const int s = (int)(chunk % c->pipe);
+    const int64_t cnt = std::min<int64_t>(chunk_n, n - off);
     cudaStream_t st = c->hs[s];
     if (host_words) {
       if ((e = cudaMemcpyAsync(c->h_planes[s], host_words + off, sizeof(uint64_t) * (size_t)cnt,
@@ -486,7 +506,7 @@ static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_st
                        cudaSuccess)
         return cuda_fail(e, "D2H field");
   }
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < c->pipe; ++s)
     if ((e = cudaStreamSynchronize(c->hs[s])) != cudaSuccess) return cuda_fail(e, "pipeline sync");
   return LS_OK;
 }
@@ -534,7 +554,8 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
 
 size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
   if (!c || k < 1) return 0;
-  const size_t fused = (size_t)c->blocks_tma * (size_t)k * sizeof(ls_elite_rec) + (size_t)c->blocks_tma * 4 + 32;
+  const size_t lists = (size_t)c->blocks_tma * (size_t)fused_lists_per_cta();
+  const size_t fused = lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4 + 32;
   return std::max(fused, topk_scratch_bytes(n, k, 0));
 }
 
@@ -585,10 +606,11 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   if (k <= fused_k_max() && c->blocks_tma > 0 && tma_eligible(a, c->M.A)) {
     LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
     const int64_t grid = ws_grid(lp, n);
+    const int64_t lists = grid * fused_lists_per_cta();
     TopkArgs tk{k, index_base, static_cast<ls_elite_rec*>(scratch), nullptr, nullptr};
-    tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
+    tk.part_counts = reinterpret_cast<int32_t*>(tk.part + lists * k);
     tk.floor = reinterpret_cast<unsigned long long*>(
-        (reinterpret_cast<uintptr_t>(tk.part_counts + grid) + 7) & ~uintptr_t(7));
+        (reinterpret_cast<uintptr_t>(tk.part_counts + lists) + 7) & ~uintptr_t(7));
     if (n == 0) {
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
       return LS_OK;
@@ -599,7 +621,7 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
     if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s,
                                   words ? &pk : nullptr)) != cudaSuccess)
       return cuda_fail(e, "evaluate_topk launch");
-    if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, tk.floor, topk_out, count_out, s)) !=
+    if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)lists, k, k, tk.floor, topk_out, count_out, s)) !=
         cudaSuccess)
       return cuda_fail(e, "topk merge launch");
     return LS_OK;
@@ -767,9 +789,10 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   }
   LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
   const int64_t grid = std::min<int64_t>((n + 1023) / 1024, c->blocks_tma);
+  const int64_t lists = grid * fused_lists_per_cta();
   TopkArgs tk{k, start, static_cast<ls_elite_rec*>(scratch), nullptr, nullptr};
-  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
-  tk.floor = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(tk.part_counts + grid) + 7) &
+  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + lists * k);
+  tk.floor = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(tk.part_counts + lists) + 7) &
                                                    ~uintptr_t(7));
   cudaError_t e;
   if ((e = cudaMemsetAsync(tk.floor, 0, sizeof(unsigned long long), s)) != cudaSuccess)
@@ -777,7 +800,7 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=
       cudaSuccess)
     return cuda_fail(e, "sweep launch");
-  if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)grid, k, k, tk.floor, topk_out, count_out, s)) !=
+  if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)lists, k, k, tk.floor, topk_out, count_out, s)) !=
       cudaSuccess)
     return cuda_fail(e, "sweep merge launch");
   return LS_OK;

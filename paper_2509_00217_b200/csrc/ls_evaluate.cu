@@ -41,6 +41,7 @@ constexpr int kTile = kGateWarps * kWarpCands;  // candidates per stage
 constexpr int kStages = 4;
 constexpr int kWarpQueue = 160;  // < 32 left over + 128 from one tile
 constexpr int kSlots = 2;        // mailbox slots per gate warp
+static_assert(kGateWarps / kFpWarps * kSlots <= 32, "mailbox bits per fp64 warp");
 constexpr int kGenericThreads = 256;
 constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
 constexpr uint32_t kStageBytes = 16 * kTile;  // 16 plane slices per stage (planes >= A stay zero)
@@ -82,6 +83,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
         : "memory");
   }
 }
@@ -229,7 +243,7 @@ struct WsSmem {
   uint32_t* qy;
   uint64_t* mkey;  // mailboxes [kGateWarps][kSlots][32]
   uint32_t* my;
-  uint8_t* lists;  // [kWorkWarps] elite lists
+  uint8_t* lists;  // [kWorkWarps] elite lists (end-of-kernel merge)
 };
 
 // words staged into shared memory: the coarse words in raw mode, else the gate segment
@@ -293,10 +307,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t gate_bar;
-  __shared__ int list_count[kWorkWarps];
   __shared__ int mb_n[kGateWarps][kSlots];
   __shared__ volatile int mb_state[kGateWarps][kSlots];  // 0 empty, 1 full
   __shared__ volatile int gates_done;
+  __shared__ int list_count[kWorkWarps];
+  __shared__ volatile uint32_t mb_pending[kFpWarps];  // full mailboxes per fp64 warp (bitmask)
   const int A = M.A;
   const uint32_t stage_bytes = (uint32_t)A * kTile;  // bytes the producer copies per stage
   WsSmem S;
@@ -319,8 +334,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int s = 0; s < kStages; ++s)
       for (int o = A * kTile + 16 * (int)threadIdx.x; o < (int)kStageBytes; o += 16 * kThreads)
         *reinterpret_cast<uint4*>(S.ring + s * kStageBytes + o) = make_uint4(0, 0, 0, 0);
-  if (threadIdx.x < kWorkWarps) list_count[threadIdx.x] = 0;
   if (threadIdx.x < kGateWarps * kSlots) mb_state[threadIdx.x / kSlots][threadIdx.x % kSlots] = 0;
+  if (threadIdx.x < kFpWarps) mb_pending[threadIdx.x] = 0;
+  if (threadIdx.x < kWorkWarps) list_count[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     gates_done = 0;
     for (int s = 0; s < NST; ++s) {
@@ -367,36 +383,33 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int f = warp - kGateWarps;
     unsigned backoff = 128;  // ns; idle fp64 warps back off so gate warps keep the issue slots
     for (;;) {
-      bool found = false;
-      for (int g = f; g < kGateWarps; g += kFpWarps) {
-        for (int sl = 0; sl < kSlots; ++sl) {
-          if (mb_state[g][sl] != 1) continue;
-          __threadfence_block();
-          found = true;
+      // one shared word per fp64 warp: bit (g / kFpWarps) * kSlots + slot set
+      // for every full mailbox of its gate warps g = f, f + kFpWarps, ...
+      uint32_t pend = __shfl_sync(0xffffffffu, mb_pending[f], 0);
+      if (pend) {
+        __threadfence_block();
+        while (pend) {
+          const int bit = __ffs(pend) - 1;
+          pend &= pend - 1;
+          const int g = f + kFpWarps * (bit / kSlots), sl = bit % kSlots;
           const int base = (g * kSlots + sl) * 32;
           fp64_batch<NEU, FULL, TOPK, MODE>(gtab, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl, gfloor,
                                             gm.pk);
           __syncwarp();
           if (lane == 0) {
+            atomicAnd((uint32_t*)&mb_pending[f], ~(1u << bit));
             __threadfence_block();
             mb_state[g][sl] = 0;
           }
           __syncwarp();
         }
-      }
-      if (!found) {
-        if (gates_done == kGateWarps) {
-          __threadfence_block();
-          bool any = false;  // gate warps finished: one last sweep of the slots
-          for (int g = f; g < kGateWarps; g += kFpWarps)
-            for (int sl = 0; sl < kSlots; ++sl) any |= mb_state[g][sl] == 1;
-          if (!any) break;
-        } else {
-          __nanosleep(backoff);
-          backoff = backoff < 4096 ? 2 * backoff : 4096;
-        }
-      } else {
         backoff = 128;
+      } else if (gates_done == kGateWarps) {
+        __threadfence_block();  // gate warps finished: one last look at the mailboxes
+        if (__shfl_sync(0xffffffffu, mb_pending[f], 0) == 0) break;
+      } else {
+        __nanosleep(backoff);
+        backoff = backoff < 4096 ? 2 * backoff : 4096;
       }
     }
   } else {  // ---------------- gate warps
@@ -425,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           mb_n[warp][slot] = n;
           __threadfence_block();
           mb_state[warp][slot] = 1;
+          atomicOr((uint32_t*)&mb_pending[warp % kFpWarps], 1u << ((warp / kFpWarps) * kSlots + slot));
         }
       } else {
         fp64_batch<NEU, FULL, TOPK, MODE>(gtab, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor, gm.pk);
@@ -436,7 +450,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // gate pass over this lane's 4 decoded candidates (stream indices base..)
     // ranks: coarse ranks of the 4 candidates when the candidates came as
     // packed words (t, e, p, b then split only where needed)
-    auto pass_a = [&](Decoded* cs, uint32_t badb, int64_t base, int count, const uint32_t* ranks) {
+    // whole: a full tile (every lane of the warp has count 4)
+    auto pass_a = [&](Decoded* cs, uint32_t badb, int64_t base, int count, const uint32_t* ranks, bool whole) {
       uint32_t r4 = 0, reason[4];
       double m[4];
       // the 4 gate evaluations are independent: issue them back to back (ILP)
@@ -467,26 +482,39 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         r4 |= reason[j] << (8 * j);
       }
-      // then compact the survivors into the warp queue
+      // then compact the survivors (~1% of a uniform batch) into the warp
+      // queue: the lane's survivor count 0..4 as three ballots gives every
+      // lane its queue position and the warp total in one step
+      uint32_t sv = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool surv = j < count && reason[j] == LS_REASON_NONE;
-        const unsigned mask = __ballot_sync(0xffffffffu, surv);
-        if (surv) {
-          const int pos = qcount + __popc(mask & ((1u << lane) - 1u));
-          qkey[pos] = (MODE == GEN_WORDS && !FULL) ? (uint64_t)(base + j) | ((uint64_t)ranks[j] << 40)
-                                                   : pack_key(base + j, cs[j]);
-          qy[pos] = cs[j].Y;
-        }
-        qcount += __popc(mask);
+      for (int j = 0; j < 4; ++j) sv |= (j < count && reason[j] == LS_REASON_NONE) ? 1u << j : 0u;
+      const uint32_t nsv = __popc(sv);
+      const uint32_t b0 = __ballot_sync(0xffffffffu, nsv & 1u), b1 = __ballot_sync(0xffffffffu, nsv & 2u),
+                     b2 = __ballot_sync(0xffffffffu, nsv & 4u);
+      if (b0 | b1 | b2) {
+        const uint32_t lt = (1u << lane) - 1u;
+        int pos = qcount + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (sv & (1u << j)) {
+            qkey[pos] = (MODE == GEN_WORDS && !FULL) ? (uint64_t)(base + j) | ((uint64_t)ranks[j] << 40)
+                                                     : pack_key(base + j, cs[j]);
+            qy[pos] = cs[j].Y;
+            ++pos;
+          }
+        qcount += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
       }
       if (!a.reason) {
         // sweep mode: no per-candidate verdicts, only the fused elite
-      } else if (count == 4) {
+      } else if (whole) {
         *reinterpret_cast<uint32_t*>(a.reason + base) = r4;
+        // zero fields: the warp's 128 consecutive doubles as two fully
+        // coalesced 512-byte stores (every lane of a full tile has count 4;
+        // survivors' values are stored later by the fp64 pass)
+        const int64_t wz = base - 4 * lane + 2 * lane;
         if (a.thr) {
-          st2(a.thr, base, 0.0, 0.0);
-          st2(a.thr, base + 2, 0.0, 0.0);
+          st2(a.thr, wz, 0.0, 0.0);
+          st2(a.thr, wz + 64, 0.0, 0.0);
         }
         if (FULL) {
           if (a.mem) {
@@ -497,8 +525,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int f = 0; f < 4; ++f)
             if (zf[f]) {
-              st2(zf[f], base, 0.0, 0.0);
-              st2(zf[f], base + 2, 0.0, 0.0);
+              st2(zf[f], wz, 0.0, 0.0);
+              st2(zf[f], wz + 64, 0.0, 0.0);
             }
         }
       } else {
@@ -534,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         Decoded cs[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
-        pass_a(cs, badb, tile * kTile + lane_off, 4, nullptr);
+        pass_a(cs, badb, tile * kTile + lane_off, 4, nullptr, true);
       }
       // ragged tail (< one tile): the CTA that would own the next tile
       const int64_t tail0 = ntiles * kTile;
@@ -553,24 +581,27 @@ __global__ void __launch_bounds__(kThreads, 2)
         Decoded cs[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
-        pass_a(cs, badb, base, count, nullptr);
+        pass_a(cs, badb, base, count, nullptr, false);
       }
     } else if (MODE == GEN_WORDS) {  // 4 consecutive 8-byte candidate words per lane
+      // shared addresses hoisted out of the loop (barriers are 8 B apart)
+      const uint32_t st0 = ring_base + 8u * (uint32_t)lane_off;
+      const uint32_t fb0 = smem_u32(&full_bar[0]), eb0 = smem_u32(&empty_bar[0]);
       int i = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-        const int s = i % NST;
-        mbar_wait(&full_bar[s], (uint32_t)((i / NST) & 1));
+        const uint32_t s = (uint32_t)(i % NST);
+        mbar_wait_a(fb0 + 8u * s, (uint32_t)((i / NST) & 1));
         uint64_t w[4];
-        const uint32_t st = ring_base + (uint32_t)s * STB + 8u * (uint32_t)lane_off;
+        const uint32_t st = st0 + s * STB;
         lds_u64x2(st, w[0], w[1]);
         lds_u64x2(st + 16, w[2], w[3]);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        if (lane == 0) mbar_arrive_a(eb0 + 8u * s);
         Decoded cs[4];
         uint32_t badb = 0, rk[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) badb |= word_decode(w[j], gm.pk, rk[j], cs[j].Y) << (8 * j);
-        pass_a(cs, badb, tile * kTile + lane_off, 4, rk);
+        pass_a(cs, badb, tile * kTile + lane_off, 4, rk, true);
       }
       const int64_t tail0 = ntiles * kTile;
       if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
@@ -581,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, rk[j], cs[j].Y) << (8 * j);
-        pass_a(cs, badb, base, count, rk);
+        pass_a(cs, badb, base, count, rk, false);
       }
     } else {  // candidates generated in registers: nothing read from HBM
       const int64_t gtiles = (a.n + kTile - 1) / kTile;
@@ -592,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int j = 0; j < 4; ++j)  // past-the-end lanes regenerate the last valid index (never enqueued)
           gen_candidate<MODE>(gm, (uint64_t)(gm.start + (base + j < a.n ? base + j : a.n - 1)), cs[j]);
-        pass_a(cs, 0u, base, count, nullptr);
+        pass_a(cs, 0u, base, count, nullptr, false);
       }
     }
     if (qcount > 0) flush(qcount);
@@ -612,8 +643,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int o = 1; o < kWorkWarps; ++o) wl.absorb(slots + o * 32, list_count[o], tk.k, fl);
       wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
     }
-  }
-}
+  }}
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
 template <bool NEU>
@@ -796,6 +826,7 @@ int64_t ws_grid(const LaunchPlan& lp, int64_t n) {
 }
 
 int fused_k_max() { return kFusedK; }
+int fused_lists_per_cta() { return 1; }
 
 cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
                         cudaStream_t s) {

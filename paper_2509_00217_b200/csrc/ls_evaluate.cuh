@@ -97,6 +97,11 @@ __device__ __forceinline__ int op_axis(const EvalMeta& M, uint32_t Y, int k) {
   return src >= 0 ? (int)((Y >> src) & 3u) : (int)M.op_pin[k];
 }
 
+// attn_core sharded on DIM1 (the high bit of its 2-bit field), or its pin.
+__device__ __forceinline__ uint32_t attn_dim1(const EvalMeta& M, uint32_t Y) {
+  return ((Y | M.attn_or) >> M.attn_shift) & 1u;
+}
+
 // Gate pass (every candidate), branch-free: one 128-bit lookup of the
 // (t, e, p) entry gives the weights term, the gate bits and the kv row; the
 // reason is then selected in the reference's gate order — device budget
@@ -110,7 +115,7 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
   const uint4 ent = *reinterpret_cast<const uint4*>(G + L.tep + 2 * tep);
   const double w = __hiloint2double((int)ent.y, (int)ent.x);
   const uint32_t bits = ent.z, kv_row = ent.w;
-  const uint32_t a2 = M.attn_src >= 0 ? (c.Y >> (M.attn_src + 1)) & 1u : (uint32_t)(M.attn_pin == 2);
+  const uint32_t a2 = attn_dim1(M, c.Y);
   const double m = (w + dget(G, L.mem_kv + (int)(a2 * (uint32_t)(L.nt * L.np * L.nb) + kv_row) + c.b)) +
                    dget(G, L.mem_ws + c.b);
   const bool over = (bits & GATE_BUDGET) != 0;
@@ -126,10 +131,10 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
 __device__ __forceinline__ uint32_t gate_coarse(const uint32_t* C, const TabLayout& L, const EvalMeta& M,
                                                 const Decoded& c) {
   const uint32_t cw = C[((c.t * L.ne + c.e) * L.np + c.p) * L.nb + c.b];
-  const uint32_t a2 = M.attn_src >= 0 ? (c.Y >> (M.attn_src + 1)) & 1u : (uint32_t)(M.attn_pin == 2);
+  const uint32_t a2 = attn_dim1(M, c.Y);
   const bool over = (cw & GATE_BUDGET) != 0;
   const bool bad = ((c.Y & cw & GATE_FIELDS) | (cw & (GATE_PINNED | GATE_LAYOUT))) != 0;
-  const bool oom = (cw & (a2 ? GATE_OOM1 : GATE_OOM0)) != 0;
+  const bool oom = (cw & (GATE_OOM0 << a2)) != 0;
   return over ? LS_REASON_OVER_DEVICE_BUDGET
               : (bad ? LS_REASON_LAYOUT_ERROR : (oom ? LS_REASON_OOM : LS_REASON_NONE));
 }
@@ -137,10 +142,10 @@ __device__ __forceinline__ uint32_t gate_coarse(const uint32_t* C, const TabLayo
 // Same, from the coarse rank ((t*ne + e)*np + p)*nb + b directly.
 __device__ __forceinline__ uint32_t gate_rank(const uint32_t* C, const EvalMeta& M, uint32_t rank, uint32_t Y) {
   const uint32_t cw = C[rank];
-  const uint32_t a2 = M.attn_src >= 0 ? (Y >> (M.attn_src + 1)) & 1u : (uint32_t)(M.attn_pin == 2);
+  const uint32_t a2 = attn_dim1(M, Y);
   const bool over = (cw & GATE_BUDGET) != 0;
   const bool bad = ((Y & cw & GATE_FIELDS) | (cw & (GATE_PINNED | GATE_LAYOUT))) != 0;
-  const bool oom = (cw & (a2 ? GATE_OOM1 : GATE_OOM0)) != 0;
+  const bool oom = (cw & (GATE_OOM0 << a2)) != 0;
   return over ? LS_REASON_OVER_DEVICE_BUDGET
               : (bad ? LS_REASON_LAYOUT_ERROR : (oom ? LS_REASON_OOM : LS_REASON_NONE));
 }

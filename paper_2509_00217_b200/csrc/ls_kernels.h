@@ -71,6 +71,7 @@ cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_
                         cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n);
 int fused_k_max();
+int fused_lists_per_cta();  // elite lists one eval_ws_kernel CTA emits (TOPK)
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
                                  const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s,
                                  const PackMeta* pk = nullptr);

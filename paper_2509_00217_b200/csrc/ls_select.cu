@@ -167,12 +167,13 @@ __device__ __forceinline__ void list_init<WarpList>(WarpList& l, TopkSmem& s, in
 
 // Merge the CTA's warp lists into warp 0's and write it out.
 template <class List>
-__device__ void merge_and_emit(List& l, TopkSmem& s, int k, double floor, ls_elite_rec* out, int32_t* count_out) {
+__device__ void merge_and_emit(List& l, TopkSmem& s, int k, double floor, ls_elite_rec* out, int32_t* count_out,
+                               int64_t floor_idx = INT64_MAX) {
   const int w = threadIdx.x >> 5;
   l.store(s.slots[w], &s.slot_count[w]);
   __syncthreads();
   if (w == 0) {
-    for (int o = 1; o < kTopkWarps; ++o) l.absorb(s.slots[o], s.slot_count[o], k, floor);
+    for (int o = 1; o < kTopkWarps; ++o) l.absorb(s.slots[o], s.slot_count[o], k, floor, floor_idx);
     l.emit(out, count_out);
   }
 }
@@ -241,13 +242,45 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite
                                                                   ls_elite_rec* __restrict__ out,
                                                                   int32_t* __restrict__ count_out) {
   __shared__ TopkSmem s;
-  __shared__ unsigned long long s_floor;  // CTA-wide pruning floor
+  __shared__ double s_fk[kTopkWarps];
+  __shared__ int64_t s_fi[kTopkWarps];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_floor = 0;
+  // Exact floor (key, index): the best k-th entry of any full input list.
+  // That list holds k distinct vectors at least as good, so every record
+  // strictly worse cannot be in the merged top-k (or is not its vector's best
+  // occurrence). Unlike a key-only floor it also prunes ties on the key.
+  double fk = floor ? read_floor(floor) : -1.0e308;
+  int64_t fi = INT64_MAX;
+  if (k <= k_in)
+    for (int t = threadIdx.x; t < m; t += kTopkThreads)
+      if (counts[t] >= k) {
+        const ls_elite_rec& e = recs[(int64_t)t * k_in + k - 1];
+        if (better(e.key, e.index, fk, fi)) {
+          fk = e.key;
+          fi = e.index;
+        }
+      }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ok = __shfl_xor_sync(0xffffffffu, fk, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, fi, o);
+    if (better(ok, oi, fk, fi)) {
+      fk = ok;
+      fi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_fk[w] = fk;
+    s_fi[w] = fi;
+  }
   __syncthreads();
+  for (int o = 0; o < kTopkWarps; ++o)
+    if (better(s_fk[o], s_fi[o], fk, fi)) {
+      fk = s_fk[o];
+      fi = s_fi[o];
+    }
   List wl;
   list_init(wl, s, w);
-  double fl = floor ? read_floor(floor) : -1.0e308;
   // records flattened across lists, 32 per warp step: independent loads, so
   // the single CTA is bound by a few L2 round trips, not by m sequential lists
   const int total = m * k_in;
@@ -263,17 +296,109 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite
         r.raw = e.raw;
         r.idx = e.index;
         r.code = e.code;
-        have = r.key >= fl;
+        have = at_least(r.key, r.idx, fk, fi);
       }
     }
     wl.offer(have, r, k);
-    if (floor) {
-      const double mine = wl.floor_key(k);
-      if (lane == 0 && mine > fl) raise_floor(&s_floor, mine);
-      fl = fmax(fl, fmax(mine, read_floor(&s_floor)));
+  }
+  merge_and_emit(wl, s, k, fk, out, count_out, fi);
+}
+
+// Fast merge of m short lists (k <= 32, register lists), one CTA of 1024
+// threads. It is latency-bound, so it runs as a few rounds of independent
+// loads instead of a walk over the lists:
+//   1. every thread loads the counts of a few lists and the k-th record of
+//      each full one; a block reduction gives the exact (key, index) floor —
+//      the best k-th entry of any full list (see at_least());
+//   2. lane l of a warp takes list l of a 32-list group and loads its
+//      records two at a time; records at least as good as the floor (usually
+//      a handful: the lists of the fused evaluate are already pruned by the
+//      global key floor) are offered to the warp's register list;
+//   3. the 32 warp lists merge in a 5-level tree.
+constexpr int kMergeThreads = 1024;
+constexpr int kMergeWarps = kMergeThreads / 32;
+
+__global__ void __launch_bounds__(kMergeThreads) topk_merge_fast_kernel(const ls_elite_rec* __restrict__ recs,
+                                                                        const int32_t* __restrict__ counts, int m,
+                                                                        int k_in, int k,
+                                                                        const unsigned long long* floor,
+                                                                        ls_elite_rec* __restrict__ out,
+                                                                        int32_t* __restrict__ count_out) {
+  __shared__ Rec slots[kMergeWarps][32];
+  __shared__ int slot_count[kMergeWarps];
+  __shared__ double s_fk[kMergeWarps];
+  __shared__ int64_t s_fi[kMergeWarps];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // 1. the (key, index) floor
+  double fk = floor ? read_floor(floor) : -1.0e308;
+  int64_t fi = INT64_MAX;
+  for (int l = threadIdx.x; l < m; l += kMergeThreads)
+    if (__ldg(counts + l) >= k && k <= k_in) {
+      const ls_elite_rec& e = recs[(int64_t)l * k_in + k - 1];
+      if (better(e.key, e.index, fk, fi)) {
+        fk = e.key;
+        fi = e.index;
+      }
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ok = __shfl_xor_sync(0xffffffffu, fk, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, fi, o);
+    if (better(ok, oi, fk, fi)) {
+      fk = ok;
+      fi = oi;
     }
   }
-  merge_and_emit(wl, s, k, floor ? fl : -1.0e308, out, count_out);
+  if (lane == 0) {
+    s_fk[w] = fk;
+    s_fi[w] = fi;
+  }
+  __syncthreads();
+  for (int o = 0; o < kMergeWarps; ++o)
+    if (better(s_fk[o], s_fi[o], fk, fi)) {
+      fk = s_fk[o];
+      fi = s_fi[o];
+    }
+
+  // 2. lane-per-list offers, four records per lane per round
+  RegList wl;
+  wl.init();
+  for (int l0 = w * 32; l0 < m; l0 += kMergeThreads) {
+    const int l = l0 + lane;
+    const int c = l < m ? min(__ldg(counts + l), k_in) : 0;
+    int cmax = c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    const ls_elite_rec* base = recs + (int64_t)l * k_in;
+    for (int j0 = 0; j0 < cmax; j0 += 2) {
+      Rec r[2];
+      bool have[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        have[u] = j0 + u < c;
+        r[u] = Rec{0.0, 0.0, 0, 0};
+        if (have[u]) {
+          const ls_elite_rec& e = base[j0 + u];
+          r[u] = Rec{e.key, e.raw, e.index, e.code};
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) wl.offer(have[u] && at_least(r[u].key, r[u].idx, fk, fi), r[u], k);
+    }
+  }
+
+  // 3. tree merge of the warp lists
+  wl.store(slots[w], &slot_count[w]);
+  __syncthreads();
+  for (int st = 1; st < kMergeWarps; st <<= 1) {
+    if ((w & (2 * st - 1)) == 0 && slot_count[w + st] > 0) {
+      wl.absorb(slots[w + st], slot_count[w + st], k, fk, fi);
+      wl.store(slots[w], &slot_count[w]);
+    }
+    __syncthreads();
+  }
+  if (w == 0) wl.emit(out, count_out);
 }
 
 }  // namespace
@@ -323,7 +448,7 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
   if (k <= 32) {
     topk_local_kernel<RegList><<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k,
                                                           index_base, part, counts);
-    topk_merge_kernel<RegList><<<1, kTopkThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
+    topk_merge_fast_kernel<<<1, kMergeThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
   } else {
     topk_local_kernel<WarpList><<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k,
                                                            index_base, part, counts);
@@ -336,7 +461,7 @@ cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, i
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s) {
   if (k <= 32)
-    topk_merge_kernel<RegList><<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
+    topk_merge_fast_kernel<<<1, kMergeThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
   else
     topk_merge_kernel<WarpList><<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
   return cudaGetLastError();

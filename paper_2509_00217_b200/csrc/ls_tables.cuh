@@ -85,6 +85,8 @@ struct EvalMeta {
   int A;                              // vector length
   int attn_src;                       // 2*(h-4) of the head controlling attn_core, or -1
   int attn_pin;                       // attn_core axis when not controlled
+  int attn_shift;                     // attn_core is DIM1: ((Y | attn_or) >> attn_shift) & 1
+  uint32_t attn_or;                   //   (shift 31 and a constant bit 31 when pinned; Y < 2^24)
   int pad0_;
   uint8_t head_size[LS_MAX_HEADS];    // domain size per head
   int8_t head_slot[LS_MAX_HEADS];     // Y field of each head (head_slots), -1 none

@@ -27,6 +27,12 @@ struct Rec {
 __device__ __forceinline__ bool better(double ka, int64_t ia, double kb, int64_t ib) {
   return ka > kb || (ka == kb && ia < ib);
 }
+// (ka, ia) is the floor record or better than it. A floor (key, idx) taken
+// from a full list's k-th entry is beaten by k distinct vectors; with
+// idx = INT64_MAX it is the key-only floor (key >= floor).
+__device__ __forceinline__ bool at_least(double ka, int64_t ia, double kf, int64_t i_f) {
+  return ka > kf || (ka == kf && ia <= i_f);
+}
 
 // Sorted (best first) list of at most k <= 64 distinct records in shared
 // memory, operated on by one full warp.
@@ -160,7 +166,8 @@ struct WarpList {
     for (int j = lane; j < c; j += 32) slots[j] = Rec{key[j], raw[j], idx[j], code[j]};
     if (lane == 0) *cnt = c;
   }
-  __device__ void absorb(const Rec* slots, int n, int k, double floor = -1.0e308) {
+  __device__ void absorb(const Rec* slots, int n, int k, double floor = -1.0e308,
+                         int64_t floor_idx = INT64_MAX) {
     const int lane = threadIdx.x & 31;
     for (int j0 = 0; j0 < n; j0 += 32) {
       const int j = j0 + lane;
@@ -168,7 +175,7 @@ struct WarpList {
       bool have = false;
       if (j < n) {
         r = slots[j];
-        have = r.key >= floor;
+        have = at_least(r.key, r.idx, floor, floor_idx);
       }
       offer(have, r, k);
     }
@@ -284,7 +291,8 @@ struct RegList {
   }
 
   // Offer n records held in shared memory slots (any order is exact).
-  __device__ void absorb(const Rec* slots, int n, int k, double floor = -1.0e308) {
+  __device__ void absorb(const Rec* slots, int n, int k, double floor = -1.0e308,
+                         int64_t floor_idx = INT64_MAX) {
     const int lane = threadIdx.x & 31;
     for (int j0 = 0; j0 < n; j0 += 32) {
       const int j = j0 + lane;
@@ -292,10 +300,25 @@ struct RegList {
       bool have = false;
       if (j < n) {
         r = slots[j];
-        have = r.key >= floor;
+        have = at_least(r.key, r.idx, floor, floor_idx);
       }
       offer(have, r, k);
     }
+  }
+
+  // Emit only the entries with key >= floor (a prefix: the list is sorted).
+  __device__ void emit_from(double floor, ls_elite_rec* out, int32_t* count_out) const {
+    const int lane = threadIdx.x & 31;
+    const int c = __popc(__ballot_sync(0xffffffffu, lane < count && key >= floor));
+    if (lane < c) {
+      ls_elite_rec e;
+      e.key = key;
+      e.raw = raw;
+      e.index = idx;
+      e.code = code;
+      out[lane] = e;
+    }
+    if (lane == 0) *count_out = c;
   }
 
   __device__ void emit(ls_elite_rec* out, int32_t* count_out) const {
