@@ -248,16 +248,18 @@ def run_ours(args, rank, world, local_rank):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
         if world > 1:
+            # records + count land in the all-gather's send buffer (one collective)
             if cands.dim() == 1:
-                _, recs, count = ev.evaluate_packed_topk(cands, k=ELITE_K, index_base=base, out=out)
+                _, recs, count = ev.evaluate_packed_topk(cands, k=ELITE_K, index_base=base, out=out,
+                                                         into=sweep._send)
             else:
-                _, recs, count = ev.evaluate_topk(cands, k=ELITE_K, index_base=base, out=out)
+                _, recs, count = ev.evaluate_topk(cands, k=ELITE_K, index_base=base, out=out, into=sweep._send)
             if timed:
                 b.record(stream)
                 ev_start.append(a)
                 ev_end.append(b)
             recs, count = sweep.merge(recs, count)
-            return recs, count, 3
+            return recs, count, 3  # our kernels: evaluate, local merge, global merge
         _, recs, count = sweep.run(cands, index_base=base, out=out)
         if timed:
             b.record(stream)

@@ -64,8 +64,9 @@ class ShardedSweep:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         dev = evaluator.device
-        self._gathered = torch.empty((self.world * self.k, 32), dtype=torch.uint8, device=dev)
-        self._gcounts = torch.empty(self.world, dtype=torch.int32, device=dev)
+        # one message per rank: k records + a 32-byte row holding the count
+        self._send = torch.empty((self.k + 1, 32), dtype=torch.uint8, device=dev)
+        self._gathered = torch.empty((self.world * (self.k + 1), 32), dtype=torch.uint8, device=dev)
 
     def run(self, candidates: torch.Tensor, index_base: int, out=None, verdicts: bool = True):
         """Score this rank's candidates (global indices index_base..) and return the global elite.
@@ -73,19 +74,25 @@ class ShardedSweep:
         ``candidates``: [A, n] uint8 planes, or n packed 64-bit words.
         Returns (out, recs, count) with recs/count the merged global top-k on device.
         """
+        into = self._send if self.world > 1 else None
         if candidates.dim() == 1:
             out, recs, count = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
-                                                            verdicts=verdicts)
+                                                            verdicts=verdicts, into=into)
         else:
             out, recs, count = self.ev.evaluate_topk(candidates, k=self.k, index_base=index_base, out=out,
-                                                     verdicts=verdicts)
+                                                     verdicts=verdicts, into=into)
         recs, count = self.merge(recs, count)
         return out, recs, count
 
     def merge(self, recs: torch.Tensor, count: torch.Tensor):
-        """All-gather every rank's device top-k (k x 32 B) and merge on device."""
+        """All-gather every rank's device top-k (k x 32 B + count) in ONE collective and merge on device."""
         if self.world == 1:
             return recs, count
-        dist.all_gather_into_tensor(self._gathered, recs, group=self.group)
-        dist.all_gather_into_tensor(self._gcounts, count, group=self.group)
-        return self.ev.merge_records(self._gathered, self._gcounts, self.k, self.k)
+        if recs.data_ptr() != self._send.data_ptr():  # not produced in place by run()
+            self._send[: self.k].copy_(recs)
+            self._send[self.k, :4].view(torch.int32).copy_(count)
+        dist.all_gather_into_tensor(self._gathered, self._send, group=self.group)
+        g = self._gathered.view(self.world, self.k + 1, 32)
+        counts = g[:, self.k, :4].contiguous().view(torch.int32).reshape(self.world)
+        # each rank's list is k_in = k + 1 slots; the count row is never read (count <= k)
+        return self.ev.merge_records(self._gathered, counts, self.k + 1, self.k)

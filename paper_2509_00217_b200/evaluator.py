@@ -228,7 +228,7 @@ class Evaluator:
                 for i in range(n)]
 
     def evaluate_topk(self, planes: torch.Tensor, k: int = 3, index_base: int = 0, out: BatchResult | None = None,
-                      fields=("throughput",), verdicts: bool = True):
+                      fields=("throughput",), verdicts: bool = True, into: torch.Tensor | None = None):
         """Fused sweep: score the batch and reduce it to the top-k by raw in one pass.
 
         With ``verdicts=False`` nothing per-candidate is written (16 B of HBM
@@ -248,8 +248,7 @@ class Evaluator:
             for f in (FIELDS if fields == "all" else fields):
                 setattr(out, f, torch.empty(n, dtype=torch.float64, device=self.device))
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
-        recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
-        count = torch.empty(1, dtype=torch.int32, device=self.device)
+        recs, count = self._elite_out(k, into)
         nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
         if self._scratch is None or self._scratch.numel() < nbytes:
             self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -297,15 +296,26 @@ class Evaluator:
                                            self._stream()))
         return out
 
+    def _elite_out(self, k: int, into: torch.Tensor | None):
+        """(records, count) outputs: fresh tensors, or views of a caller's [(k + 1), 32]
+        uint8 buffer (records in rows 0..k-1, the int32 count at the start of row k) —
+        one contiguous message for the cross-rank all-gather."""
+        if into is None:
+            return (torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device),
+                    torch.empty(1, dtype=torch.int32, device=self.device))
+        if into.shape != (k + 1, _REC_BYTES) or into.dtype != torch.uint8 or not into.is_contiguous():
+            raise ValueError("into must be a contiguous [(k + 1), 32] uint8 tensor")
+        return into[:k], into[k, :4].view(torch.int32)
+
     def evaluate_packed_topk(self, words: torch.Tensor, k: int = 3, index_base: int = 0,
-                             out: BatchResult | None = None, fields=("throughput",), verdicts: bool = True):
+                             out: BatchResult | None = None, fields=("throughput",), verdicts: bool = True,
+                             into: torch.Tensor | None = None):
         """Fused evaluate + top-k by raw over packed words. Returns (out, records, count)."""
         n = self._check_words(words)
         if verdicts and out is None:
             out = self._alloc(n, fields)
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
-        recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
-        count = torch.empty(1, dtype=torch.int32, device=self.device)
+        recs, count = self._elite_out(k, into)
         nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
         if self._scratch is None or self._scratch.numel() < nbytes:
             self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)

@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, k, q):
+def _worker(rank, world, port, n, k, q, packed=False):
     import torch.distributed as dist
 
     from paper_2509_00217_b200.config import load_workload
@@ -35,6 +35,8 @@ def _worker(rank, world, port, n, k, q):
         planes = np.stack([rng.integers(0, s, size=n, dtype=np.uint8) for s in ev.head_sizes])
         lo, hi = shard_range(n, rank, world)
         mine = torch.from_numpy(np.ascontiguousarray(planes[:, lo:hi])).cuda(rank)
+        if packed:  # 8-byte candidate words (the bench's resident format)
+            mine = ev.pack(mine)
         sweep = ShardedSweep(ev, k=k)
         _, recs, count = sweep.run(mine, index_base=lo)
         elites = ev.decode_records(recs, count)
@@ -49,15 +51,16 @@ def _worker(rank, world, port, n, k, q):
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("packed", [False, True])
 @pytest.mark.parametrize("k", [3, 8])
-def test_two_gpu_elite_equals_single_gpu(k):
+def test_two_gpu_elite_equals_single_gpu(k, packed):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     n = 5_000_003
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, k, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, k, q, packed)) for r in range(2)]
     for p in procs:
         p.start()
     merged, single = q.get(timeout=300)
