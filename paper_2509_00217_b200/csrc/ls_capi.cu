@@ -319,10 +319,9 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
     delete c;
     return cuda_fail(e, "build_tables");
   }
-  // gate tables go to shared memory when the whole TMA footprint still
-  // allows two CTAs per SM; otherwise they are read through L1.
-  const size_t two_cta = (size_t)prop.sharedMemPerMultiprocessor / 2 - 2048;
-  c->smem_gate = tma_smem_bytes(c->L, c->desc.vector_length, true) <= two_cta;
+  // the workload's tables go to shared memory when they fit beside the ring
+  // at the kernel's CTAs-per-SM; otherwise both passes read them through L1
+  c->smem_gate = tma_smem_bytes(c->L, c->desc.vector_length, true) <= tma_smem_budget(prop);
   if (c->desc.vector_length <= 16) {
     prepare_eval_kernels(c->L, c->desc.vector_length, c->smem_gate);
     c->blocks_tma = (int64_t)c->num_sms * std::max(1, tma_blocks_per_sm(c->L, c->desc.vector_length, c->smem_gate));

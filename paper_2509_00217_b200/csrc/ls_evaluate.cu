@@ -32,20 +32,36 @@ namespace ls {
 
 namespace {
 
-constexpr int kGateWarps = 8;
-constexpr int kFpWarps = 2;
+// Role counts and ring size (LS_* overrides are for tuning builds only).
+#ifndef LS_GATE_WARPS
+#define LS_GATE_WARPS 12
+#endif
+#ifndef LS_FP_WARPS
+#define LS_FP_WARPS 4
+#endif
+#ifndef LS_RING_KB
+#define LS_RING_KB 48
+#endif
+#ifndef LS_MIN_BLOCKS
+#define LS_MIN_BLOCKS 1
+#endif
+#ifndef LS_BACKOFF_MAX
+#define LS_BACKOFF_MAX 512
+#endif
+constexpr int kGateWarps = LS_GATE_WARPS;
+constexpr int kFpWarps = LS_FP_WARPS;
 constexpr int kWorkWarps = kGateWarps + kFpWarps;
 constexpr int kThreads = 32 * (kWorkWarps + 1);  // + producer warp
 constexpr int kWarpCands = 128;
 constexpr int kTile = kGateWarps * kWarpCands;  // candidates per stage
-constexpr int kStages = 4;
 constexpr int kWarpQueue = 160;  // < 32 left over + 128 from one tile
 constexpr int kSlots = 2;        // mailbox slots per gate warp
 static_assert(kGateWarps / kFpWarps * kSlots <= 32, "mailbox bits per fp64 warp");
 constexpr int kGenericThreads = 256;
 constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
 constexpr uint32_t kStageBytes = 16 * kTile;  // 16 plane slices per stage (planes >= A stay zero)
-constexpr uint32_t kRingBytes = kStages * kStageBytes;
+constexpr uint32_t kRingBytes = LS_RING_KB * 1024;
+static_assert(kRingBytes % kStageBytes == 0 && kRingBytes / kStageBytes >= 2, "ring holds whole plane stages");
 // packed words are 8 B per candidate: the same ring holds twice the stages,
 // keeping the bytes in flight per SM (and so the HBM pipe) as full as for planes
 constexpr int kMaxStages = kRingBytes / (8 * kTile);
@@ -247,7 +263,9 @@ struct WsSmem {
 };
 
 // words staged into shared memory: the coarse words in raw mode, else the gate segment
-__host__ __device__ inline int stage_words(const TabLayout& L) { return L.gate_words > L.coarse_words ? L.gate_words : L.coarse_words; }
+// words staged into shared memory: the whole table (gate words, coarse
+// words and every fp64 segment), so neither pass touches L1 or L2 for tables
+__host__ __device__ inline int stage_words(const TabLayout& L) { return L.words; }
 
 inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
   return (size_t)kRingBytes + (smem_gate ? (size_t)gate_words * 8 : 0) +
@@ -257,7 +275,7 @@ inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
 
 // fp64 pass over n <= 32 survivors (lane i takes entry i of keys/ys), with
 // verdict stores and the optional elite offer. Called by whole warps.
-template <bool NEU, bool FULL, bool TOPK, int MODE>
+template <bool NEU, bool FULL, bool TOPK, int MODE, bool SMEM_TAB>
 __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, const TabLayout& L, const EvalMeta& M,
                                         const EvalArgs& a, const TopkArgs& tk, const uint64_t* keys,
                                         const uint32_t* ys, int n, RegList& wl, double& gfloor,
@@ -276,7 +294,7 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
     } else {
       unpack_key(keys[lane], ys[lane], idx, c);
     }
-    full_path<NEU>(gtab, L, M, c, v);
+    full_path<NEU, !SMEM_TAB>(gtab, L, M, c, v);  // gtab: the shared-memory copy when SMEM_TAB
     if (a.reason) write_verdict<FULL>(a, idx, v);
   }
   if (TOPK) {  // fused elite: valid survivors offered to this warp's list
@@ -298,7 +316,7 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
 }
 
 template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
                    const int64_t ntiles, const TopkArgs tk, const GenMeta gm) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -318,8 +336,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   S.ring = smem;
   S.gate = reinterpret_cast<uint64_t*>(smem + kRingBytes);
   S.qkey = SMEM_GATE ? S.gate + stage_words(L) : S.gate;
+  const uint64_t* T = SMEM_GATE ? S.gate : gtab;  // the table the fp64 pass reads
   const bool coarse = !FULL && L.coarse_words > 0;
-  const uint32_t* Cg = reinterpret_cast<const uint32_t*>(SMEM_GATE ? S.gate : gtab + L.coarse);
+  const uint32_t* Cg = reinterpret_cast<const uint32_t*>((SMEM_GATE ? S.gate : gtab) + L.coarse);
   S.qy = reinterpret_cast<uint32_t*>(S.qkey + kGateWarps * kWarpQueue);
   S.mkey = reinterpret_cast<uint64_t*>(S.qy + kGateWarps * kWarpQueue);
   S.my = reinterpret_cast<uint32_t*>(S.mkey + kGateWarps * kSlots * 32);
@@ -331,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // plane slices >= A are never written by the TMA: zero them once so the
   // gate warps can load all 16 unconditionally (zero = in range, UNSHARDED)
   if (MODE == GEN_PLANES)
-    for (int s = 0; s < kStages; ++s)
+    for (int s = 0; s < NST; ++s)
       for (int o = A * kTile + 16 * (int)threadIdx.x; o < (int)kStageBytes; o += 16 * kThreads)
         *reinterpret_cast<uint4*>(S.ring + s * kStageBytes + o) = make_uint4(0, 0, 0, 0);
   if (threadIdx.x < kGateWarps * kSlots) mb_state[threadIdx.x / kSlots][threadIdx.x % kSlots] = 0;
@@ -352,9 +371,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kWorkWarps) {  // ---------------- producer warp
     if (lane == 0) {
       if (SMEM_GATE) {
-        const uint32_t words = coarse ? (uint32_t)L.coarse_words : (uint32_t)L.gate_words;
-        mbar_expect_tx(&gate_bar, words * 8u);
-        bulk_g2s(S.gate, coarse ? gtab + L.coarse : gtab, words * 8u, &gate_bar);
+        const uint32_t bytes = (uint32_t)stage_words(L) * 8u;
+        mbar_expect_tx(&gate_bar, bytes);
+        bulk_g2s(S.gate, gtab, bytes, &gate_bar);
       }
       int i = 0;
       for (int64_t tile = blockIdx.x; (MODE == GEN_PLANES || MODE == GEN_WORDS) && tile < ntiles;
@@ -381,7 +400,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp >= kGateWarps) {  // ---------------- fp64 warps: drain the mailboxes
     const int f = warp - kGateWarps;
-    unsigned backoff = 128;  // ns; idle fp64 warps back off so gate warps keep the issue slots
+    if (SMEM_GATE) mbar_wait(&gate_bar, 0);  // the staged table they read
+    unsigned backoff = LS_BACKOFF_MAX < 128 ? LS_BACKOFF_MAX : 128;  // ns; idle fp64 warps back off so gate warps keep the issue slots
     for (;;) {
       // one shared word per fp64 warp: bit (g / kFpWarps) * kSlots + slot set
       // for every full mailbox of its gate warps g = f, f + kFpWarps, ...
@@ -393,8 +413,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           pend &= pend - 1;
           const int g = f + kFpWarps * (bit / kSlots), sl = bit % kSlots;
           const int base = (g * kSlots + sl) * 32;
-          fp64_batch<NEU, FULL, TOPK, MODE>(gtab, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl, gfloor,
-                                            gm.pk);
+          fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl,
+                                                       gfloor, gm.pk);
           __syncwarp();
           if (lane == 0) {
             atomicAnd((uint32_t*)&mb_pending[f], ~(1u << bit));
@@ -403,13 +423,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           __syncwarp();
         }
-        backoff = 128;
+        backoff = LS_BACKOFF_MAX < 128 ? LS_BACKOFF_MAX : 128;
       } else if (gates_done == kGateWarps) {
         __threadfence_block();  // gate warps finished: one last look at the mailboxes
         if (__shfl_sync(0xffffffffu, mb_pending[f], 0) == 0) break;
       } else {
         __nanosleep(backoff);
-        backoff = backoff < 4096 ? 2 * backoff : 4096;
+        backoff = backoff < LS_BACKOFF_MAX ? 2 * backoff : LS_BACKOFF_MAX;
       }
     }
   } else {  // ---------------- gate warps
@@ -441,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           atomicOr((uint32_t*)&mb_pending[warp % kFpWarps], 1u << ((warp / kFpWarps) * kSlots + slot));
         }
       } else {
-        fp64_batch<NEU, FULL, TOPK, MODE>(gtab, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor, gm.pk);
+        fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor, gm.pk);
       }
       qcount -= n;
       __syncwarp();
@@ -771,6 +791,11 @@ __global__ void pack_kernel(const PackMeta pk, int A, const uint8_t* __restrict_
 }
 
 }  // namespace
+
+size_t tma_smem_budget(const cudaDeviceProp& prop) {
+  const size_t per_cta = (size_t)prop.sharedMemPerMultiprocessor / LS_MIN_BLOCKS - 2048;
+  return per_cta < (size_t)prop.sharedMemPerBlockOptin ? per_cta : (size_t)prop.sharedMemPerBlockOptin;
+}
 
 size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate) {
   return ws_dynamic_bytes(A, stage_words(L), smem_gate);

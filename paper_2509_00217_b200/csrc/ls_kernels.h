@@ -79,6 +79,7 @@ cudaError_t prepare_eval_kernels(const TabLayout& L, int A, bool smem_gate);
 int tma_blocks_per_sm(const TabLayout& L, int A, bool smem_gate);
 int generic_blocks_per_sm();
 size_t tma_smem_bytes(const TabLayout& L, int A, bool smem_gate);
+size_t tma_smem_budget(const cudaDeviceProp& prop);  // dynamic smem one eval_ws_kernel CTA may use
 cudaError_t launch_evaluate(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
                             const EvalMeta& M, const EvalArgs& a, cudaStream_t s, const PackMeta* pk = nullptr);
 
