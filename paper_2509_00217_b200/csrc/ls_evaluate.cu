@@ -34,13 +34,13 @@ namespace {
 
 // Role counts and ring size (LS_* overrides are for tuning builds only).
 #ifndef LS_GATE_WARPS
-#define LS_GATE_WARPS 12
+#define LS_GATE_WARPS 16
 #endif
 #ifndef LS_FP_WARPS
 #define LS_FP_WARPS 4
 #endif
 #ifndef LS_RING_KB
-#define LS_RING_KB 48
+#define LS_RING_KB 64
 #endif
 #ifndef LS_MIN_BLOCKS
 #define LS_MIN_BLOCKS 1
@@ -259,7 +259,7 @@ struct WsSmem {
   uint32_t* qy;
   uint64_t* mkey;  // mailboxes [kGateWarps][kSlots][32]
   uint32_t* my;
-  uint8_t* lists;  // [kWorkWarps] elite lists (end-of-kernel merge)
+  uint8_t* lists;  // [kWorkWarps] elite lists (end-of-kernel merge, aliases the ring)
 };
 
 // words staged into shared memory: the coarse words in raw mode, else the gate segment
@@ -269,8 +269,7 @@ __host__ __device__ inline int stage_words(const TabLayout& L) { return L.words;
 
 inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
   return (size_t)kRingBytes + (smem_gate ? (size_t)gate_words * 8 : 0) +
-         (size_t)kGateWarps * kWarpQueue * 12 + (size_t)kGateWarps * kSlots * 32 * 12 +
-         (size_t)kWorkWarps * warp_list_bytes(kFusedK);
+         (size_t)kGateWarps * kWarpQueue * 12 + (size_t)kGateWarps * kSlots * 32 * 12;
 }
 
 // fp64 pass over n <= 32 survivors (lane i takes entry i of keys/ys), with
@@ -278,7 +277,7 @@ inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
 template <bool NEU, bool FULL, bool TOPK, int MODE, bool SMEM_TAB>
 __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, const TabLayout& L, const EvalMeta& M,
                                         const EvalArgs& a, const TopkArgs& tk, const uint64_t* keys,
-                                        const uint32_t* ys, int n, RegList& wl, double& gfloor,
+                                        const uint32_t* ys, int n, RegList& wl, double& gfloor, double& gpend,
                                         const PackMeta& pk) {
   const int lane = threadIdx.x & 31;
   int64_t idx = 0;
@@ -298,6 +297,7 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
     if (a.reason) write_verdict<FULL>(a, idx, v);
   }
   if (TOPK) {  // fused elite: valid survivors offered to this warp's list
+    gfloor = fmax(gfloor, gpend);  // the global floor loaded after the previous offer
     Rec r{v.thr, v.thr, tk.index_base + idx, 0};
     const bool ok = lane < n && v.reason == LS_REASON_NONE && r.key >= gfloor && wl.admits(r.key, r.idx, tk.k);
     if (ok) {
@@ -310,7 +310,8 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
     if (__any_sync(0xffffffffu, ok)) {  // the list may have moved: share / refresh the pruning floor
       const double mine = wl.floor_key(tk.k);
       if (lane == 0 && mine > gfloor) raise_floor(tk.floor, mine);
-      gfloor = fmax(mine, read_floor(tk.floor));
+      gfloor = fmax(gfloor, mine);
+      gpend = read_floor(tk.floor);  // consumed by the next batch: the L2 round trip overlaps other work
     }
   }
 }
@@ -342,7 +343,8 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
   S.qy = reinterpret_cast<uint32_t*>(S.qkey + kGateWarps * kWarpQueue);
   S.mkey = reinterpret_cast<uint64_t*>(S.qy + kGateWarps * kWarpQueue);
   S.my = reinterpret_cast<uint32_t*>(S.mkey + kGateWarps * kSlots * 32);
-  S.lists = reinterpret_cast<uint8_t*>(S.my + kGateWarps * kSlots * 32);
+  S.lists = S.ring;  // end-of-kernel elite merge reuses the drained ring
+  static_assert(kWorkWarps * warp_list_bytes(kFusedK) <= kRingBytes, "elite lists fit in the ring");
   const uint64_t* Gt = SMEM_GATE ? S.gate : gtab;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
   RegList wl;  // this warp's elite list, one entry per lane
   wl.init();
   double gfloor = -1.0e308;  // cached global pruning floor (raw keys are >= 0)
+  double gpend = -1.0e308;   // in-flight read of the global floor
 
   if (warp >= kGateWarps) {  // ---------------- fp64 warps: drain the mailboxes
     const int f = warp - kGateWarps;
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
           const int g = f + kFpWarps * (bit / kSlots), sl = bit % kSlots;
           const int base = (g * kSlots + sl) * 32;
           fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl,
-                                                       gfloor, gm.pk);
+                                                       gfloor, gpend, gm.pk);
           __syncwarp();
           if (lane == 0) {
             atomicAnd((uint32_t*)&mb_pending[f], ~(1u << bit));
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
           atomicOr((uint32_t*)&mb_pending[warp % kFpWarps], 1u << ((warp / kFpWarps) * kSlots + slot));
         }
       } else {
-        fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor, gm.pk);
+        fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, qkey + pos0, qy + pos0, n, wl, gfloor, gpend, gm.pk);
       }
       qcount -= n;
       __syncwarp();
@@ -656,6 +659,8 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 
   if (TOPK) {  // merge the work warps' lists (named barrier: the producer warp is gone)
     Rec* slots = reinterpret_cast<Rec*>(S.lists);
+    // the lists live in the ring: every gate warp must be past its last stage
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
     wl.store(slots + warp * 32, &list_count[warp]);
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
     if (warp == 0) {
