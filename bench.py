@@ -259,13 +259,13 @@ def run_ours(args, rank, world, local_rank):
                 ev_start.append(a)
                 ev_end.append(b)
             recs, count = sweep.merge(recs, count)
-            return recs, count, 3  # our kernels: evaluate, local merge, global merge
+            return recs, count, 2  # our kernels: fused evaluate (+ in-kernel elite merge), cross-rank merge
         _, recs, count = sweep.run(cands, index_base=base, out=out)
         if timed:
             b.record(stream)
             ev_start.append(a)
             ev_end.append(b)
-        return recs, count, 2
+        return recs, count, 1  # one kernel: evaluate + elite, the last CTA merges the CTA lists
 
     for _ in range(args.warmup):
         step(False)
@@ -362,9 +362,9 @@ def run_ours(args, rank, world, local_rank):
                         else "Evaluator.evaluate_host -> ls_evaluate_host")},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved_gbs / pk.get("hbm_gbs"), "traffic": traffic,
-                     "kernel": "eval_ws_kernel<GEN_WORDS> (fused evaluate + elite) + topk_merge_kernel"
+                     "kernel": "eval_ws_kernel<GEN_WORDS> (fused evaluate + elite, last-CTA merge)"
                                if args.format == "packed" else
-                               "eval_ws_kernel (fused evaluate + elite) + topk_merge_kernel", "algorithmic_bytes_per_candidate": algo_bytes,
+                               "eval_ws_kernel (fused evaluate + elite, last-CTA merge)", "algorithmic_bytes_per_candidate": algo_bytes,
                      "kernel_ms_avg": kern_avg, "peak_source": f"{pk_kind} hbm_gbs (MEASURED_PEAKS.json)"},
         "gpu_launches": launches,
         "clocks": clk,

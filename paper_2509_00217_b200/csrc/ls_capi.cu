@@ -551,10 +551,27 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
+// Scratch of the fused evaluate + top-k: per-CTA lists and counts, then the
+// 16 zeroed bytes of the global pruning floor and the finished-CTA counter.
+static TopkArgs fused_topk_args(void* scratch, int64_t grid, int k, int64_t index_base, ls_elite_rec* out,
+                                int32_t* count_out) {
+  TopkArgs tk{};
+  tk.k = k;
+  tk.index_base = index_base;
+  tk.part = static_cast<ls_elite_rec*>(scratch);
+  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
+  tk.floor = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(tk.part_counts + grid) + 15) &
+                                                   ~uintptr_t(15));
+  tk.done = reinterpret_cast<unsigned int*>(tk.floor + 1);
+  tk.out = out;
+  tk.count_out = count_out;
+  return tk;
+}
+
 size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
   if (!c || k < 1) return 0;
-  const size_t lists = (size_t)c->blocks_tma * (size_t)fused_lists_per_cta();
-  const size_t fused = lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4 + 32;
+  const size_t lists = (size_t)c->blocks_tma;
+  const size_t fused = lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4 + 48;
   return std::max(fused, topk_scratch_bytes(n, k, 0));
 }
 
@@ -605,24 +622,16 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   if (k <= fused_k_max() && c->blocks_tma > 0 && tma_eligible(a, c->M.A)) {
     LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
     const int64_t grid = ws_grid(lp, n);
-    const int64_t lists = grid * fused_lists_per_cta();
-    TopkArgs tk{k, index_base, static_cast<ls_elite_rec*>(scratch), nullptr, nullptr};
-    tk.part_counts = reinterpret_cast<int32_t*>(tk.part + lists * k);
-    tk.floor = reinterpret_cast<unsigned long long*>(
-        (reinterpret_cast<uintptr_t>(tk.part_counts + lists) + 7) & ~uintptr_t(7));
+    TopkArgs tk = fused_topk_args(scratch, grid, k, index_base, topk_out, count_out);
     if (n == 0) {
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
       return LS_OK;
     }
-    if ((e = cudaMemsetAsync(tk.floor, 0, sizeof(unsigned long long), s)) != cudaSuccess)
-      return cuda_fail(e, "floor reset");
+    if ((e = cudaMemsetAsync(tk.floor, 0, 16, s)) != cudaSuccess) return cuda_fail(e, "floor reset");
     const PackMeta pk = pack_meta(c->desc);
     if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s,
                                   words ? &pk : nullptr)) != cudaSuccess)
       return cuda_fail(e, "evaluate_topk launch");
-    if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)lists, k, k, tk.floor, topk_out, count_out, s)) !=
-        cudaSuccess)
-      return cuda_fail(e, "topk merge launch");
     return LS_OK;
   }
   if (words) return fail(LS_ERR_UNSUPPORTED, "packed candidates need k <= 32 and 16-byte aligned buffers");
@@ -788,20 +797,12 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   }
   LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
   const int64_t grid = std::min<int64_t>((n + 1023) / 1024, c->blocks_tma);
-  const int64_t lists = grid * fused_lists_per_cta();
-  TopkArgs tk{k, start, static_cast<ls_elite_rec*>(scratch), nullptr, nullptr};
-  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + lists * k);
-  tk.floor = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(tk.part_counts + lists) + 7) &
-                                                   ~uintptr_t(7));
+  TopkArgs tk = fused_topk_args(scratch, grid, k, start, topk_out, count_out);
   cudaError_t e;
-  if ((e = cudaMemsetAsync(tk.floor, 0, sizeof(unsigned long long), s)) != cudaSuccess)
-    return cuda_fail(e, "floor reset");
+  if ((e = cudaMemsetAsync(tk.floor, 0, 16, s)) != cudaSuccess) return cuda_fail(e, "floor reset");
   if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=
       cudaSuccess)
     return cuda_fail(e, "sweep launch");
-  if ((e = launch_topk_merge(tk.part, tk.part_counts, (int)lists, k, k, tk.floor, topk_out, count_out, s)) !=
-      cudaSuccess)
-    return cuda_fail(e, "sweep merge launch");
   return LS_OK;
 }
 

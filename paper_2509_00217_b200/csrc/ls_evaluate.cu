@@ -195,9 +195,11 @@ __device__ __forceinline__ void extract(const uint32_t* w, const uint32_t* q, in
 __device__ __forceinline__ uint32_t word_decode(uint64_t w, const PackMeta& pk, uint32_t& rank, uint32_t& Y) {
   Y = (uint32_t)w & 0xffffffu;
   rank = (uint32_t)(w >> 24) & 0xffffffu;
-  const bool bad = (w >> 48) != 0 || (Y & ~pk.axis_mask) != 0 || (Y & (Y >> 1) & 0x555555u) != 0 ||
-                   rank >= pk.ncoarse;
-  return bad ? 1u : 0u;
+  // branch-free: any bit past the rank, an axis bit past head A, a field of 3,
+  // or rank >= ncoarse (both < 2^24: the sign of ncoarse - 1 - rank)
+  const uint32_t bad = (uint32_t)(w >> 48) | (Y & ~pk.axis_mask) | (Y & (Y >> 1) & 0x555555u) |
+                       ((pk.ncoarse - 1u - rank) & 0x80000000u);
+  return bad != 0 ? 1u : 0u;
 }
 
 // ---- on-device candidate streams (ls_sweep) ----------------------------
@@ -316,6 +318,164 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
   }
 }
 
+// Named barrier 1 over the work warps (gate + fp64; the producer has exited).
+__device__ __forceinline__ void bar_work() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory"); }
+
+// Tree merge of the work warps' register lists through shared slots
+// ([kWorkWarps][32] Rec): log2(kWorkWarps) levels, warp 0 ends with the
+// merged list. Records below the floor (fk, fi) are skipped (at_least()).
+__device__ __forceinline__ void tree_merge(RegList& wl, Rec* slots, int* cnt, int warp, int k, double fk,
+                                           int64_t fi = INT64_MAX) {
+  wl.store(slots + warp * 32, &cnt[warp]);
+  bar_work();
+#pragma unroll 1
+  for (int st = 1; st < kWorkWarps; st <<= 1) {
+    if ((warp & (2 * st - 1)) == 0 && warp + st < kWorkWarps && cnt[warp + st] > 0) {
+      wl.absorb(slots + (warp + st) * 32, cnt[warp + st], k, fk, fi);
+      wl.store(slots + warp * 32, &cnt[warp]);
+    }
+    bar_work();
+  }
+}
+
+// Final merge of the gridDim.x CTA lists by the last CTA's work warps: lists
+// are staged into shared memory a window at a time (one round of coalesced
+// L2 loads for the counts, one for the records) and cut by the exact
+// (key, index) floor. When everything fits in one window the top-k is
+// selected by k rounds of block-wide argmax; otherwise every warp offers its share to its own list and
+// the warp lists tree-merge into tk.out.
+__device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt, int warp, const TopkArgs& tk) {
+  constexpr int kThr = 32 * kWorkWarps;
+  const int lane = threadIdx.x & 31, tid = warp * 32 + lane, k = tk.k, m = (int)gridDim.x;
+  Rec* slots = reinterpret_cast<Rec*>(smem);  // [kWorkWarps][32]
+  int* wcnt = reinterpret_cast<int*>(smem + kWorkWarps * 32 * sizeof(Rec));
+  Rec* win = reinterpret_cast<Rec*>(smem + kWorkWarps * 32 * sizeof(Rec) + 512 * sizeof(int));
+  const int cap = (int)((kRingBytes - kWorkWarps * 32 * sizeof(Rec) - 512 * sizeof(int)) / sizeof(Rec));
+  const int lists_per_win = cap / k < 512 ? cap / k : 512;
+  __shared__ double s_fk[kWorkWarps];
+  __shared__ int64_t s_fi[kWorkWarps];
+  __shared__ int s_slot[kWorkWarps];
+  double fk = read_floor(tk.floor);
+  int64_t fi = INT64_MAX;
+  wl.init();
+  for (int l0 = 0; l0 < m; l0 += lists_per_win) {
+    const int nl = m - l0 < lists_per_win ? m - l0 : lists_per_win;
+    for (int i = tid; i < nl; i += kThr) wcnt[i] = __ldcg(tk.part_counts + l0 + i);
+    bar_work();
+    for (int i = tid; i < nl * k; i += kThr) {
+      const int l = i / k, j = i - l * k;
+      Rec r{-1.0e308, 0.0, INT64_MAX, 0};
+      if (j < wcnt[l]) {
+        const ls_elite_rec* e = tk.part + (int64_t)(l0 + l) * k + j;
+        const double2 kr = __ldcg(reinterpret_cast<const double2*>(e));
+        const longlong2 ic = __ldcg(reinterpret_cast<const longlong2*>(e) + 1);
+        r = Rec{kr.x, kr.y, (int64_t)ic.x, (uint64_t)ic.y};
+      }
+      win[i] = r;
+    }
+    bar_work();
+    // exact (key, index) floor: the best k-th entry of any full list (ties on
+    // the key are common — equivalent strategies — and a key-only floor
+    // would let them all through to the serial inserts)
+    for (int l = tid; l < nl; l += kThr)
+      if (wcnt[l] >= k) {
+        const Rec& e = win[l * k + k - 1];
+        if (better(e.key, e.idx, fk, fi)) {
+          fk = e.key;
+          fi = e.idx;
+        }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, fk, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, fi, o);
+      if (better(ok, oi, fk, fi)) {
+        fk = ok;
+        fi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_fk[warp] = fk;
+      s_fi[warp] = fi;
+    }
+    bar_work();
+    for (int o = 0; o < kWorkWarps; ++o)
+      if (better(s_fk[o], s_fi[o], fk, fi)) {
+        fk = s_fk[o];
+        fi = s_fi[o];
+      }
+    if (nl == m) {
+      // every list is staged: k rounds of a block-wide argmax over the
+      // records at least as good as the floor; each round emits the best
+      // remaining record and retires every record of the same vector
+      // (dedupe), so the output is the top-k distinct vectors by best
+      // occurrence, in order — no serial inserts
+      const int total = nl * k;
+      for (int i = tid; i < total; i += kThr)
+        if (!at_least(win[i].key, win[i].idx, fk, fi)) win[i].key = -1.0e308;  // retired
+      bar_work();
+      int emitted = 0;
+      for (int r = 0; r < k; ++r) {
+        double bk = -1.0e308;
+        int64_t bi = INT64_MAX;
+        int bs = -1;
+        for (int i = tid; i < total; i += kThr)
+          if (win[i].key != -1.0e308 && better(win[i].key, win[i].idx, bk, bi)) {
+            bk = win[i].key;
+            bi = win[i].idx;
+            bs = i;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+          if (better(ok, oi, bk, bi)) {
+            bk = ok;
+            bi = oi;
+            bs = os;
+          }
+        }
+        if (lane == 0) {
+          s_fk[warp] = bk;
+          s_fi[warp] = bi;
+          s_slot[warp] = bs;
+        }
+        bar_work();
+        for (int o = 0; o < kWorkWarps; ++o)
+          if (better(s_fk[o], s_fi[o], bk, bi)) {
+            bk = s_fk[o];
+            bi = s_fi[o];
+            bs = s_slot[o];
+          }
+        if (bs < 0) break;  // block-uniform: nothing left
+        const Rec best = win[bs];
+        if (tid == 0) tk.out[r] = ls_elite_rec{best.key, best.raw, best.idx, best.code};
+        ++emitted;
+        bar_work();  // everyone has read win[bs] before it is retired
+        for (int i = tid; i < total; i += kThr)
+          if (win[i].code == best.code) win[i].key = -1.0e308;
+        bar_work();
+      }
+      if (tid == 0) *tk.count_out = emitted;
+      return;
+    }
+    for (int b = warp * 32; b < nl * k; b += kThr) {
+      const int i = b + lane;
+      Rec r{0.0, 0.0, 0, 0};
+      bool have = false;
+      if (i < nl * k) {
+        r = win[i];
+        have = at_least(r.key, r.idx, fk, fi);  // unused slots carry -inf
+      }
+      wl.offer(have, r, k);
+    }
+    bar_work();
+  }
+  tree_merge(wl, slots, cnt, warp, k, fk, fi);
+  if (warp == 0) wl.emit(tk.out, tk.count_out);
+}
+
 template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK, int MODE>
 __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     eval_ws_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const EvalArgs a,
@@ -343,8 +503,9 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
   S.qy = reinterpret_cast<uint32_t*>(S.qkey + kGateWarps * kWarpQueue);
   S.mkey = reinterpret_cast<uint64_t*>(S.qy + kGateWarps * kWarpQueue);
   S.my = reinterpret_cast<uint32_t*>(S.mkey + kGateWarps * kSlots * 32);
-  S.lists = S.ring;  // end-of-kernel elite merge reuses the drained ring
-  static_assert(kWorkWarps * warp_list_bytes(kFusedK) <= kRingBytes, "elite lists fit in the ring");
+  S.lists = S.ring;  // end-of-kernel elite merges reuse the drained ring
+  static_assert(kWorkWarps * 32 * sizeof(Rec) + 512 * sizeof(int) + 64 * sizeof(Rec) <= kRingBytes,
+                "elite slots and a merge window fit in the ring");
   const uint64_t* Gt = SMEM_GATE ? S.gate : gtab;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -508,10 +669,9 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
       // then compact the survivors (~1% of a uniform batch) into the warp
       // queue: the lane's survivor count 0..4 as three ballots gives every
       // lane its queue position and the warp total in one step
-      uint32_t sv = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sv |= (j < count && reason[j] == LS_REASON_NONE) ? 1u << j : 0u;
-      const uint32_t nsv = __popc(sv);
+      // survivors = zero reason bytes of r4 (SWAR), within the lane's count
+      const uint32_t zb = __vcmpeq4(r4, 0u) & (count >= 4 ? 0xffffffffu : (1u << (8 * count)) - 1u);
+      const uint32_t nsv = __popc(zb) >> 3;
       const uint32_t b0 = __ballot_sync(0xffffffffu, nsv & 1u), b1 = __ballot_sync(0xffffffffu, nsv & 2u),
                      b2 = __ballot_sync(0xffffffffu, nsv & 4u);
       if (b0 | b1 | b2) {
@@ -519,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         int pos = qcount + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (sv & (1u << j)) {
+          if (zb & (1u << (8 * j))) {
             qkey[pos] = (MODE == GEN_WORDS && !FULL) ? (uint64_t)(base + j) | ((uint64_t)ranks[j] << 40)
                                                      : pack_key(base + j, cs[j]);
             qy[pos] = cs[j].Y;
@@ -657,18 +817,40 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     }
   }
 
-  if (TOPK) {  // merge the work warps' lists (named barrier: the producer warp is gone)
+  if (TOPK) {
+    // (named barrier 1 over the work warps: the producer warp is gone)
     Rec* slots = reinterpret_cast<Rec*>(S.lists);
     // the lists live in the ring: every gate warp must be past its last stage
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
+    bar_work();
+    const double fl = read_floor(tk.floor);  // global floor so far: most entries are already beaten
+#ifdef LS_DIAG_SERIAL
     wl.store(slots + warp * 32, &list_count[warp]);
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory");
-    if (warp == 0) {
-      const double fl = read_floor(tk.floor);  // global floor so far: most entries are already beaten
+    bar_work();
+    if (warp == 0)
       for (int o = 1; o < kWorkWarps; ++o) wl.absorb(slots + o * 32, list_count[o], tk.k, fl);
+#else
+    tree_merge(wl, slots, list_count, warp, tk.k, fl);
+#endif
+    __shared__ int s_last;
+    if (warp == 0) {
       wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
+      __threadfence();  // this CTA's list is visible device-wide before it is counted
+      unsigned t = 0;
+      if (lane == 0) t = atomicAdd(tk.done, 1u);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (lane == 0) s_last = t == gridDim.x - 1;
     }
-  }}
+    bar_work();
+#ifdef LS_DIAG_NOFINAL
+    if (false) {
+#else
+    if (s_last) {  // the last CTA merges every CTA's list (L2-resident, no second launch)
+#endif
+      __threadfence();
+      final_merge(wl, S.ring, list_count, warp, tk);
+    }
+  }
+}
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
 template <bool NEU>
@@ -856,7 +1038,6 @@ int64_t ws_grid(const LaunchPlan& lp, int64_t n) {
 }
 
 int fused_k_max() { return kFusedK; }
-int fused_lists_per_cta() { return 1; }
 
 cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
                         cudaStream_t s) {

@@ -126,28 +126,21 @@ __device__ __forceinline__ uint32_t gate(const uint64_t* G, const TabLayout& L, 
   return reason;
 }
 
-// Raw-mode gate (no memory_bytes output): the coarse word of (t, e, p, b)
-// carries the same three gates, OOM precomputed for both attention layouts.
+// Raw-mode gate (no memory_bytes output) from a coarse word: the static
+// reason of the candidate's attention layout, unless the budget passed and an
+// axis field is inadmissible (a layout error, gate order of simulator.py:257-284).
+__device__ __forceinline__ uint32_t coarse_reason(uint32_t cw, uint32_t Y, uint32_t a2) {
+  const uint32_t rs = (cw >> (COARSE_RS_SHIFT + 2 * a2)) & 3u;
+  return ((Y & cw & GATE_FIELDS) != 0 && rs != LS_REASON_OVER_DEVICE_BUDGET) ? (uint32_t)LS_REASON_LAYOUT_ERROR : rs;
+}
 __device__ __forceinline__ uint32_t gate_coarse(const uint32_t* C, const TabLayout& L, const EvalMeta& M,
                                                 const Decoded& c) {
-  const uint32_t cw = C[((c.t * L.ne + c.e) * L.np + c.p) * L.nb + c.b];
-  const uint32_t a2 = attn_dim1(M, c.Y);
-  const bool over = (cw & GATE_BUDGET) != 0;
-  const bool bad = ((c.Y & cw & GATE_FIELDS) | (cw & (GATE_PINNED | GATE_LAYOUT))) != 0;
-  const bool oom = (cw & (GATE_OOM0 << a2)) != 0;
-  return over ? LS_REASON_OVER_DEVICE_BUDGET
-              : (bad ? LS_REASON_LAYOUT_ERROR : (oom ? LS_REASON_OOM : LS_REASON_NONE));
+  return coarse_reason(C[((c.t * L.ne + c.e) * L.np + c.p) * L.nb + c.b], c.Y, attn_dim1(M, c.Y));
 }
 
 // Same, from the coarse rank ((t*ne + e)*np + p)*nb + b directly.
 __device__ __forceinline__ uint32_t gate_rank(const uint32_t* C, const EvalMeta& M, uint32_t rank, uint32_t Y) {
-  const uint32_t cw = C[rank];
-  const uint32_t a2 = attn_dim1(M, Y);
-  const bool over = (cw & GATE_BUDGET) != 0;
-  const bool bad = ((Y & cw & GATE_FIELDS) | (cw & (GATE_PINNED | GATE_LAYOUT))) != 0;
-  const bool oom = (cw & (GATE_OOM0 << a2)) != 0;
-  return over ? LS_REASON_OVER_DEVICE_BUDGET
-              : (bad ? LS_REASON_LAYOUT_ERROR : (oom ? LS_REASON_OOM : LS_REASON_NONE));
+  return coarse_reason(C[rank], Y, attn_dim1(M, Y));
 }
 
 // fp64 pass for a candidate that passed gate(). T: the full table (global).

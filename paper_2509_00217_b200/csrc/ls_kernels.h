@@ -26,13 +26,17 @@ struct LaunchPlan {
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
 
 // Fused evaluate + top-k by raw (eval_ws_kernel<..., TOPK>): every CTA emits
-// its elite list to part[blockIdx.x * k ..] / part_counts[blockIdx.x].
+// its elite list to part[blockIdx.x * k ..] / part_counts[blockIdx.x]; the
+// last CTA to finish merges them into out / count_out.
 struct TopkArgs {
   int k;
   int64_t index_base;
   ls_elite_rec* part;
   int32_t* part_counts;
   unsigned long long* floor;  // device word, zeroed before launch
+  unsigned int* done;         // CTAs finished (zeroed before launch): the last one merges every CTA list
+  ls_elite_rec* out;          // final top-k and its count
+  int32_t* count_out;
 };
 
 // Candidate sources of eval_ws_kernel.
@@ -71,7 +75,6 @@ cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_
                         cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n);
 int fused_k_max();
-int fused_lists_per_cta();  // elite lists one eval_ws_kernel CTA emits (TOPK)
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
                                  const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s,
                                  const PackMeta* pk = nullptr);

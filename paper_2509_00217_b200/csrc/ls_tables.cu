@@ -69,16 +69,22 @@ __device__ double ws_mem(const ls_workload_desc& d, int64_t b) {
   return ((2.0 * (double)b) * (double)(d.hidden_dim + d.ffn_dim)) * (double)d.dtype_bytes;
 }
 
-// Coarse gate word of one (t, e, p, b): the gate bits plus OOM outcomes for
-// both attention layouts, with gate()'s expression (w + kv) + ws > capacity.
+// Coarse gate word of one (t, e, p, b) (COARSE_RS_SHIFT): the axis-field bits
+// and, per attention layout, the static reason in gate order; the OOM test is
+// gate()'s expression (w + kv) + ws > capacity.
 __device__ uint32_t coarse_word(const ls_workload_desc& d, const TabLayout& L, int c) {
   const int b = c % L.nb, p = (c / L.nb) % L.np, e = (c / (L.nb * L.np)) % L.ne, t = c / (L.nb * L.np * L.ne);
   const int64_t TP = d.domain[0][t], EP = d.domain[1][e], PP = d.domain[2][p], B = d.domain[3][b];
-  uint32_t g = gate_bits(d, TP, EP, PP);
+  const uint32_t g = gate_bits(d, TP, EP, PP);
   const double w = weights_mem(d, TP, EP, PP), ws = ws_mem(d, B);
-  if ((w + kv_mem(d, TP, PP, B, false)) + ws > d.hbm_capacity) g |= GATE_OOM0;
-  if ((w + kv_mem(d, TP, PP, B, true)) + ws > d.hbm_capacity) g |= GATE_OOM1;
-  return g;
+  const bool oom0 = (w + kv_mem(d, TP, PP, B, false)) + ws > d.hbm_capacity;
+  const bool oom1 = (w + kv_mem(d, TP, PP, B, true)) + ws > d.hbm_capacity;
+  auto rs = [&](bool oom) -> uint32_t {
+    if (g & GATE_BUDGET) return LS_REASON_OVER_DEVICE_BUDGET;
+    if (g & (GATE_PINNED | GATE_LAYOUT)) return LS_REASON_LAYOUT_ERROR;
+    return oom ? LS_REASON_OOM : LS_REASON_NONE;
+  };
+  return (g & GATE_FIELDS) | rs(oom0) << COARSE_RS_SHIFT | rs(oom1) << (COARSE_RS_SHIFT + 2);
 }
 
 __device__ uint64_t table_word(const ls_workload_desc& d, const TabLayout& L, int w) {

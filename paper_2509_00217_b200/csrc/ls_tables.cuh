@@ -46,14 +46,16 @@ enum : uint32_t {
   GATE_FIELDS = 0x00ffffffu,  // 12 axis fields x {DIM0, DIM1}
   GATE_PINNED = 1u << 24,     // a pinned (uncontrolled) op is a layout error at this tp
   GATE_LAYOUT = 1u << 25,     // pp does not divide num_layers, or ep vs num_experts
-  GATE_BUDGET = 1u << 26,     // tp * ep * pp > device_budget
-  GATE_OOM0 = 1u << 27,       // memory > capacity with attn_core not on DIM1 (coarse words only)
-  GATE_OOM1 = 1u << 28        // memory > capacity with attn_core on DIM1 (coarse words only)
+  GATE_BUDGET = 1u << 26      // tp * ep * pp > device_budget
 };
 
-// Coarse gate words: one uint32 per (t, e, p, b) = the (t, e, p) gate bits plus
-// both memory-gate outcomes, so a raw-mode gate is one shared-memory load and
-// a few bit tests. Built only when the coarse space is small enough to stage.
+// Coarse gate words: one uint32 per (t, e, p, b) = the 24 axis-field bits of
+// the (t, e, p) entry plus, for each attention layout (attn_core on DIM1 or
+// not), the reason the candidate-independent gates give in the reference's
+// order — over budget (1), pinned-op / pp / ep layout error (2), OOM (3) or
+// none (0) — so a raw-mode gate is one shared-memory load, one field test and
+// one select. Built only when the coarse space is small enough to stage.
+enum : uint32_t { COARSE_RS_SHIFT = 24 };  // 2-bit static reason at 24 (attn not DIM1) and 26 (DIM1)
 constexpr int kCoarseMax = 6144;
 
 // Offsets (in 8-byte words) of every table segment inside one buffer.

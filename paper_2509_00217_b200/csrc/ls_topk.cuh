@@ -345,7 +345,9 @@ __device__ __forceinline__ void raise_floor(unsigned long long* floor, double k_
 }
 __device__ __forceinline__ double read_floor(const unsigned long long* floor) {
   if (!floor) return -1.0e308;
-  return __longlong_as_double((long long)*reinterpret_cast<const volatile unsigned long long*>(floor));
+  unsigned long long v;  // relaxed, GPU scope (a volatile load would be a system-scope strong load)
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(floor) : "memory");
+  return __longlong_as_double((long long)v);
 }
 
 // Bytes of one WarpList of capacity cap.
