@@ -62,7 +62,7 @@ def _elite_by_raw(wl, vectors, k, base=0):
     ("dsv3_style_h100x256", 3, 1_500_000, 7_777),
     ("edge_odd", 2, 364_500, 0),  # the whole space: 5*5*4*5 coarse x 3^6 axes
 ])
-@pytest.mark.parametrize("k", [1, 8])
+@pytest.mark.parametrize("k", [1, 8, 32])  # k = 32 over a full grid: the windowed last-CTA merge
 def test_sweep_matches_sequential_elite(name, mode, n, start, k, make_ev):
     from paper_2509_00217_b200.generator import stream_vectors
 
