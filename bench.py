@@ -11,7 +11,8 @@ so inputs (16 B/candidate, ~2 GB) dwarf the 126 MB L2 — no flush needed.
 One step = the hot path over one batch:
   evaluate (reason + raw throughput per candidate, HBM SoA in/out)
   -> device top-k by raw over distinct vectors (elite of the batch)
-  -> (N > 1) NCCL all-gather of the per-rank top-k + device merge.
+  -> (N > 1) one NCCL all-gather of the per-rank top-k (records + count) and
+     a device merge.
 
 Also reported: ``e2e`` — the same metric through the public API with HOST
 buffers (Evaluator.evaluate_host -> ls_evaluate_host: pinned H2D of the
@@ -354,7 +355,7 @@ def run_ours(args, rank, world, local_rank):
                                f"{n} per GPU per step, " + ("packed 8-byte candidate words" if args.format == "packed"
                                                              else "SoA uint8 planes") + " in HBM",
                    "format": args.format,
-                   "candidates_per_gpu": n, "elite_k": ELITE_K, "parallelism": f"dp{world} (index-range shards)",
+                   "candidates_per_gpu": n, "elite_k": ELITE_K, "parallelism": f"dp{world} (index-range shards)", "elite_exchange": sweep.transport,
                    "l2": f"inputs {ALGO_BYTES[args.format] - 9} B x n per GPU >> 126 MB L2; no flush"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * in_bytes,
                 "d2h_bytes_per_step": world * e2e_n * 9, "candidates_per_gpu": e2e_n,

@@ -243,6 +243,21 @@ int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int
  * into the global top-k with the same ordering and dedupe rule. */
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                   ls_elite_rec* out, int32_t* count_out, void* stream);
+/* Cross-rank elite exchange over peer memory (NVLink / NVSwitch), fused with
+ * the merge — the device-side replacement of "all-gather the per-rank top-k,
+ * then ls_topk_merge". Every rank owns a symmetric buffer
+ * of ls_elite_exchange_bytes(world, k) bytes, zeroed before first use, whose
+ * base addresses on all ranks are in the device array peer_bases[world]
+ * (e.g. torch symmetric memory). Each call pushes `block` ((k + 1) x 32 B: k
+ * ls_elite_rec rows, the int32 count at the start of row k) into slot `rank`
+ * of every buffer as 8-byte stores that carry `seq` (1, 2, ... — one per
+ * call, the same on all ranks) beside each 4-byte data word, waits until all
+ * ranks' words of this call have arrived (bounded by about a second; then
+ * *count_out = -1) and writes the merged top-k. world <= 8, k <= 32. Single
+ * CTA, stream-ordered. */
+size_t ls_elite_exchange_bytes(int world, int k);
+int ls_elite_exchange(const void* block, const uint64_t* peer_bases, void* local_base, int rank, int world, int k,
+                      uint32_t seq, ls_elite_rec* out, int32_t* count_out, void* stream);
 /* ls_evaluate_topk over packed words (fused path only: k <= 32). */
 int ls_evaluate_packed_topk(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
                             int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,

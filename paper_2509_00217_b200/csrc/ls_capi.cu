@@ -658,6 +658,26 @@ int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge launch");
 }
 
+size_t ls_elite_exchange_bytes(int world, int k) {
+  if (world < 1 || world > 8 || k < 1 || k > 32) return 0;
+  return elite_exchange_bytes(world, k);
+}
+
+int ls_elite_exchange(const void* block, const uint64_t* peer_bases, void* local_base, int rank, int world, int k,
+                      uint32_t seq, ls_elite_rec* out, int32_t* count_out, void* stream) {
+  g_err.clear();
+  if (!block || !peer_bases || !local_base || !out || !count_out || world < 1 || world > 8 || rank < 0 ||
+      rank >= world || k < 1 || k > 32 || seq == 0)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad elite_exchange arguments");
+  int dev = 0, mhz = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mhz, cudaDevAttrClockRate, dev);  // kHz
+  const long long timeout = (long long)(mhz > 0 ? mhz : 2000000) * 1000LL;  // ~1 s of SM cycles
+  cudaError_t e = launch_elite_exchange(block, peer_bases, local_base, rank, world, k, seq, timeout, out, count_out,
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "elite_exchange launch");
+}
+
 int ls_env_step(ls_ctx* c, const ls_search_state* st, const int64_t* action, double* reward_out, void* stream) {
   g_err.clear();
   if (!c || !st || !action || !reward_out) return fail(LS_ERR_INVALID_ARGUMENT, "null env_step argument");

@@ -105,6 +105,12 @@ cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, i
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);
 
+// Cross-rank elite exchange over peer memory (ls_exchange.cu)
+size_t elite_exchange_bytes(int world, int k);
+cudaError_t launch_elite_exchange(const void* block, const uint64_t* peer_bases, void* local_base, int rank,
+                                  int world, int k, uint32_t seq, long long timeout_cycles, ls_elite_rec* out,
+                                  int32_t* count_out, cudaStream_t s);
+
 // Search-loop environment step (ls_search.cu)
 cudaError_t launch_env_step(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
                             const ls_search_state& S, const int64_t* action, double* reward_out, cudaStream_t s);

@@ -221,6 +221,8 @@ class Evaluator:
 
     def decode_records(self, recs: torch.Tensor, count: torch.Tensor) -> list[Elite]:
         n = int(count.item())
+        if n < 0:
+            raise RuntimeError("elite exchange timed out: a peer rank never published its block")
         raw = recs[:n].cpu().numpy().view(np.dtype([("key", "<f8"), ("raw", "<f8"), ("index", "<i8"), ("code", "<u8")]))
         raw = raw.reshape(-1)
         vecs = codes_to_vectors(raw["code"], self.space) if n else np.zeros((0, self.vector_length), np.int64)
