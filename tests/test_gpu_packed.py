@@ -104,3 +104,21 @@ def test_ragged_sizes_match_planes(n, ev_factory):
     assert [(e.vector, e.index, e.raw) for e in got] == [(e.vector, e.index, e.raw) for e in want]
     _, r3, c3 = ev.evaluate_packed_topk(words, k=8, index_base=7, verdicts=False)
     assert [e.index for e in ev.decode_records(r3, c3)] == [e.index for e in want]
+
+
+@pytest.mark.parametrize("n", [4, 4096, 4098, 100_003])
+def test_pack_vectorised_path_and_tail(n, ev_factory):
+    """ls_pack's 4-per-thread path (4-byte aligned planes, stride % 4 == 0)
+    plus the per-candidate tail equal the host packing, malformed heads
+    included."""
+    wl, meta, data = load_eval("moe_1p2t")
+    ev = ev_factory(wl)
+    rng = np.random.default_rng(n)
+    vecs = rng.integers(0, 4, size=(n, wl.space.vector_length))
+    vecs[:, :4] = np.stack([rng.integers(0, k + 1, size=n) for k in wl.space.head_sizes[:4]], axis=1)
+    width = (n + 3) // 4 * 4 + 4  # stride % 4 == 0 with n % 4 != 0 for the odd sizes
+    big = np.zeros((wl.space.vector_length, width), dtype=np.uint8)
+    big[:, :n] = vecs.T
+    planes = torch.from_numpy(big).cuda()[:, :n]
+    dev = ev.pack(planes).cpu().numpy().view(np.uint64)
+    np.testing.assert_array_equal(dev, pack_vectors(vecs, wl.space))
