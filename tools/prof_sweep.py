@@ -1,0 +1,34 @@
+"""On-device stream sweeps (0 B of candidate input) for timing and ncu.
+
+    python tools/prof_sweep.py [--config moe_1p2t_h100] [--mode 3] [--n 0 (= whole stream)] [--reps 3]
+mode 1 = uniform, 2 = full enumeration, 3 = admissible-axis enumeration.
+"""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2509_00217_b200.config import load_workload  # noqa: E402
+from paper_2509_00217_b200.evaluator import Evaluator  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="moe_1p2t_h100")
+ap.add_argument("--mode", type=int, default=3)
+ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--k", type=int, default=8)
+args = ap.parse_args()
+ev = Evaluator(load_workload(args.config), device=0)
+n = args.n or (ev.stream_size(args.mode) if args.mode != 1 else 1 << 30)
+for _ in range(args.reps):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    recs, count = ev.sweep(args.mode, n, k=args.k)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    print(f"sweep mode {args.mode} n={n}: {ms:.3f} ms  {n / ms / 1e6:.2f} G evals/s", flush=True)
+best = ev.decode_records(recs, count)[0]
+print("best", best.vector, best.raw, best.index)
