@@ -32,6 +32,19 @@ namespace ls {
 
 namespace {
 
+#ifdef LS_DIAG_TIMES
+// diagnostic build only: per-CTA phase stamps (globaltimer ns), read by ls_diag_times()
+__device__ unsigned long long g_diag_t[1024][16];
+__device__ __forceinline__ void diag_stamp(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_diag_t[blockIdx.x & 1023][slot] = t;
+}
+#define LS_STAMP(slot) diag_stamp(slot)
+#else
+#define LS_STAMP(slot) ((void)0)
+#endif
+
 // Role counts and ring size (LS_* overrides are for tuning builds only).
 #ifndef LS_GATE_WARPS
 #define LS_GATE_WARPS 16
@@ -338,12 +351,114 @@ __device__ __forceinline__ void tree_merge(RegList& wl, Rec* slots, int* cnt, in
   }
 }
 
+// Exact warp argmax of (key desc, index asc) over the lanes with have set, in
+// a handful of REDUX steps instead of a shuffle butterfly: keys are raws
+// (finite, > 0), so their IEEE bit patterns order like their values; the
+// index (>= 0, unique per record) breaks key ties. Returns the winning lane,
+// or -1 when no lane has a record.
+__device__ __forceinline__ int warp_argbest(bool have, double key, int64_t idx) {
+  constexpr unsigned kAll = 0xffffffffu;
+  unsigned c = __ballot_sync(kAll, have);
+  if (!c) return -1;
+  const unsigned long long kb = (unsigned long long)__double_as_longlong(key);
+  const unsigned hi = have ? (unsigned)(kb >> 32) : 0u;
+  const unsigned mh = __reduce_max_sync(kAll, hi);
+  const bool in1 = have && hi == mh;
+  const unsigned lo = in1 ? (unsigned)kb : 0u;
+  const unsigned ml = __reduce_max_sync(kAll, lo);
+  const bool in2 = in1 && lo == ml;
+  c = __ballot_sync(kAll, in2);
+  if (__popc(c) == 1) return __ffs(c) - 1;
+  const unsigned ih = in2 ? (unsigned)((unsigned long long)idx >> 32) : 0xffffffffu;
+  const unsigned mih = __reduce_min_sync(kAll, ih);
+  const bool in3 = in2 && ih == mih;
+  const unsigned il = in3 ? (unsigned)idx : 0xffffffffu;
+  const unsigned mil = __reduce_min_sync(kAll, il);
+  return __ffs(__ballot_sync(kAll, in3 && il == mil)) - 1;
+}
+
+// One warp merges m staged lists (win[l * stride + j], j < wcnt[l], each
+// best-first and free of duplicate vectors) by repeated argmax over the list
+// heads: lane l & 31 owns list l and keeps the best head of its lists in
+// registers; the winner is emitted unless its vector already was (its best
+// occurrence came first), and only the owner lane re-reads its heads.
+// k <= 32: lane j holds the code of the j-th emitted record for the dedupe.
+__device__ __forceinline__ void warp_merge_lists(const Rec* win, int stride, const int* wcnt, int m, int k,
+                                                 ls_elite_rec* out, int32_t* count_out, int* cur, double* hk,
+                                                 int64_t* hx, bool stamp = false) {
+  const int lane = threadIdx.x & 31;
+  // list heads as shared SoA (key, index): a rescan is independent loads
+  for (int l = lane; l < m; l += 32) {
+    cur[l] = 0;
+    const bool h = wcnt[l] > 0;
+    hk[l] = h ? win[l * stride].key : -1.0e308;
+    hx[l] = h ? win[l * stride].idx : INT64_MAX;
+  }
+  __syncwarp();
+  double bk = -1.0e308;
+  int64_t bi = INT64_MAX;
+  int bl = -1;
+  auto rescan = [&]() {
+    bk = -1.0e308;
+    bi = INT64_MAX;
+    bl = -1;
+#pragma unroll 4
+    for (int l = lane; l < m; l += 32) {
+      const double k_ = hk[l];
+      const int64_t i_ = hx[l];
+      if (k_ != -1.0e308 && (bl < 0 || better(k_, i_, bk, bi))) {
+        bk = k_;
+        bi = i_;
+        bl = l;
+      }
+    }
+  };
+  rescan();
+  if (lane == 0 && stamp) LS_STAMP(9);
+  uint64_t mine = 0;
+  int emitted = 0;
+#ifdef LS_DIAG_TIMES
+  int rounds = 0;
+#endif
+  while (emitted < k) {
+#ifdef LS_DIAG_TIMES
+    ++rounds;
+#endif
+    const int win_lane = warp_argbest(bl >= 0, bk, bi);
+    if (win_lane < 0) break;  // every list is exhausted (warp-uniform)
+    const int wl = __shfl_sync(0xffffffffu, bl, win_lane);
+    const Rec r = win[wl * stride + cur[wl]];
+    if (!__any_sync(0xffffffffu, lane < emitted && mine == r.code)) {
+      if (lane == emitted) mine = r.code;
+      if (lane == 0) out[emitted] = ls_elite_rec{r.key, r.raw, r.idx, r.code};
+      ++emitted;
+    }
+    __syncwarp();
+    if ((wl & 31) == lane) {  // the owner lane advances list wl and rescans its lists
+      const int c = cur[wl] + 1;
+      cur[wl] = c;
+      const bool h = c < wcnt[wl];
+      hk[wl] = h ? win[wl * stride + c].key : -1.0e308;
+      hx[wl] = h ? win[wl * stride + c].idx : INT64_MAX;
+      rescan();
+    }
+    __syncwarp();
+  }
+  if (lane == 0) *count_out = emitted;
+#ifdef LS_DIAG_TIMES
+  if (lane == 0 && stamp) {
+    LS_STAMP(10);
+    g_diag_t[blockIdx.x & 1023][11] = rounds;
+  }
+#endif
+}
+
 // Final merge of the gridDim.x CTA lists by the last CTA's work warps: lists
 // are staged into shared memory a window at a time (one round of coalesced
-// L2 loads for the counts, one for the records) and cut by the exact
-// (key, index) floor. When everything fits in one window the top-k is
-// selected by k rounds of block-wide argmax; otherwise every warp offers its share to its own list and
-// the warp lists tree-merge into tk.out.
+// L2 loads for the counts, one for the records). When everything fits in one
+// window a single warp merges the lists (warp_merge_lists); otherwise the
+// window is cut by the exact (key, index) floor, every warp offers its share
+// to its own list and the warp lists tree-merge into tk.out.
 __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt, int warp, const TopkArgs& tk) {
   constexpr int kThr = 32 * kWorkWarps;
   const int lane = threadIdx.x & 31, tid = warp * 32 + lane, k = tk.k, m = (int)gridDim.x;
@@ -354,8 +469,7 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
   const int lists_per_win = cap / k < 512 ? cap / k : 512;
   __shared__ double s_fk[kWorkWarps];
   __shared__ int64_t s_fi[kWorkWarps];
-  __shared__ int s_slot[kWorkWarps];
-  double fk = read_floor(tk.floor);
+  double fk = m <= lists_per_win ? 0.0 : read_floor(tk.floor);
   int64_t fi = INT64_MAX;
   wl.init();
   for (int l0 = 0; l0 < m; l0 += lists_per_win) {
@@ -374,6 +488,16 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
       win[i] = r;
     }
     bar_work();
+    if (nl == m) {  // every list is staged: one warp merges them, no block-wide rounds
+      if (tid == 0) LS_STAMP(8);
+      if (warp == 0) {  // scratch for the heads: the (unused) warp-slot area
+        int* cur = reinterpret_cast<int*>(slots);
+        double* hk = reinterpret_cast<double*>(smem + 512 * sizeof(int));
+        int64_t* hx = reinterpret_cast<int64_t*>(smem + 512 * (sizeof(int) + sizeof(double)));
+        warp_merge_lists(win, k, wcnt, m, k, tk.out, tk.count_out, cur, hk, hx, true);
+      }
+      return;
+    }
     // exact (key, index) floor: the best k-th entry of any full list (ties on
     // the key are common — equivalent strategies — and a key-only floor
     // would let them all through to the serial inserts)
@@ -404,62 +528,6 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
         fk = s_fk[o];
         fi = s_fi[o];
       }
-    if (nl == m) {
-      // every list is staged: k rounds of a block-wide argmax over the
-      // records at least as good as the floor; each round emits the best
-      // remaining record and retires every record of the same vector
-      // (dedupe), so the output is the top-k distinct vectors by best
-      // occurrence, in order — no serial inserts
-      const int total = nl * k;
-      for (int i = tid; i < total; i += kThr)
-        if (!at_least(win[i].key, win[i].idx, fk, fi)) win[i].key = -1.0e308;  // retired
-      bar_work();
-      int emitted = 0;
-      for (int r = 0; r < k; ++r) {
-        double bk = -1.0e308;
-        int64_t bi = INT64_MAX;
-        int bs = -1;
-        for (int i = tid; i < total; i += kThr)
-          if (win[i].key != -1.0e308 && better(win[i].key, win[i].idx, bk, bi)) {
-            bk = win[i].key;
-            bi = win[i].idx;
-            bs = i;
-          }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-          if (better(ok, oi, bk, bi)) {
-            bk = ok;
-            bi = oi;
-            bs = os;
-          }
-        }
-        if (lane == 0) {
-          s_fk[warp] = bk;
-          s_fi[warp] = bi;
-          s_slot[warp] = bs;
-        }
-        bar_work();
-        for (int o = 0; o < kWorkWarps; ++o)
-          if (better(s_fk[o], s_fi[o], bk, bi)) {
-            bk = s_fk[o];
-            bi = s_fi[o];
-            bs = s_slot[o];
-          }
-        if (bs < 0) break;  // block-uniform: nothing left
-        const Rec best = win[bs];
-        if (tid == 0) tk.out[r] = ls_elite_rec{best.key, best.raw, best.idx, best.code};
-        ++emitted;
-        bar_work();  // everyone has read win[bs] before it is retired
-        for (int i = tid; i < total; i += kThr)
-          if (win[i].code == best.code) win[i].key = -1.0e308;
-        bar_work();
-      }
-      if (tid == 0) *tk.count_out = emitted;
-      return;
-    }
     for (int b = warp * 32; b < nl * k; b += kThr) {
       const int i = b + lane;
       Rec r{0.0, 0.0, 0, 0};
@@ -475,6 +543,7 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
   tree_merge(wl, slots, cnt, warp, k, fk, fi);
   if (warp == 0) wl.emit(tk.out, tk.count_out);
 }
+
 
 template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK, int MODE>
 __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
@@ -530,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0) LS_STAMP(0);
 
   if (warp == kWorkWarps) {  // ---------------- producer warp
     if (lane == 0) {
@@ -590,7 +660,10 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         backoff = LS_BACKOFF_MAX < 128 ? LS_BACKOFF_MAX : 128;
       } else if (gates_done == kGateWarps) {
         __threadfence_block();  // gate warps finished: one last look at the mailboxes
-        if (__shfl_sync(0xffffffffu, mb_pending[f], 0) == 0) break;
+        if (__shfl_sync(0xffffffffu, mb_pending[f], 0) == 0) {
+          if (f == 0 && lane == 0) LS_STAMP(3);
+          break;
+        }
       } else {
         __nanosleep(backoff);
         backoff = backoff < LS_BACKOFF_MAX ? 2 * backoff : LS_BACKOFF_MAX;
@@ -601,6 +674,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     uint32_t* qy = S.qy + warp * kWarpQueue;
     int qcount = 0;  // warp-uniform
     if (SMEM_GATE) mbar_wait(&gate_bar, 0);
+    if (threadIdx.x == 0) LS_STAMP(1);
 
     // hand the newest n (<= 32) queue entries to a free mailbox slot, or
     // score them here when both slots are still busy
@@ -811,6 +885,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     }
     if (qcount > 0) flush(qcount);
     __syncwarp();
+    if (threadIdx.x == 0) LS_STAMP(2);
     if (lane == 0) {
       __threadfence_block();
       atomicAdd((int*)&gates_done, 1);
@@ -822,18 +897,19 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     Rec* slots = reinterpret_cast<Rec*>(S.lists);
     // the lists live in the ring: every gate warp must be past its last stage
     bar_work();
-    const double fl = read_floor(tk.floor);  // global floor so far: most entries are already beaten
-#ifdef LS_DIAG_SERIAL
+    if (threadIdx.x == 0) LS_STAMP(4);
+    // every warp's list (best-first, distinct vectors) to shared memory; warp 0
+    // merges the kWorkWarps lists into this CTA's list (one list per lane)
     wl.store(slots + warp * 32, &list_count[warp]);
     bar_work();
-    if (warp == 0)
-      for (int o = 1; o < kWorkWarps; ++o) wl.absorb(slots + o * 32, list_count[o], tk.k, fl);
-#else
-    tree_merge(wl, slots, list_count, warp, tk.k, fl);
-#endif
+    __shared__ int s_cur[kWorkWarps];
+    __shared__ double s_hk[kWorkWarps];
+    __shared__ int64_t s_hx[kWorkWarps];
     __shared__ int s_last;
     if (warp == 0) {
-      wl.emit(tk.part + (int64_t)blockIdx.x * tk.k, tk.part_counts + blockIdx.x);
+      warp_merge_lists(slots, 32, list_count, kWorkWarps, tk.k, tk.part + (int64_t)blockIdx.x * tk.k,
+                       tk.part_counts + blockIdx.x, s_cur, s_hk, s_hx);
+      if (lane == 0) LS_STAMP(5);
       __threadfence();  // this CTA's list is visible device-wide before it is counted
       unsigned t = 0;
       if (lane == 0) t = atomicAdd(tk.done, 1u);
@@ -846,8 +922,10 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 #else
     if (s_last) {  // the last CTA merges every CTA's list (L2-resident, no second launch)
 #endif
+      if (threadIdx.x == 0) LS_STAMP(6);
       __threadfence();
       final_merge(wl, S.ring, list_count, warp, tk);
+      if (threadIdx.x == 0) LS_STAMP(7);
     }
   }
 }
@@ -1141,3 +1219,9 @@ cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8
 }
 
 }  // namespace ls
+
+#ifdef LS_DIAG_TIMES
+extern "C" int ls_diag_times(unsigned long long* host, int rows) {
+  return (int)cudaMemcpyFromSymbol(host, ls::g_diag_t, sizeof(unsigned long long) * 16 * (rows < 1024 ? rows : 1024));
+}
+#endif
