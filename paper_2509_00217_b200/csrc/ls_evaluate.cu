@@ -645,13 +645,16 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         while (pend) {
           const int bit = __ffs(pend) - 1;
           pend &= pend - 1;
+          // claim the batch (its gate warp may take it back once it is done)
+          uint32_t old = 0;
+          if (lane == 0) old = atomicAnd((uint32_t*)&mb_pending[f], ~(1u << bit));
+          if (!((__shfl_sync(0xffffffffu, old, 0) >> bit) & 1u)) continue;
           const int g = f + kFpWarps * (bit / kSlots), sl = bit % kSlots;
           const int base = (g * kSlots + sl) * 32;
           fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, S.mkey + base, S.my + base, mb_n[g][sl], wl,
                                                        gfloor, gpend, gm.pk);
           __syncwarp();
           if (lane == 0) {
-            atomicAnd((uint32_t*)&mb_pending[f], ~(1u << bit));
             __threadfence_block();
             mb_state[g][sl] = 0;
           }
@@ -885,6 +888,21 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     }
     if (qcount > 0) flush(qcount);
     __syncwarp();
+    // take back this warp's mailbox batches no fp64 warp has claimed yet, so
+    // the end-of-stream backlog is shared by all work warps
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int bit = (warp / kFpWarps) * kSlots + sl;
+      uint32_t old = 0;
+      if (lane == 0) old = atomicAnd((uint32_t*)&mb_pending[warp % kFpWarps], ~(1u << bit));
+      if ((__shfl_sync(0xffffffffu, old, 0) >> bit) & 1u) {
+        const int base = (warp * kSlots + sl) * 32;
+        fp64_batch<NEU, FULL, TOPK, MODE, SMEM_GATE>(T, L, M, a, tk, S.mkey + base, S.my + base, mb_n[warp][sl], wl,
+                                                     gfloor, gpend, gm.pk);
+        __syncwarp();
+        if (lane == 0) mb_state[warp][sl] = 0;
+        __syncwarp();
+      }
+    }
     if (threadIdx.x == 0) LS_STAMP(2);
     if (lane == 0) {
       __threadfence_block();
