@@ -139,22 +139,21 @@ def run_reference(args, rank):
 
 
 class Clocks:
-    """SM clock + throttle-reason sampler running across the timed region: NVML
-    polled every millisecond from a thread (so even a few-millisecond region
-    gets samples), nvidia-smi at its 200 ms floor when NVML is unavailable."""
+    """SM clock + throttle-reason sampler over the timed region: once the
+    steps are queued, the host polls NVML until the region's end event
+    completes (so even a few-millisecond region gets samples); nvidia-smi at
+    its 200 ms floor when NVML is unavailable."""
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
-        self.thread = None
+        self.sampler = None
         self.sm, self.smax, self.reasons = [], None, set()
 
     def start(self):
         try:
-            import threading
-
             import pynvml
 
             pynvml.nvmlInit()
@@ -164,20 +163,16 @@ class Clocks:
                     "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
                     "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
-            self._stop = threading.Event()
 
-            def poll():
-                while not self._stop.is_set():
-                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
-                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.reasons.update(n for n, bit in bits.items() if r & bit)
-                    time.sleep(0.001)
+            def sample():
+                self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.reasons.update(n for n, bit in bits.items() if r & bit)
 
-            self.thread = threading.Thread(target=poll, daemon=True)
-            self.thread.start()
+            self.sampler = sample
             return
         except Exception:
-            self.thread = None
+            self.sampler = None
         try:
             q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -188,11 +183,17 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def poll_until(self, event):
+        """Sample on the calling thread until ``event`` has completed: every
+        sample falls inside the region the event closes."""
+        if self.sampler is None:
+            return
+        while not event.query():
+            self.sampler()
+
     def stop(self):
-        if self.thread is not None:
-            self._stop.set()
-            self.thread.join(timeout=2)
-            src = "nvml 1 ms"
+        if self.sampler is not None:
+            src = "nvml, polled until the end event completed"
         elif self.proc is not None:
             self.proc.terminate()
             try:
@@ -320,6 +321,7 @@ def run_ours(args, rank, world, local_rank):
         recs, count, nl = step(True)
         launches += nl
     t_end.record(stream)
+    clocks.poll_until(t_end)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     if world > 1:
