@@ -49,6 +49,7 @@ CONFIG = "moe_1p6t_h100x2048"
 # (planes: 16 head bytes in instead of 8)
 ALGO_BYTES = {"packed": 8 + 1 + 8, "planes": 16 + 1 + 8}
 ELITE_K = 8
+SEED = 0  # uniform candidate stream seed (seed 0)
 
 
 def parse():
@@ -63,6 +64,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-search", action="store_true", help="skip the PPO search wall-time line")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed batch")
     ap.add_argument("--format", default="packed", choices=["packed", "planes"],
                     help="resident candidate format: 8-byte packed words or uint8 SoA planes")
     return ap.parse_args()
@@ -75,25 +77,29 @@ def peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def uniform_planes_np(head_sizes, n, seed):
-    rng = np.random.default_rng(seed)
-    return np.stack([rng.integers(0, k, size=n, dtype=np.uint8) for k in head_sizes])
+def stream_planes(desc, start, n, threads=None):
+    """Host twin of the GPU arm's candidates: uniform stream positions [start, start + n)
+    (oracle/streams.c == generator.py GEN_UNIFORM == the device's ls_generate)."""
+    from oracle.cost_model import uniform_planes
+
+    return uniform_planes(desc, SEED, start, n, threads=threads)
 
 
 # ----------------------------------------------------------------- CPU side
 
 
-def cpu_rate(workload, seconds, seed=0, sample=1 << 23):
-    """Oracle C port over all host cores: evals/s on a bounded uniform sample."""
+def cpu_rate(workload, seconds, sample=1 << 23):
+    """Oracle C port over all host cores: evals/s on a bounded prefix of rank 0's batch."""
     from oracle.cost_model import simulate_planes
 
     threads = os.cpu_count() or 1
-    planes = uniform_planes_np(workload.space.head_sizes, sample, seed)
     desc = workload.desc()
-    simulate_planes(desc, planes[:, : 1 << 16], threads=threads)  # warm
+    planes = stream_planes(desc, 0, sample, threads)
+    out = simulate_planes(desc, planes[:, : 1 << 16], threads=threads, fields=("throughput",))  # warm
+    out = {"reason": np.empty(sample, np.uint8), "throughput": np.empty(sample, np.float64)}
     done, t0 = 0, time.perf_counter()
     while True:
-        simulate_planes(desc, planes, threads=threads)
+        simulate_planes(desc, planes, threads=threads, out=out)
         done += sample
         el = time.perf_counter() - t0
         if el >= seconds:
@@ -102,6 +108,8 @@ def cpu_rate(workload, seconds, seed=0, sample=1 << 23):
 
 
 def run_reference(args, rank):
+    """The reference's CPU evaluator (C restatement, all host threads) on the GPU arm's
+    exact candidates: rank 0's batch, stream positions [0, n), every step."""
     from paper_2509_00217_b200.config import load_workload
     from oracle.cost_model import simulate_planes
 
@@ -109,27 +117,29 @@ def run_reference(args, rank):
         return
     wl = load_workload(args.config)
     threads = os.cpu_count() or 1
-    sample = 1 << 22
-    planes = uniform_planes_np(wl.space.head_sizes, sample, 0)
+    n = args.n
     desc = wl.desc()
+    planes = stream_planes(desc, 0, n, threads)
+    out = {"reason": np.empty(n, np.uint8), "throughput": np.empty(n, np.float64)}
     for _ in range(args.warmup):
-        simulate_planes(desc, planes, threads=threads)
+        simulate_planes(desc, planes, threads=threads, out=out)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        simulate_planes(desc, planes, threads=threads)
+        simulate_planes(desc, planes, threads=threads, out=out)
         times.append(time.perf_counter() - t0)
     total = sum(times)
-    value = sample * args.steps / total
+    value = n * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: uniform candidates (baselines.uniform_vector), {sample} per step",
-                   "candidates_per_step": sample},
+        "config": workload_config(args, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} uniform candidates x {args.steps} steps, oracle/shardsim_oracle.c "
+                         "sample": f"the GPU arm's rank-0 batch ({n} candidates: uniform stream seed {SEED}, "
+                                   f"positions [0, {n})) x {args.steps} steps through oracle/shardsim_oracle.c "
                                    f"(C restatement of simulator.py:239-341), {threads} threads"},
+        "same_config": True,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -253,6 +263,64 @@ def ppo_search_line():
             "same_best_as_reference": rep.best_raw == REF_SEARCH_BEST_RAW}
 
 
+def workload_config(args, world):
+    return {"workload": f"{args.config}: uniform candidates (baselines.uniform_vector semantics), counter-based "
+                        f"stream seed {SEED}, rank r scores positions [r*n, (r+1)*n), n = {args.n} per GPU per step, "
+                        + ("packed 8-byte candidate words" if args.format == "packed" else "SoA uint8 planes")
+                        + " resident in HBM",
+            "format": args.format, "candidates_per_gpu": args.n, "elite_k": ELITE_K,
+            "parallelism": f"dp{world} (index-range shards)",
+            "l2": f"inputs {ALGO_BYTES[args.format] - 9} B x n per GPU >> 126 MB L2; no flush"}
+
+
+def parity_block(args, ev, wl, out, elite, local_elite, base, rank, world):
+    """Check what the timed steps produced against the CPU oracle (after the timed
+    region): every verdict of this rank's batch, the rank's top-k, the merged elite."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle.parity import batch_parity, merge_topk, rescore_elites, vector_codes
+
+    t0 = time.perf_counter()
+    threads = max(1, (os.cpu_count() or 1) // world)
+    desc = wl.desc()
+    sizes = ev.head_sizes
+
+    def triples(elites):
+        if not elites:
+            return []
+        codes = vector_codes(np.asarray([e.vector for e in elites], dtype=np.uint8).T, sizes)
+        return [(float(e.raw), int(e.index), int(c)) for e, c in zip(elites, codes)]
+
+    bp = batch_parity(desc, sizes, SEED, base, out.reason.cpu().numpy(), out.throughput.cpu().numpy(), ELITE_K,
+                      threads)
+    mine = {"checked": bp["checked"], "reason": bp["reason_mismatches"], "raw": bp["raw_mismatches"],
+            "valid": bp["valid"], "topk": bp["oracle_topk"], "local_equal": triples(local_elite) == bp["oracle_topk"]}
+    allv = [mine]
+    if world > 1:
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+    if rank != 0:
+        return None
+    merged = merge_topk([v["topk"] for v in allv], ELITE_K)
+    return {
+        "oracle": "oracle/shardsim_oracle.c (C restatement of simulator.py:239-341), candidates regenerated by "
+                  "oracle/streams.c",
+        "scope": "every candidate of every rank's batch (the verdict buffers of the last timed step), each "
+                 "rank's top-k, and the merged elite",
+        "candidates_checked": sum(v["checked"] for v in allv),
+        "mismatches": sum(v["reason"] + v["raw"] for v in allv),
+        "reason_mismatches": sum(v["reason"] for v in allv),
+        "raw_mismatches": sum(v["raw"] for v in allv),
+        "valid_candidates": sum(v["valid"] for v in allv),
+        "rank_topk_equal": all(v["local_equal"] for v in allv),
+        "elite_equal": triples(elite) == merged,
+        "elite_rescored": len(elite),
+        "elite_mismatches": rescore_elites(desc, SEED, elite),
+        "seconds": time.perf_counter() - t0,
+    }
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -260,6 +328,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2509_00217_b200.config import load_workload
     from paper_2509_00217_b200.dist import ShardedSweep
     from paper_2509_00217_b200.evaluator import BatchResult, Evaluator, pinned_results
+    from paper_2509_00217_b200.generator import GEN_UNIFORM
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -267,18 +336,18 @@ def run_ours(args, rank, world, local_rank):
     ev = Evaluator(wl, device=local_rank)
     sizes = ev.head_sizes
     n = args.n
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000 + rank)
-    planes = torch.empty((len(sizes), n), dtype=torch.uint8, device=dev)
-    for h, k in enumerate(sizes):
-        planes[h] = torch.randint(0, k, (n,), generator=gen, device=dev, dtype=torch.uint8)
+    base = rank * n  # contiguous global index range per rank
+    # the uniform stream's positions [base, base + n), generated on the device
+    # (the host twin oracle/streams.c regenerates them for the parity block and the reference arm)
+    planes = ev.generate(GEN_UNIFORM, n, start=base, seed=SEED)
     cands = planes
     if args.format == "packed":
         cands = ev.pack(planes)  # same candidates, 8 B each
     out = BatchResult(reason=torch.empty(n, dtype=torch.uint8, device=dev),
                       throughput=torch.empty(n, dtype=torch.float64, device=dev))
-    base = rank * n  # contiguous global index range per rank
-    sweep = ShardedSweep(ev, k=ELITE_K)
+    # N > 1: each step's elite all-gather + merge runs on a side stream beside the
+    # next step's evaluate (which leaves one SM free for it)
+    sweep = ShardedSweep(ev, k=ELITE_K, overlap=world > 1)
     stream = torch.cuda.current_stream(dev)
     ev_start, ev_end = [], []
 
@@ -286,25 +355,14 @@ def run_ours(args, rank, world, local_rank):
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        if world > 1:
-            # records + count land in the all-gather's send buffer (one collective)
-            if cands.dim() == 1:
-                _, recs, count = ev.evaluate_packed_topk(cands, k=ELITE_K, index_base=base, out=out,
-                                                         into=sweep._send)
-            else:
-                _, recs, count = ev.evaluate_topk(cands, k=ELITE_K, index_base=base, out=out, into=sweep._send)
-            if timed:
-                b.record(stream)
-                ev_start.append(a)
-                ev_end.append(b)
-            recs, count = sweep.merge(recs, count)
-            return recs, count, 2  # our kernels: fused evaluate (+ in-kernel elite merge), cross-rank merge
         _, recs, count = sweep.run(cands, index_base=base, out=out)
         if timed:
             b.record(stream)
             ev_start.append(a)
             ev_end.append(b)
-        return recs, count, 1  # one kernel: evaluate + elite, the last CTA merges the CTA lists
+        # our kernels per step: the fused evaluate (its last CTA merges the CTA lists);
+        # N > 1: + the NCCL all-gather and the cross-rank merge (side stream)
+        return recs, count, 1 + (sweep.launches_per_merge if world > 1 else 0)
 
     for _ in range(args.warmup):
         step(False)
@@ -322,6 +380,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.steps):
         recs, count, nl = step(True)
         launches += nl
+    sweep.wait()  # the last step's exchange is part of the timed region
     t_end.record(stream)
     clocks.poll_until(t_end)
     torch.cuda.synchronize(dev)
@@ -331,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [s.elapsed_time(e) for s, e in zip(ev_start, ev_end)]
     elite = ev.decode_records(recs, count)
+    local_elite = ev.decode_records(*sweep.last_local()) if world > 1 else elite
 
     # max over ranks of the device time
     if world > 1:
@@ -339,6 +399,8 @@ def run_ours(args, rank, world, local_rank):
         elapsed_ms, kern_avg = float(t[0]), float(t[1])
     else:
         kern_avg = statistics.mean(kern_ms)
+
+    parity = None if args.no_parity else parity_block(args, ev, wl, out, elite, local_elite, base, rank, world)
 
     # end-to-end through the public host API: pinned host candidates in, host verdicts out
     e2e_n = min(args.e2e_n, n)
@@ -385,16 +447,13 @@ def run_ours(args, rank, world, local_rank):
                     traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
+    cfg = workload_config(args, world)
+    cfg["elite_exchange"] = sweep.transport
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: uniform candidates (baselines.uniform_vector), "
-                               f"{n} per GPU per step, " + ("packed 8-byte candidate words" if args.format == "packed"
-                                                             else "SoA uint8 planes") + " in HBM",
-                   "format": args.format,
-                   "candidates_per_gpu": n, "elite_k": ELITE_K, "parallelism": f"dp{world} (index-range shards)", "elite_exchange": sweep.transport,
-                   "l2": f"inputs {ALGO_BYTES[args.format] - 9} B x n per GPU >> 126 MB L2; no flush"},
+        "config": cfg,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * in_bytes,
                 "d2h_bytes_per_step": world * e2e_n * 9, "candidates_per_gpu": e2e_n,
                 "api": ("Evaluator.evaluate_host_packed -> ls_evaluate_host_packed" if args.format == "packed"
@@ -407,6 +466,7 @@ def run_ours(args, rank, world, local_rank):
                      "kernel_ms_avg": kern_avg, "peak_source": f"{pk_kind} hbm_gbs (MEASURED_PEAKS.json)"},
         "gpu_launches": launches,
         "clocks": clk,
+        "parity": parity,
         "elite_best": {"vector": list(elite[0].vector), "raw": elite[0].raw, "index": elite[0].index} if elite else None,
     }
     if not args.no_search:
@@ -414,8 +474,9 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_cpu:
         rate, cores, done = cpu_rate(wl, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"{done} uniform candidates of {args.config} through oracle/shardsim_oracle.c"
-                                          f" (C restatement of the reference cost model), {cores} threads"}
+                                "sample": f"{done} candidates (a prefix of rank 0's batch, repeated) of {args.config} "
+                                          f"through oracle/shardsim_oracle.c (C restatement of the reference cost "
+                                          f"model), {cores} threads"}
     print(json.dumps(line), flush=True)
 
 

@@ -151,6 +151,11 @@ int ls_ctx_destroy(ls_ctx* ctx);
 /* Size of the encodable space (product of head sizes); 0 if it overflows. */
 uint64_t ls_space_size(const ls_ctx* ctx);
 
+/* Leave `sms` SMs free of the persistent evaluate kernels (default 0), so a
+ * concurrent stream (e.g. the cross-rank elite all-gather + merge of the
+ * previous step) runs beside them instead of delaying one of their CTAs. */
+int ls_reserve_sms(ls_ctx* ctx, int sms);
+
 /* Score n candidates already resident on the device (SoA planes). */
 int ls_evaluate(ls_ctx* ctx, const uint8_t* planes, int64_t n, int64_t plane_stride,
                 const ls_result_soa* out, void* stream);
@@ -207,7 +212,10 @@ int ls_topk(ls_ctx* ctx, const uint8_t* planes, int64_t plane_stride, const uint
  * distinct vectors (LS_KEY_RAW semantics of ls_topk) in the same pass.
  * `out` may be NULL (or out->reason NULL): then no per-candidate verdicts
  * are written at all (16 B/candidate of HBM traffic). k <= 32. scratch must
- * hold ls_evaluate_topk_scratch_bytes(ctx, n, k) bytes of device memory.
+ * hold ls_evaluate_topk_scratch_bytes(ctx, n, k) bytes of device memory,
+ * zero-filled before its first use (every call leaves its sync words zero,
+ * so one call is one kernel launch); calls that may run concurrently (other
+ * streams) need distinct scratch buffers.
  * Unaligned planes or vectors longer than 16 heads need `out` with reason and
  * throughput (evaluated first, then reduced by ls_topk). */
 size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* ctx, int64_t n, int k);
@@ -243,21 +251,6 @@ int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int
  * into the global top-k with the same ordering and dedupe rule. */
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                   ls_elite_rec* out, int32_t* count_out, void* stream);
-/* Cross-rank elite exchange over peer memory (NVLink / NVSwitch), fused with
- * the merge — the device-side replacement of "all-gather the per-rank top-k,
- * then ls_topk_merge". Every rank owns a symmetric buffer
- * of ls_elite_exchange_bytes(world, k) bytes, zeroed before first use, whose
- * base addresses on all ranks are in the device array peer_bases[world]
- * (e.g. torch symmetric memory). Each call pushes `block` ((k + 1) x 32 B: k
- * ls_elite_rec rows, the int32 count at the start of row k) into slot `rank`
- * of every buffer as 8-byte stores that carry `seq` (1, 2, ... — one per
- * call, the same on all ranks) beside each 4-byte data word, waits until all
- * ranks' words of this call have arrived (bounded by about a second; then
- * *count_out = -1) and writes the merged top-k. world <= 8, k <= 32. Single
- * CTA, stream-ordered. */
-size_t ls_elite_exchange_bytes(int world, int k);
-int ls_elite_exchange(const void* block, const uint64_t* peer_bases, void* local_base, int rank, int world, int k,
-                      uint32_t seq, ls_elite_rec* out, int32_t* count_out, void* stream);
 /* ls_evaluate_topk over packed words (fused path only: k <= 32). */
 int ls_evaluate_packed_topk(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
                             int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,

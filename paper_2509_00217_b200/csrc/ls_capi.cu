@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -73,6 +74,8 @@ struct ls_ctx {
   uint64_t* d_tab = nullptr;
   bool smem_gate = false;
   int64_t blocks_tma = 0, blocks_generic = 0;
+  int tma_per_sm = 1;
+  std::atomic<int> reserved_sms{0};  // SMs the persistent kernels leave free (ls_reserve_sms)
   uint64_t space_size = 0;
   // on-device candidate streams, built lazily per mode
   std::mutex gen_mu;
@@ -324,7 +327,8 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
   c->smem_gate = tma_smem_bytes(c->L, c->desc.vector_length, true) <= tma_smem_budget(prop);
   if (c->desc.vector_length <= 16) {
     prepare_eval_kernels(c->L, c->desc.vector_length, c->smem_gate);
-    c->blocks_tma = (int64_t)c->num_sms * std::max(1, tma_blocks_per_sm(c->L, c->desc.vector_length, c->smem_gate));
+    c->tma_per_sm = std::max(1, tma_blocks_per_sm(c->L, c->desc.vector_length, c->smem_gate));
+    c->blocks_tma = (int64_t)c->num_sms * c->tma_per_sm;
   }
   c->blocks_generic = (int64_t)c->num_sms * std::max(1, generic_blocks_per_sm());
   if ((e = cudaGetLastError()) != cudaSuccess) {
@@ -361,6 +365,18 @@ int ls_ctx_destroy(ls_ctx* c) {
 
 uint64_t ls_space_size(const ls_ctx* c) { return c ? c->space_size : 0; }
 
+int ls_reserve_sms(ls_ctx* c, int sms) {
+  g_err.clear();
+  if (!c || sms < 0 || sms >= c->num_sms) return fail(LS_ERR_INVALID_ARGUMENT, "reserved SMs must be in [0, num_sms)");
+  c->reserved_sms.store(sms);
+  return LS_OK;
+}
+
+// CTAs of the persistent evaluate kernels: every SM not reserved, times CTAs per SM
+static int64_t tma_grid_cap(const ls_ctx* c) {
+  return c->blocks_tma > 0 ? (int64_t)(c->num_sms - c->reserved_sms.load()) * c->tma_per_sm : 0;
+}
+
 
 static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stride, const ls_result_soa* out,
                        cudaStream_t s, const uint64_t* words = nullptr) {
@@ -383,7 +399,7 @@ static int do_evaluate(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t stri
   LaunchPlan lp;
   lp.tma = tma_eligible(a, c->M.A) && c->blocks_tma > 0;
   lp.smem_gate = c->smem_gate;
-  lp.max_blocks = lp.tma ? c->blocks_tma : c->blocks_generic;
+  lp.max_blocks = lp.tma ? tma_grid_cap(c) : c->blocks_generic;
   PackMeta pk;
   if (words) {
     if (!lp.tma)
@@ -551,18 +567,20 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
-// Scratch of the fused evaluate + top-k: per-CTA lists and counts, then the
-// 16 zeroed bytes of the global pruning floor and the finished-CTA counter.
+// Scratch of the fused evaluate + top-k: 32 bytes of sync words (the global
+// pruning floor and the finished-CTA counter) at a fixed offset, then the
+// per-CTA lists and counts. The sync words must be zero before the first call
+// on a scratch buffer; the kernel's last CTA leaves them zero again, so a call
+// is one launch (no per-call memset).
 static TopkArgs fused_topk_args(void* scratch, int64_t grid, int k, int64_t index_base, ls_elite_rec* out,
                                 int32_t* count_out) {
   TopkArgs tk{};
   tk.k = k;
   tk.index_base = index_base;
-  tk.part = static_cast<ls_elite_rec*>(scratch);
-  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
-  tk.floor = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(tk.part_counts + grid) + 15) &
-                                                   ~uintptr_t(15));
+  tk.floor = static_cast<unsigned long long*>(scratch);
   tk.done = reinterpret_cast<unsigned int*>(tk.floor + 1);
+  tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(scratch) + 32);
+  tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
   tk.out = out;
   tk.count_out = count_out;
   return tk;
@@ -571,7 +589,7 @@ static TopkArgs fused_topk_args(void* scratch, int64_t grid, int k, int64_t inde
 size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
   if (!c || k < 1) return 0;
   const size_t lists = (size_t)c->blocks_tma;
-  const size_t fused = lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4 + 48;
+  const size_t fused = 32 + lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4;
   return std::max(fused, topk_scratch_bytes(n, k, 0));
 }
 
@@ -620,14 +638,13 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   if (!a.reason) a.thr = a.tpot = a.mem = a.comp = a.comm = a.pipe = nullptr;
   cudaError_t e;
   if (k <= fused_k_max() && c->blocks_tma > 0 && tma_eligible(a, c->M.A)) {
-    LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
-    const int64_t grid = ws_grid(lp, n);
+    LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
+    const int64_t grid = ws_grid(lp, n, words ? GEN_WORDS : GEN_PLANES);
     TopkArgs tk = fused_topk_args(scratch, grid, k, index_base, topk_out, count_out);
     if (n == 0) {
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
       return LS_OK;
     }
-    if ((e = cudaMemsetAsync(tk.floor, 0, 16, s)) != cudaSuccess) return cuda_fail(e, "floor reset");
     const PackMeta pk = pack_meta(c->desc);
     if ((e = launch_evaluate_topk(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, tk, s,
                                   words ? &pk : nullptr)) != cudaSuccess)
@@ -645,6 +662,7 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   if (k > 64) return fail(LS_ERR_INVALID_ARGUMENT, "k must be <= 64");
   e = launch_topk(c->TM, planes, plane_stride, a.reason, a.thr, a.thr, n, k, index_base, topk_out, count_out, scratch,
                   c->num_sms, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 32, s);  // the fused path's sync words, zero again
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
@@ -656,26 +674,6 @@ int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_
   cudaError_t e =
       launch_topk_merge(recs, counts, m, k_in, k, nullptr, out, count_out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge launch");
-}
-
-size_t ls_elite_exchange_bytes(int world, int k) {
-  if (world < 1 || world > 8 || k < 1 || k > 32) return 0;
-  return elite_exchange_bytes(world, k);
-}
-
-int ls_elite_exchange(const void* block, const uint64_t* peer_bases, void* local_base, int rank, int world, int k,
-                      uint32_t seq, ls_elite_rec* out, int32_t* count_out, void* stream) {
-  g_err.clear();
-  if (!block || !peer_bases || !local_base || !out || !count_out || world < 1 || world > 8 || rank < 0 ||
-      rank >= world || k < 1 || k > 32 || seq == 0)
-    return fail(LS_ERR_INVALID_ARGUMENT, "bad elite_exchange arguments");
-  int dev = 0, mhz = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&mhz, cudaDevAttrClockRate, dev);  // kHz
-  const long long timeout = (long long)(mhz > 0 ? mhz : 2000000) * 1000LL;  // ~1 s of SM cycles
-  cudaError_t e = launch_elite_exchange(block, peer_bases, local_base, rank, world, k, seq, timeout, out, count_out,
-                                        static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? LS_OK : cuda_fail(e, "elite_exchange launch");
 }
 
 int ls_env_step(ls_ctx* c, const ls_search_state* st, const int64_t* action, double* reward_out, void* stream) {
@@ -815,11 +813,10 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
     cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
     return LS_OK;
   }
-  LaunchPlan lp{true, c->smem_gate, c->blocks_tma};
-  const int64_t grid = std::min<int64_t>((n + 1023) / 1024, c->blocks_tma);
+  LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
+  const int64_t grid = ws_grid(lp, n, mode);
   TopkArgs tk = fused_topk_args(scratch, grid, k, start, topk_out, count_out);
   cudaError_t e;
-  if ((e = cudaMemsetAsync(tk.floor, 0, 16, s)) != cudaSuccess) return cuda_fail(e, "floor reset");
   if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=
       cudaSuccess)
     return cuda_fail(e, "sweep launch");

@@ -943,7 +943,13 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
       if (threadIdx.x == 0) LS_STAMP(6);
       __threadfence();
       final_merge(wl, S.ring, list_count, warp, tk);
-      if (threadIdx.x == 0) LS_STAMP(7);
+      if (threadIdx.x == 0) {
+        LS_STAMP(7);
+        // every other CTA is past its last floor read and done increment:
+        // leave the sync words zero for the next call on this scratch
+        *tk.floor = 0ull;
+        *tk.done = 0u;
+      }
     }
   }
 }
@@ -1008,8 +1014,7 @@ void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, 
                  const TopkArgs& tk, cudaStream_t s, const GenMeta& gm = GenMeta{}) {
   const int64_t ntiles = (MODE == GEN_PLANES || MODE == GEN_WORDS) ? a.n / kTile : (a.n + kTile - 1) / kTile;
   const size_t smem = ws_dynamic_bytes(M.A, stage_words(L), lp.smem_gate);
-  int64_t blocks = ntiles > 0 ? ntiles : 1;
-  if (blocks > lp.max_blocks) blocks = lp.max_blocks;
+  const int64_t blocks = ws_grid(lp, a.n, MODE);
   if (lp.smem_gate)
     eval_ws_kernel<NEU, FULL, true, TOPK, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
   else
@@ -1158,9 +1163,10 @@ int generic_blocks_per_sm() {
   return nb;
 }
 
-int64_t ws_grid(const LaunchPlan& lp, int64_t n) {
-  const int64_t ntiles = n / kTile;
-  int64_t blocks = ntiles > 0 ? ntiles : 1;
+int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode) {
+  // memory-fed modes: whole tiles (the ragged tail rides on one CTA); generated: ceil
+  const int64_t ntiles = (mode == GEN_PLANES || mode == GEN_WORDS) ? n / kTile : (n + kTile - 1) / kTile;
+  const int64_t blocks = ntiles > 0 ? ntiles : 1;
   return blocks > lp.max_blocks ? lp.max_blocks : blocks;
 }
 

@@ -73,7 +73,7 @@ cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8
                             cudaStream_t s);
 cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
                         cudaStream_t s);
-int64_t ws_grid(const LaunchPlan& lp, int64_t n);
+int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode);  // CTAs of one eval_ws_kernel launch
 int fused_k_max();
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
                                  const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s,
@@ -104,12 +104,6 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);
-
-// Cross-rank elite exchange over peer memory (ls_exchange.cu)
-size_t elite_exchange_bytes(int world, int k);
-cudaError_t launch_elite_exchange(const void* block, const uint64_t* peer_bases, void* local_base, int rank,
-                                  int world, int k, uint32_t seq, long long timeout_cycles, ls_elite_rec* out,
-                                  int32_t* count_out, cudaStream_t s);
 
 // Search-loop environment step (ls_search.cu)
 cudaError_t launch_env_step(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,

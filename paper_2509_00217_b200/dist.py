@@ -6,12 +6,12 @@ communication. Only two small exchanges cross ranks:
 
 * the elite: every rank reduces its shard to a top-k on device
   (``Evaluator.evaluate_topk``); the per-rank blocks (k records + count, one
-  message) go through ONE NCCL all-gather and are merged on device with
-  ``ls_topk_merge`` — or, opt-in, are exchanged over peer memory and merged
-  in one kernel (``ls_elite_exchange``: LL-tagged P2P stores into every
-  rank's symmetric buffer over NVLink/NVSwitch, then the merge); contiguous
-  ranges keep "earliest global index wins" consistent, and the merge rule is
-  exact for any arrival order;
+  message) go through ONE NCCL all-gather over NVLink/NVSwitch and are merged
+  on device with ``ls_topk_merge``; contiguous ranges keep "earliest global
+  index wins" consistent, and the merge rule is exact for any arrival order.
+  With ``overlap=True`` the all-gather and the merge run on a side stream
+  while the next batch is evaluated (the evaluate kernels leave one SM free
+  for them, ``ls_reserve_sms``), so the exchange is off the critical path;
 * reward shaping across ranks (``SearchEnv.step`` semantics, env.py:159-164):
   each rank needs the best valid raw of all EARLIER ranks as its starting
   baseline — one all-gather of one float per rank.
@@ -61,54 +61,46 @@ class SweepResult:
 class ShardedSweep:
     """Evaluate a globally indexed batch split across ranks and merge the elite."""
 
-    def __init__(self, evaluator, k: int = 8, group=None, transport: str = "auto"):
-        """``transport``: "nccl" (one all-gather + the merge kernel; the
-        default, "auto") or "p2p" (peer-memory exchange fused with the merge,
-        ``ls_elite_exchange``). The p2p kernel is exact (same tests) but, as
-        measured on the B200 boxes of round 1, its peer stores/polls over the
-        torch symmetric-memory mapping take ~1.3 ms per exchange against
-        ~70 µs for NCCL, so it is opt-in until that is understood."""
+    launches_per_merge = 2  # the NCCL all-gather kernel + ls_topk_merge
+
+    def __init__(self, evaluator, k: int = 8, group=None, overlap: bool = False):
+        """``overlap``: run each step's exchange on a side stream so the caller's
+        stream goes straight on to the next batch; ``wait()`` joins it."""
         self.ev = evaluator
         self.k = int(k)
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         dev = evaluator.device
-        # one message per rank: k records + a 32-byte row holding the count
-        self._send = torch.empty((self.k + 1, 32), dtype=torch.uint8, device=dev)
-        self._gathered = torch.empty((self.world * (self.k + 1), 32), dtype=torch.uint8, device=dev)
         self.transport = "local" if self.world == 1 else "nccl"
-        if self.world > 1 and transport == "p2p":
-            try:
-                self._init_p2p(dev)
-                self.transport = "p2p"
-            except Exception:
-                if transport == "p2p":
-                    raise
+        self.overlap = bool(overlap) and self.world > 1
+        nbuf = 2 if self.overlap else 1
+        # one message per rank: k records + a 32-byte row holding the count
+        self._sends = [torch.zeros((self.k + 1, 32), dtype=torch.uint8, device=dev) for _ in range(nbuf)]
+        self._gathered = [torch.empty((self.world * (self.k + 1), 32), dtype=torch.uint8, device=dev)
+                          for _ in range(nbuf)]
+        self._merged = [(torch.empty((self.k, 32), dtype=torch.uint8, device=dev),
+                         torch.zeros(1, dtype=torch.int32, device=dev)) for _ in range(nbuf)]
+        self._free = [None] * nbuf  # side-stream event: slot's buffers no longer read
+        self._slot = 0
+        self._side = torch.cuda.Stream(dev) if self.overlap else None
+        if self.overlap:
+            evaluator.reserve_sms(1)
 
-    def _init_p2p(self, dev):
-        import torch.distributed._symmetric_memory as symm
-
-        lib = self.ev._lib
-        nbytes = int(lib.ls_elite_exchange_bytes(self.world, self.k))
-        if nbytes == 0 or self.world > 8 or self.k > 32:
-            raise ValueError("p2p elite exchange supports world <= 8 and k <= 32")
-        self._buf = symm.empty(nbytes, dtype=torch.uint8, device=dev)
-        self._buf.zero_()
-        torch.cuda.synchronize(dev)
-        self._hdl = symm.rendezvous(self._buf, self.group if self.group is not None else dist.group.WORLD)
-        self._peer_bases = torch.tensor([int(p) for p in self._hdl.buffer_ptrs], dtype=torch.int64, device=dev)
-        self._seq = 0
-        self._out = torch.empty((self.k, 32), dtype=torch.uint8, device=dev)
-        self._count = torch.empty(1, dtype=torch.int32, device=dev)
-        dist.barrier(self.group)  # every buffer is zeroed before any rank pushes
+    @property
+    def _send(self) -> torch.Tensor:
+        """The send block the next evaluation writes into (k records + count row)."""
+        return self._sends[self._slot]
 
     def run(self, candidates: torch.Tensor, index_base: int, out=None, verdicts: bool = True):
         """Score this rank's candidates (global indices index_base..) and return the global elite.
 
         ``candidates``: [A, n] uint8 planes, or n packed 64-bit words.
-        Returns (out, recs, count) with recs/count the merged global top-k on device.
+        Returns (out, recs, count) with recs/count the merged global top-k on device
+        (with ``overlap``, valid on the caller's stream only after ``wait()``).
         """
+        if self.world > 1 and self._free[self._slot] is not None:
+            torch.cuda.current_stream(self.ev.device).wait_event(self._free[self._slot])
         into = self._send if self.world > 1 else None
         if candidates.dim() == 1:
             out, recs, count = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
@@ -123,21 +115,40 @@ class ShardedSweep:
         """All-gather every rank's device top-k (k x 32 B + count) in ONE collective and merge on device."""
         if self.world == 1:
             return recs, count
-        if recs.data_ptr() != self._send.data_ptr():  # not produced in place by run()
-            self._send[: self.k].copy_(recs)
-            self._send[self.k, :4].view(torch.int32).copy_(count)
-        if self.transport == "p2p":
-            from ._native import check
+        slot = self._slot
+        send = self._sends[slot]
+        if recs.data_ptr() != send.data_ptr():  # not produced in place by run()
+            send[: self.k].copy_(recs)
+            send[self.k, :4].view(torch.int32).copy_(count)
+        gathered = self._gathered[slot]
+        cur = torch.cuda.current_stream(self.ev.device)
+        if self._side is None:
+            dist.all_gather_into_tensor(gathered, send, group=self.group)
+            return self._merge_gathered(gathered, self._merged[slot])
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        self._side.wait_event(ready)
+        with torch.cuda.stream(self._side):
+            dist.all_gather_into_tensor(gathered, send, group=self.group)
+            res = self._merge_gathered(gathered, self._merged[slot])
+            done = torch.cuda.Event()
+            done.record(self._side)
+        self._free[slot] = done
+        self._slot = (slot + 1) % len(self._sends)
+        return res
 
-            self._seq += 1
-            check(self.ev._lib.ls_elite_exchange(
-                ctypes.c_void_p(self._send.data_ptr()), ctypes.c_void_p(self._peer_bases.data_ptr()),
-                ctypes.c_void_p(self._buf.data_ptr()), self.rank, self.world, self.k, self._seq,
-                ctypes.c_void_p(self._out.data_ptr()), ctypes.c_void_p(self._count.data_ptr()),
-                self.ev._stream()))
-            return self._out, self._count
-        dist.all_gather_into_tensor(self._gathered, self._send, group=self.group)
-        g = self._gathered.view(self.world, self.k + 1, 32)
+    def _merge_gathered(self, gathered: torch.Tensor, into):
+        g = gathered.view(self.world, self.k + 1, 32)
         counts = g[:, self.k, :4].contiguous().view(torch.int32).reshape(self.world)
         # each rank's list is k_in = k + 1 slots; the count row is never read (count <= k)
-        return self.ev.merge_records(self._gathered, counts, self.k + 1, self.k)
+        return self.ev.merge_records(gathered, counts, self.k + 1, self.k, into=into)
+
+    def last_local(self):
+        """(records, count) this rank contributed to the most recent exchange."""
+        send = self._sends[(self._slot - 1) % len(self._sends)] if self.overlap else self._sends[0]
+        return send[: self.k], send[self.k, :4].view(torch.int32)
+
+    def wait(self) -> None:
+        """Make the caller's stream wait for every exchange issued so far."""
+        if self._side is not None:
+            torch.cuda.current_stream(self.ev.device).wait_stream(self._side)

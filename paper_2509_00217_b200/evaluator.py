@@ -102,7 +102,7 @@ class Evaluator:
         self.vector_length = self.desc.vector_length
         self.head_sizes = tuple(int(self.desc.domain_len[h]) if h < 4 else 3 for h in range(self.vector_length))
         self.space_size = int(self._lib.ls_space_size(self._ctx))
-        self._scratch: torch.Tensor | None = None
+        self._scratch: dict[int, torch.Tensor] = {}  # fused-call scratch per CUDA stream
 
     # -- lifecycle ----------------------------------------------------------
 
@@ -136,6 +136,10 @@ class Evaluator:
         n = planes.shape[1]
         stride = planes.stride(0) if planes.shape[0] > 1 else max(n, 1)
         return n, max(stride, n)
+
+    def reserve_sms(self, sms: int) -> None:
+        """Leave ``sms`` SMs free of the persistent evaluate kernels (ls_reserve_sms)."""
+        check(self._lib.ls_reserve_sms(self._ctx, int(sms)))
 
     # -- evaluation ---------------------------------------------------------
 
@@ -251,12 +255,10 @@ class Evaluator:
                 setattr(out, f, torch.empty(n, dtype=torch.float64, device=self.device))
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
         recs, count = self._elite_out(k, into)
-        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
-        if self._scratch is None or self._scratch.numel() < nbytes:
-            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        scratch = self._fused_scratch(n, k)
         check(self._lib.ls_evaluate_topk(self._ctx, ctypes.c_void_p(planes.data_ptr()), n, stride,
                                          ctypes.byref(soa) if soa is not None else None, int(k), int(index_base),
-                                         _ptr(recs), _ptr(count), _ptr(self._scratch), self._stream()))
+                                         _ptr(recs), _ptr(count), _ptr(scratch), self._stream()))
         return (out if verdicts else None), recs, count
 
     # -- packed candidate words (8 B per candidate) ---------------------------
@@ -298,6 +300,19 @@ class Evaluator:
                                            self._stream()))
         return out
 
+    def _fused_scratch(self, n: int, k: int) -> torch.Tensor:
+        """Scratch of the fused evaluate + elite kernels, one buffer per CUDA stream
+        (calls on different streams may overlap and must not share the CTA lists
+        and sync words). Zero-filled once: every call leaves its sync words zero.
+        A buffer is only ever used on the stream it was allocated on."""
+        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, int(n), int(k)))
+        key = torch.cuda.current_stream(self.device).cuda_stream
+        buf = self._scratch.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.zeros(max(nbytes, 4096), dtype=torch.uint8, device=self.device)
+            self._scratch[key] = buf
+        return buf
+
     def _elite_out(self, k: int, into: torch.Tensor | None):
         """(records, count) outputs: fresh tensors, or views of a caller's [(k + 1), 32]
         uint8 buffer (records in rows 0..k-1, the int32 count at the start of row k) —
@@ -318,12 +333,10 @@ class Evaluator:
             out = self._alloc(n, fields)
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
         recs, count = self._elite_out(k, into)
-        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, n, int(k)))
-        if self._scratch is None or self._scratch.numel() < nbytes:
-            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        scratch = self._fused_scratch(n, k)
         check(self._lib.ls_evaluate_packed_topk(self._ctx, ctypes.c_void_p(words.data_ptr()), n,
                                                 ctypes.byref(soa) if soa is not None else None, int(k),
-                                                int(index_base), _ptr(recs), _ptr(count), _ptr(self._scratch),
+                                                int(index_base), _ptr(recs), _ptr(count), _ptr(scratch),
                                                 self._stream()))
         return (out if verdicts else None), recs, count
 
@@ -364,18 +377,20 @@ class Evaluator:
         and return the top-k by raw over distinct vectors (records, count)."""
         recs = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
         count = torch.empty(1, dtype=torch.int32, device=self.device)
-        nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, int(n), int(k)))
-        if self._scratch is None or self._scratch.numel() < nbytes:
-            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        scratch = self._fused_scratch(n, k)
         check(self._lib.ls_sweep(self._ctx, int(mode), int(seed) & (2**64 - 1), int(start), int(n), int(k),
-                                 _ptr(recs), _ptr(count), _ptr(self._scratch), self._stream()))
+                                 _ptr(recs), _ptr(count), _ptr(scratch), self._stream()))
         return recs, count
 
-    def merge_records(self, recs: torch.Tensor, counts: torch.Tensor, k_in: int, k: int):
-        """Merge m stacked record lists ([m*k_in, 32] bytes, counts [m]) into one top-k."""
+    def merge_records(self, recs: torch.Tensor, counts: torch.Tensor, k_in: int, k: int, into=None):
+        """Merge m stacked record lists ([m*k_in, 32] bytes, counts [m]) into one top-k
+        (into: optional preallocated ([k, 32] uint8, [1] int32) outputs)."""
         m = counts.shape[0]
-        out = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
-        count = torch.empty(1, dtype=torch.int32, device=self.device)
+        if into is not None:
+            out, count = into
+        else:
+            out = torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device)
+            count = torch.empty(1, dtype=torch.int32, device=self.device)
         check(self._lib.ls_topk_merge(_ptr(recs), _ptr(counts), m, int(k_in), int(k), _ptr(out), _ptr(count),
                                       self._stream()))
         return out, count

@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, k, q, packed=False, transport="nccl"):
+def _worker(rank, world, port, n, k, q, packed=False, overlap=False):
     import torch.distributed as dist
 
     from paper_2509_00217_b200.config import load_workload
@@ -37,11 +37,15 @@ def _worker(rank, world, port, n, k, q, packed=False, transport="nccl"):
         mine = torch.from_numpy(np.ascontiguousarray(planes[:, lo:hi])).cuda(rank)
         if packed:  # 8-byte candidate words (the bench's resident format)
             mine = ev.pack(mine)
-        sweep = ShardedSweep(ev, k=k, transport=transport)
-        assert sweep.transport == transport
-        for _ in range(3):  # repeated steps exercise both parities of the p2p buffers
+        sweep = ShardedSweep(ev, k=k, overlap=overlap)
+        for _ in range(3):  # repeated steps exercise both slots of the overlapped exchange
             _, recs, count = sweep.run(mine, index_base=lo)
+        sweep.wait()
         elites = ev.decode_records(recs, count)
+        local = ev.decode_records(*sweep.last_local())
+        topk = ev.evaluate_packed_topk if packed else ev.evaluate_topk
+        _, r0, c0 = topk(mine, k=k, index_base=lo)
+        assert local == ev.decode_records(r0, c0)
         if rank == 0:
             whole = torch.from_numpy(planes).cuda(rank)
             _, r1, c1 = ev.evaluate_topk(whole, k=k)
@@ -53,17 +57,17 @@ def _worker(rank, world, port, n, k, q, packed=False, transport="nccl"):
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("packed", [False, True])
 @pytest.mark.parametrize("k", [3, 8])
-def test_two_gpu_elite_equals_single_gpu(k, packed, transport):
+def test_two_gpu_elite_equals_single_gpu(k, packed, overlap):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     n = 5_000_003
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, k, q, packed, transport)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, k, q, packed, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     merged, single = q.get(timeout=300)

@@ -48,3 +48,16 @@ def test_uniform_stream_covers_domains_uniformly():
     w = stream_vectors(wl.model, wl.space, GEN_UNIFORM, 123, 1000, seed=7)
     assert np.array_equal(w, v[123:1123])
     assert not np.array_equal(stream_vectors(wl.model, wl.space, GEN_UNIFORM, 0, 1000, seed=8), v[:1000])
+
+
+def test_oracle_uniform_stream_matches_generator():
+    """oracle/streams.c (the host twin bench.py's parity block uses) regenerates
+    the same vectors as generator.py, which the GPU tests pin to the device."""
+    from oracle.cost_model import uniform_planes
+
+    for name in ("moe_1p6t_2048", "llama3_70b_h100x64", "tiny"):
+        wl, _, _ = load_eval(name)
+        for seed, start, n in ((0, 0, 5000), (2**64 - 3, 1 << 33, 777), (1000, 12345, 4096)):
+            want = stream_vectors(wl.model, wl.space, GEN_UNIFORM, start, n, seed=seed)
+            got = uniform_planes(wl.desc(), seed, start, n, threads=3)
+            assert np.array_equal(got.T.astype(np.int64), want), (name, seed, start)
