@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-search", action="store_true", help="skip the PPO search wall-time line")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed batch")
+    ap.add_argument("--no-pyref", action="store_true", help="skip timing the reference's Python evaluator")
+    ap.add_argument("--pyref-n", type=int, default=1 << 19, help="candidates for the Python reference timing")
     ap.add_argument("--format", default="packed", choices=["packed", "planes"],
                     help="resident candidate format: 8-byte packed words or uint8 SoA planes")
     return ap.parse_args()
@@ -86,6 +88,28 @@ def stream_planes(desc, start, n, threads=None):
 
 
 # ----------------------------------------------------------------- CPU side
+
+
+def python_reference_block(args, desc, gpu_reason=None, gpu_thr=None, sample=None):
+    """The reference's own Python evaluator (baseline/_ref, decode_strategy +
+    simulate per candidate) in Pool(os.cpu_count()) on the first `sample`
+    candidates of rank 0's batch; its verdicts are compared with the GPU's."""
+    from oracle import pyref
+
+    if not pyref.available():
+        return {"unavailable": "the reference package is not installed in baseline/_ref (DESIGN.md section 7)"}
+    sample = sample or args.pyref_n
+    cfg = ROOT / "paper_2509_00217_b200" / "configs" / f"{args.config}.yaml"
+    r = pyref.time_reference(str(cfg), stream_planes(desc, 0, sample))
+    blk = {"value": r["value"], "unit": UNIT, "cores": r["procs"], "per_core": r["per_core"], "kind": "reference",
+           "sample": f"first {sample} candidates of rank 0's batch; rate measured on that sample (a full batch "
+                     f"of {args.n} would take {args.n / r['value']:.0f} s at this rate)",
+           "seconds": r["seconds"], "python": r["python"], "cpu": r["cpu"],
+           "api": "shardsearch.strategy.decode_strategy + shardsearch.simulator.simulate (env.py:140-158)"}
+    if gpu_reason is not None:
+        blk["gpu_mismatches"] = int(np.count_nonzero(gpu_reason[:sample] != r["reason"]) + np.count_nonzero(
+            gpu_thr[:sample].view(np.uint64) != r["throughput"].view(np.uint64)))
+    return blk
 
 
 def cpu_rate(workload, seconds, sample=1 << 23):
@@ -142,6 +166,12 @@ def run_reference(args, rank):
         "same_config": True,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_pyref:
+        # the reference's own Python evaluator on the same candidates, checked against the port
+        pr = python_reference_block(args, desc, out["reason"], out["throughput"])
+        if "gpu_mismatches" in pr:
+            pr["port_mismatches"] = pr.pop("gpu_mismatches")
+        line["python_reference"] = pr
     print(json.dumps(line), flush=True)
 
 
@@ -240,7 +270,9 @@ REF_SEARCH_BEST_RAW = 41.90363518619595
 
 def ppo_search_line():
     """Wall time of one full PPO search through the public
-    API: ppo.run_search on the flagship 1.2T config, budget 4000, seed 0."""
+    API: ppo.run_search on the flagship 1.2T config, budget 4000, seed 0 — the
+    first (cold) call in this process, which pays the context, table build and
+    graph capture, and a second (warm) call."""
     from paper_2509_00217_b200.config import load_workload
     from paper_2509_00217_b200.env import SearchEnv
     from paper_2509_00217_b200.knobs import PpoConfig
@@ -249,18 +281,65 @@ def ppo_search_line():
     wl = load_workload("moe_1p2t_h100")
 
     def one(budget):
-        env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, budget, slo_tpot=wl.slo_tpot)
-        env.evaluator
         t0 = time.perf_counter()
+        env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, budget, slo_tpot=wl.slo_tpot)
         rep = run_search(env, PpoConfig(budget=budget), 0)
         return time.perf_counter() - t0, rep
 
-    one(200)  # loads kernels, first graph captures
+    cold, rep0 = one(4000)
     wall, rep = one(4000)
     return {"workload": "moe_1p2t_h100 PPO run_search, budget 4000, seed 0 (fused policy kernels + CUDA graphs)",
-            "wall_s": wall, "evals": rep.evals, "evals_per_s": rep.evals / wall, "best_raw": rep.best_raw,
-            "reference_wall_s": REF_SEARCH_WALL_S, "reference_best_raw": REF_SEARCH_BEST_RAW,
-            "same_best_as_reference": rep.best_raw == REF_SEARCH_BEST_RAW}
+            "wall_s": wall, "cold_wall_s": cold, "evals": rep.evals, "evals_per_s": rep.evals / wall,
+            "best_raw": rep.best_raw, "reference_wall_s": REF_SEARCH_WALL_S, "reference_best_raw": REF_SEARCH_BEST_RAW,
+            "same_best_as_reference": rep.best_raw == REF_SEARCH_BEST_RAW == rep0.best_raw}
+
+
+# reference per-call costs on this workload family (63-85 us per
+# candidate through SearchEnv.step; SA 4000 steps 0.57 s)
+REF_STEP_US = (63.0, 85.0)
+REF_SA_4000_S = 0.57
+
+
+def seam_line():
+    """Latency of the per-candidate drop-in seam (reference env.py:140-180) and the
+    device SA chain (baselines.py:112-145), through the public API."""
+    from paper_2509_00217_b200.baselines import SaConfig, simulated_annealing, uniform_vector
+    from paper_2509_00217_b200.config import load_workload
+    from paper_2509_00217_b200.env import SearchEnv
+    from paper_2509_00217_b200.simulator import SimRequest, simulate
+    from paper_2509_00217_b200.strategy import decode_strategy
+
+    wl = load_workload("moe_1p2t_h100")
+    n = 4000
+    env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, 3 * n, slo_tpot=wl.slo_tpot)
+    rng = np.random.default_rng(0)
+    vecs = [uniform_vector(wl.space, rng) for _ in range(n)]
+    for v in vecs[:200]:
+        env.step(v)
+    t0 = time.perf_counter()
+    for v in vecs:
+        env.step(v)
+    step_us = (time.perf_counter() - t0) / n * 1e6
+    ev = env.evaluator
+    t0 = time.perf_counter()
+    for v in vecs:
+        ev.evaluate_one(v)
+    one_us = (time.perf_counter() - t0) / n * 1e6
+    reqs = [SimRequest(wl.model, wl.hw, decode_strategy(v, wl.space), wl.context_len, wl.slo_tpot) for v in vecs]
+    simulate(reqs[0])
+    t0 = time.perf_counter()
+    for r in reqs:
+        simulate(r)
+    sim_us = (time.perf_counter() - t0) / n * 1e6
+    sa_env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, 4000, slo_tpot=wl.slo_tpot)
+    sa_env.evaluator
+    t0 = time.perf_counter()
+    rep = simulated_annealing(sa_env, SaConfig(), 4000, 0)
+    sa_s = time.perf_counter() - t0
+    return {"workload": "moe_1p2t_h100, uniform vectors, one call per candidate",
+            "search_env_step_us": step_us, "simulate_us": sim_us, "evaluate_one_us": one_us,
+            "reference_step_us": list(REF_STEP_US),
+            "sa_4000_wall_s": sa_s, "sa_best_raw": rep.best_raw, "reference_sa_4000_s": REF_SA_4000_S}
 
 
 def workload_config(args, world):
@@ -327,7 +406,7 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2509_00217_b200.config import load_workload
     from paper_2509_00217_b200.dist import ShardedSweep
-    from paper_2509_00217_b200.evaluator import BatchResult, Evaluator, pinned_results
+    from paper_2509_00217_b200.evaluator import BatchResult, Evaluator
     from paper_2509_00217_b200.generator import GEN_UNIFORM
 
     torch.cuda.set_device(local_rank)
@@ -401,36 +480,45 @@ def run_ours(args, rank, world, local_rank):
         kern_avg = statistics.mean(kern_ms)
 
     parity = None if args.no_parity else parity_block(args, ev, wl, out, elite, local_elite, base, rank, world)
+    out_reason_h = out_thr_h = None
+    if rank == 0 and not args.no_pyref:
+        out_reason_h = out.reason[: args.pyref_n].cpu().numpy()
+        out_thr_h = out.throughput[: args.pyref_n].cpu().numpy()
 
-    # end-to-end through the public host API: pinned host candidates in, host verdicts out
+    # end-to-end through the public host API (Evaluator.evaluate_host_compact ->
+    # ls_evaluate_host_compact): the step's candidates in pinned HOST memory in the
+    # reference's wire format (uint8 index-vector planes), packed into 8-byte words
+    # on host threads, H2D, evaluate, D2H of the reason bytes + the valid raws —
+    # all inside the timed region; the same from host packed words as a second figure
     e2e_n = min(args.e2e_n, n)
-    if args.format == "packed":
-        host_in = torch.empty(e2e_n, dtype=torch.int64).pin_memory()
-        host_in.copy_(cands[:e2e_n].cpu())
-        in_bytes = 8
-        run_host = ev.evaluate_host_packed
-    else:
-        host_in = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
-        host_in.copy_(planes[:, :e2e_n].cpu())
-        in_bytes = len(sizes)
-        run_host = ev.evaluate_host
-    hp = host_in.numpy()
+    host_planes = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
+    host_planes.copy_(planes[:, :e2e_n].cpu())
+    host_words = torch.empty(e2e_n, dtype=torch.int64).pin_memory()
+    host_words.copy_(cands[:e2e_n].cpu() if cands.dim() == 1 else ev.pack(planes[:, :e2e_n]).cpu())
     del planes
+    reason_h = torch.empty(e2e_n, dtype=torch.uint8).pin_memory().numpy()
+    vraw_h = torch.empty(e2e_n, dtype=torch.float64).pin_memory().numpy()
     e2e_steps = max(3, min(args.steps, 10))
-    hout = pinned_results(e2e_n)
-    run_host(hp, out=hout)  # warm: allocates the pipeline buffers
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        res = run_host(hp, out=hout)
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
-    e2e_value = world * e2e_n * e2e_steps / e2e_s
-    del res
+
+    def e2e_run(src):
+        ev.evaluate_host_compact(src, reason_h, vraw_h)  # warm: allocates the pipeline buffers
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        nv = 0
+        for _ in range(e2e_steps):
+            r, v = ev.evaluate_host_compact(src, reason_h, vraw_h)
+            nv = len(v)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t[0])
+        return world * e2e_n * e2e_steps / el, nv
+
+    e2e_value, nvalid = e2e_run(host_planes.numpy())
+    e2e_words, _ = e2e_run(host_words.numpy())
+    e2e_check = bool(np.array_equal(reason_h, out.reason[:e2e_n].cpu().numpy()))
 
     if rank != 0:
         return
@@ -454,10 +542,13 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": cfg,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * in_bytes,
-                "d2h_bytes_per_step": world * e2e_n * 9, "candidates_per_gpu": e2e_n,
-                "api": ("Evaluator.evaluate_host_packed -> ls_evaluate_host_packed" if args.format == "packed"
-                        else "Evaluator.evaluate_host -> ls_evaluate_host")},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * 8,
+                "d2h_bytes_per_step": world * (e2e_n + 8 * nvalid), "candidates_per_gpu": e2e_n,
+                "input": "pinned host uint8 planes [16, n] (the reference's index vectors), packed to 8-byte "
+                         "words on host threads inside the timed region",
+                "output": "reason byte per candidate + raw of the valid ones (compact host results)",
+                "api": "Evaluator.evaluate_host_compact -> ls_evaluate_host_compact(LS_HOST_PLANES)",
+                "from_packed_words": e2e_words, "reason_equal_device_batch": e2e_check},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved_gbs / pk.get("hbm_gbs"), "traffic": traffic,
                      "kernel": "eval_ws_kernel<GEN_WORDS> (fused evaluate + elite, last-CTA merge)"
@@ -471,6 +562,9 @@ def run_ours(args, rank, world, local_rank):
     }
     if not args.no_search:
         line["search"] = ppo_search_line()
+        line["seam"] = seam_line()
+    if not args.no_pyref:
+        line["python_reference"] = python_reference_block(args, wl.desc(), out_reason_h, out_thr_h)
     if not args.no_cpu:
         rate, cores, done = cpu_rate(wl, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",

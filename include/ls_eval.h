@@ -180,6 +180,24 @@ int ls_pack(ls_ctx* ctx, const uint8_t* planes, int64_t plane_stride, int64_t n,
 int ls_evaluate_packed(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, void* stream);
 int ls_evaluate_host_packed(ls_ctx* ctx, const uint64_t* host_words, int64_t n, const ls_result_soa* host_out);
 
+/* Compact host results: the reason byte of every candidate plus the raw
+ * throughput of the VALID ones (reason 0) only, in index order — all that
+ * SearchEnv.step consumes (env.py:165-172; raw is 0 for every invalid
+ * candidate, and the valid positions are the zero reason bytes). About 1 B
+ * per candidate comes back instead of 9. Input `format`:
+ *   LS_HOST_PLANES  A uint8 planes plane_stride apart (the reference's index
+ *                   vectors, SoA); packed into 8-byte candidate words on host
+ *                   worker threads inside the call (chunk by chunk, beside the
+ *                   copies and kernels of earlier chunks), so 8 B/candidate
+ *                   cross PCIe instead of A;
+ *   LS_HOST_WORDS   packed candidate words, as ls_evaluate_packed takes them.
+ * valid_raw holds up to `capacity` doubles; *valid_count receives the number
+ * of valid candidates (LS_ERR_INVALID_ARGUMENT when it exceeds capacity).
+ * Blocking; pinned host buffers (ls_host_alloc) copy fastest. */
+enum { LS_HOST_PLANES = 0, LS_HOST_WORDS = 1 };
+int ls_evaluate_host_compact(ls_ctx* ctx, int format, const void* host_in, int64_t n, int64_t plane_stride,
+                             uint8_t* reason_out, double* valid_raw, int64_t capacity, int64_t* valid_count);
+
 /* Pinned host memory helpers for ls_evaluate_host callers. */
 int ls_host_alloc(size_t bytes, void** out);
 int ls_host_free(void* ptr);
@@ -282,6 +300,37 @@ typedef struct ls_search_state {
 } ls_search_state;
 
 int ls_env_step(ls_ctx* ctx, const ls_search_state* state, const int64_t* action, double* reward_out, void* stream);
+
+/* ---- Scalar seam ----------------------------------------------------------
+ * simulate() for ONE strategy (simulator.py:239-341) with host memory on both
+ * sides: `vector` holds A index bytes; reason_out receives the verdict and
+ * fields_out (optional) the six SimResult numbers in ls_result_soa order
+ * (throughput, tpot_s, memory_bytes, compute_s, comm_s, pipeline_s). Blocking
+ * and low-latency: the vector travels in the launch parameters and the
+ * verdict comes back through host-mapped memory (no copies, no stream
+ * synchronisation). Thread-safe (calls on one context serialise). */
+int ls_evaluate_one(ls_ctx* ctx, const uint8_t* vector, uint8_t* reason_out, double* fields_out);
+
+/* ---- Simulated annealing chain on the device ------------------------------
+ * baselines.simulated_annealing (baselines.py:112-145) as one launch: `steps`
+ * SearchEnv.step evaluations on the env state (best_raw, log_*, alpha, beta,
+ * penalty of `env`; its elite fields are unused), the first of `init`, each
+ * later one of a mutation of the current vector (coords/drawn: the heads
+ * mutate_vector picks and its integers(k - 1) draws, `moves` per proposal),
+ * accepted when u < Metropolis(delta, temperature). The randomness is drawn
+ * on the host in the reference's order; all pointers are device memory. */
+typedef struct ls_sa_plan {
+  int32_t steps;
+  int32_t moves;
+  const int32_t* init;        /* [A] */
+  const int32_t* coords;      /* [(steps - 1) * moves] */
+  const int32_t* drawn;       /* [(steps - 1) * moves] */
+  const double* u;            /* [steps - 1] */
+  const double* temperature;  /* [steps - 1] */
+  ls_search_state env;
+} ls_sa_plan;
+
+int ls_sa_chain(ls_ctx* ctx, const ls_sa_plan* plan, void* stream);
 
 /* ---- Fused PPO search rounds ---------------------------------------------
  * The reference's elite-conditioned policy (policy.py:213-499: embedding,

@@ -98,6 +98,13 @@ class PpoPlan(ctypes.Structure):
         ("epochs", ctypes.c_int32)]
 
 
+class SaPlan(ctypes.Structure):
+    """ls_sa_plan: one simulated-annealing chain on the device."""
+
+    _fields_ = [("steps", ctypes.c_int32), ("moves", ctypes.c_int32)] + [
+        (n, ctypes.c_void_p) for n in ("init", "coords", "drawn", "u", "temperature")] + [("env", SearchState)]
+
+
 class EliteRec(ctypes.Structure):
     _fields_ = [
         ("key", ctypes.c_double),
@@ -119,6 +126,9 @@ _SIGS = {
                                    ctypes.POINTER(ResultSoA), ctypes.c_void_p]),
     "ls_evaluate_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.POINTER(ResultSoA)]),
+    "ls_evaluate_host_compact": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                                ctypes.POINTER(ctypes.c_int64)]),
     "ls_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "ls_host_free": (ctypes.c_int, [ctypes.c_void_p]),
     "ls_scan_scratch_bytes": (ctypes.c_size_t, [ctypes.c_int64]),
@@ -153,6 +163,8 @@ _SIGS = {
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ls_env_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SearchState), ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p]),
+    "ls_evaluate_one": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ls_sa_chain": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SaPlan), ctypes.c_void_p]),
     "ls_policy_layout_of": (ctypes.c_int, [ctypes.POINTER(PolicyDims), ctypes.POINTER(PolicyLayout)]),
     "ls_ppo_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(PolicyDims)]),
     "ls_ppo_prime": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PpoPlan), ctypes.c_void_p]),

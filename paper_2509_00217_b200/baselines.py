@@ -24,8 +24,8 @@ from typing import Callable
 
 import numpy as np
 
-from .env import SearchEnv
-from .evaluator import Elite, Evaluator
+from .env import BudgetExhausted, EvalRecord, SearchEnv
+from .evaluator import REASON_NAMES, Elite, Evaluator
 from .generator import GEN_ENUM, GEN_ENUM_ADMISSIBLE, GEN_UNIFORM
 from .knobs import SaConfig
 from .report import SearchReport, build_report
@@ -85,9 +85,55 @@ def random_walk(env: SearchEnv, budget: int, seed: int) -> SearchReport:
 
 
 def simulated_annealing(env: SearchEnv, cfg: SaConfig, budget: int, seed: int) -> SearchReport:
-    """Single-chain annealing on the shaped reward, cosine temperature."""
+    """Single-chain annealing on the shaped reward, cosine temperature
+    (reference baselines.py:112-145).
+
+    The chain runs on the device in ONE kernel (ls_sa_chain): the randomness
+    is drawn here first, in the reference's order — it does not depend on the
+    chain's accept/reject decisions — so the records equal the reference's.
+    An environment whose ``evaluate_raw`` seam was overridden runs the
+    sequential host loop through that seam instead."""
     if budget < 1:
         raise ValueError("simulated annealing budget must be >= 1")
+    if not env._stock_seam():
+        return _simulated_annealing_host(env, cfg, budget, seed)
+    start = time.perf_counter()
+    rng = np.random.default_rng(seed)
+    first = env.evals_used
+    steps = min(budget, env.budget_left)
+    if steps < 1:
+        raise BudgetExhausted(f"budget of {env.budget} evaluations spent")
+    space = env.space
+    init = uniform_vector(space, rng)
+    mutable = [i for i, k in enumerate(space.head_sizes) if k > 1]
+    moves = min(cfg.neighbor_moves, len(mutable)) if mutable else 0
+    coords = np.zeros((steps - 1, moves), dtype=np.int32)
+    drawn = np.zeros((steps - 1, moves), dtype=np.int32)
+    u = np.zeros(steps - 1, dtype=np.float64)
+    temperature = np.zeros(steps - 1, dtype=np.float64)
+    for step in range(1, steps):  # mutate_vector's and the acceptance test's draws, in order
+        temperature[step - 1] = cosine_decay(cfg.t_initial, step / budget)
+        if mutable:
+            picks = np.atleast_1d(rng.choice(len(mutable), size=moves, replace=False))
+            for j, pick in enumerate(picks):
+                coord = mutable[int(pick)]
+                coords[step - 1, j] = coord
+                drawn[step - 1, j] = int(rng.integers(space.head_sizes[coord] - 1))
+        u[step - 1] = rng.random()
+    rc = env.reward_cfg
+    vecs, raws, rewards, reasons, best = env.evaluator.sa_chain(
+        init, coords, drawn, u, temperature, moves, env.best_raw, rc.alpha, rc.beta, rc.invalid_penalty)
+    for i in range(steps):
+        env._append(EvalRecord(env.evals_used, tuple(int(x) for x in vecs[i]), float(raws[i]), float(rewards[i]),
+                               bool(reasons[i] == 0), REASON_NAMES[int(reasons[i])]))
+    env.best_raw = best
+    if steps < budget:  # the reference's next env.step would raise here
+        raise BudgetExhausted(f"budget of {env.budget} evaluations spent")
+    records = env.eval_log[first:first + budget]
+    return build_report("sa", seed, records, (), budget, time.perf_counter() - start)
+
+
+def _simulated_annealing_host(env: SearchEnv, cfg: SaConfig, budget: int, seed: int) -> SearchReport:
     start = time.perf_counter()
     rng = np.random.default_rng(seed)
     first = env.evals_used

@@ -12,8 +12,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ls_eval.h"
@@ -28,6 +31,7 @@ static_assert(sizeof(ls_elite_rec) == 32, "ls_elite_rec layout");
 static_assert(sizeof(ls_search_state) == 104, "ls_search_state layout");
 static_assert(sizeof(ls_policy_layout) == 168, "ls_policy_layout layout");
 static_assert(sizeof(ls_ppo_plan) == 344, "ls_ppo_plan layout");
+static_assert(sizeof(ls_sa_plan) == 152, "ls_sa_plan layout");
 
 namespace {
 
@@ -62,6 +66,77 @@ constexpr int kHostChunkLog2 = 22;
 constexpr int kPipe = 8;  // capacity; the depth in use is ls_ctx::pipe
 constexpr int kPipeDefault = 2;
 
+// Persistent host worker pool: run(fn, parts) calls fn(part) for part in
+// [0, parts) across the workers and the calling thread, and returns when all
+// are done. Used to pack host planes into candidate words inside the host
+// pipeline, in parallel with the copies and kernels of earlier chunks.
+class HostPool {
+ public:
+  explicit HostPool(int workers) {
+    for (int i = 0; i < workers; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  int size() const { return (int)threads_.size() + 1; }
+  void run(const std::function<void(int)>& fn, int parts) {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      fn_ = &fn;
+      parts_ = parts;
+      next_ = 0;
+      left_ = parts;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(mu_);
+    done_.wait(l, [this] { return left_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      int part;
+      const std::function<void(int)>* fn;
+      {
+        std::lock_guard<std::mutex> l(mu_);
+        if (!fn_ || next_ >= parts_) return;
+        part = next_++;
+        fn = fn_;
+      }
+      (*fn)(part);
+      std::lock_guard<std::mutex> l(mu_);
+      if (--left_ == 0) done_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int parts_ = 0, next_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 struct ls_ctx {
@@ -75,6 +150,7 @@ struct ls_ctx {
   bool smem_gate = false;
   int64_t blocks_tma = 0, blocks_generic = 0;
   int tma_per_sm = 1;
+  size_t sweep_smem = 0;  // dynamic shared memory sweep_kernel may use
   std::atomic<int> reserved_sms{0};  // SMs the persistent kernels leave free (ls_reserve_sms)
   uint64_t space_size = 0;
   // on-device candidate streams, built lazily per mode
@@ -82,6 +158,11 @@ struct ls_ctx {
   GenMeta gen[4] = {};
   bool gen_ready[4] = {};
   uint32_t* gen_tabs[4] = {};
+  // scalar seam: host-mapped verdict block, own stream
+  std::mutex one_mu;
+  OneOut* one = nullptr;  // pinned + mapped (UVA: the same pointer on the device)
+  cudaStream_t one_stream = nullptr;
+  uint32_t one_seq = 0;
   // host pipeline
   std::mutex host_mu;
   int64_t host_chunk = int64_t(1) << kHostChunkLog2;
@@ -90,6 +171,14 @@ struct ls_ctx {
   uint8_t* h_planes[kPipe] = {};
   uint8_t* h_reason[kPipe] = {};
   double* h_f[kPipe][6] = {};
+  // compact host results: valid raws per slot, their count, pinned staging
+  double* d_vraw[kPipe] = {};
+  int64_t* d_vcnt[kPipe] = {};
+  void* d_cscr[kPipe] = {};
+  uint64_t* hp_words[kPipe] = {};  // pinned: host-packed candidate words of the slot's chunk
+  int64_t* hp_cnt = nullptr;       // pinned [kPipe]
+  cudaEvent_t ev_in[kPipe] = {}, ev_cnt[kPipe] = {};
+  HostPool* pool = nullptr;
 };
 
 namespace {
@@ -325,6 +414,7 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
   // the workload's tables go to shared memory when they fit beside the ring
   // at the kernel's CTAs-per-SM; otherwise both passes read them through L1
   c->smem_gate = tma_smem_bytes(c->L, c->desc.vector_length, true) <= tma_smem_budget(prop);
+  c->sweep_smem = prepare_sweep_kernels((size_t)prop.sharedMemPerBlockOptin);
   if (c->desc.vector_length <= 16) {
     prepare_eval_kernels(c->L, c->desc.vector_length, c->smem_gate);
     c->tma_per_sm = std::max(1, tma_blocks_per_sm(c->L, c->desc.vector_length, c->smem_gate));
@@ -357,7 +447,19 @@ int ls_ctx_destroy(ls_ctx* c) {
     cudaFree(c->h_reason[s]);
     for (int f = 0; f < 6; ++f) cudaFree(c->h_f[s][f]);
   }
+  for (int s = 0; s < kPipe; ++s) {
+    cudaFree(c->d_vraw[s]);
+    cudaFree(c->d_vcnt[s]);
+    cudaFree(c->d_cscr[s]);
+    if (c->hp_words[s]) cudaFreeHost(c->hp_words[s]);
+    if (c->ev_in[s]) cudaEventDestroy(c->ev_in[s]);
+    if (c->ev_cnt[s]) cudaEventDestroy(c->ev_cnt[s]);
+  }
+  if (c->hp_cnt) cudaFreeHost(c->hp_cnt);
+  delete c->pool;
   for (int m = 0; m < 4; ++m) cudaFree(c->gen_tabs[m]);
+  if (c->one_stream) cudaStreamDestroy(c->one_stream);
+  if (c->one) cudaFreeHost(c->one);
   cudaFree(c->d_tab);
   delete c;
   return LS_OK;
@@ -526,6 +628,171 @@ static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_st
   return LS_OK;
 }
 
+// Host planes -> packed candidate words (the ls_pack / pack4_kernel rule:
+// a head out of range gives an all-ones word, which decodes as an error),
+// vectorisable blocks of 256 candidates.
+static void pack_host_range(const uint8_t* planes, int64_t stride, int A, const PackMeta& pk, int64_t lo, int64_t hi,
+                            uint64_t* out) {
+  constexpr int B = 256;
+  uint64_t y[B];
+  uint32_t bad[B];
+  for (int64_t i0 = lo; i0 < hi; i0 += B) {
+    const int m = (int)std::min<int64_t>(B, hi - i0);
+    const uint8_t* t = planes + i0;
+    const uint8_t* e = planes + stride + i0;
+    const uint8_t* p = planes + 2 * stride + i0;
+    const uint8_t* b = planes + 3 * stride + i0;
+    for (int j = 0; j < m; ++j) {
+      bad[j] = (uint32_t)(t[j] >= pk.nt) | (uint32_t)(e[j] >= pk.ne) | (uint32_t)(p[j] >= pk.np) |
+               (uint32_t)(b[j] >= pk.nb);
+      y[j] = (uint64_t)(((t[j] * pk.ne + e[j]) * pk.np + p[j]) * pk.nb + b[j]) << 24;
+    }
+    for (int h = 4; h < A; ++h) {
+      const uint8_t* v = planes + (int64_t)h * stride + i0;
+      const int sh = 2 * (h - 4);
+      for (int j = 0; j < m; ++j) {
+        bad[j] |= (uint32_t)(v[j] > 2);
+        y[j] |= (uint64_t)(v[j] & 3u) << sh;
+      }
+    }
+    for (int j = 0; j < m; ++j) out[i0 - lo + j] = bad[j] ? ~0ull : y[j];
+  }
+}
+
+// Chunked host -> device -> compact host results (see ls_evaluate_host_compact).
+static int host_pipeline_compact(ls_ctx* c, int format, const void* host_in, int64_t stride, int64_t n,
+                                 uint8_t* reason_out, double* valid_raw, int64_t capacity, int64_t* valid_count) {
+  std::lock_guard<std::mutex> lock(c->host_mu);
+  DeviceGuard g(c->device);
+  const int A = c->desc.vector_length;
+  const PackMeta pk = pack_meta(c->desc);
+  const int64_t chunk_n = c->host_chunk;
+  cudaError_t e;
+  for (int s = 0; s < c->pipe; ++s) {
+    if (!c->hs[s] && (e = cudaStreamCreateWithFlags(&c->hs[s], cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream create");
+    if (!c->h_planes[s]) {
+      if ((e = cudaMalloc(&c->h_planes[s], (size_t)LS_MAX_HEADS * chunk_n)) != cudaSuccess ||
+          (e = cudaMalloc(&c->h_reason[s], chunk_n)) != cudaSuccess)
+        return cuda_fail(e, "pipeline buffers");
+    }
+    if (!c->h_f[s][0] && (e = cudaMalloc(&c->h_f[s][0], sizeof(double) * chunk_n)) != cudaSuccess)
+      return cuda_fail(e, "pipeline buffers");
+    if (!c->d_vraw[s]) {
+      if ((e = cudaMalloc(&c->d_vraw[s], sizeof(double) * chunk_n)) != cudaSuccess ||
+          (e = cudaMalloc(&c->d_vcnt[s], sizeof(int64_t))) != cudaSuccess ||
+          (e = cudaMalloc(&c->d_cscr[s], compact_scratch_bytes(chunk_n))) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&c->ev_in[s], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&c->ev_cnt[s], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "compact buffers");
+    }
+    if (format == LS_HOST_PLANES && !c->hp_words[s] &&
+        (e = cudaHostAlloc(reinterpret_cast<void**>(&c->hp_words[s]), sizeof(uint64_t) * chunk_n,
+                           cudaHostAllocPortable)) != cudaSuccess)
+      return cuda_fail(e, "pinned staging");
+  }
+  if (!c->hp_cnt && (e = cudaHostAlloc(reinterpret_cast<void**>(&c->hp_cnt), sizeof(int64_t) * kPipe,
+                                       cudaHostAllocPortable)) != cudaSuccess)
+    return cuda_fail(e, "pinned counts");
+  if (format == LS_HOST_PLANES && !c->pool) {
+    int w = (int)std::thread::hardware_concurrency() - 1;
+    if (const char* v = getenv("LS_HOST_THREADS")) w = atoi(v) - 1;
+    c->pool = new HostPool(std::max(0, std::min(w, 255)));
+  }
+  const int64_t nchunks = (n + chunk_n - 1) / chunk_n;
+  int64_t total = 0;
+  int rc = LS_OK;
+  // second half of chunk j: its valid count is known -> copy exactly that many raws
+  auto finish = [&](int64_t j) -> int {
+    const int s = (int)(j % c->pipe);
+    cudaError_t err = cudaEventSynchronize(c->ev_cnt[s]);
+    if (err != cudaSuccess) return cuda_fail(err, "compact count");
+    const int64_t cnt = c->hp_cnt[s];
+    if (total + cnt > capacity) {
+      total += cnt;
+      return fail(LS_ERR_INVALID_ARGUMENT, "valid_raw capacity is smaller than the number of valid candidates");
+    }
+    if (cnt > 0 && (err = cudaMemcpyAsync(valid_raw + total, c->d_vraw[s], sizeof(double) * cnt,
+                                          cudaMemcpyDeviceToHost, c->hs[s])) != cudaSuccess)
+      return cuda_fail(err, "D2H valid raws");
+    total += cnt;
+    return LS_OK;
+  };
+  for (int64_t j = 0; j < nchunks && rc == LS_OK; ++j) {
+    const int s = (int)(j % c->pipe);
+    const int64_t off = j * chunk_n, cnt = std::min<int64_t>(chunk_n, n - off);
+    cudaStream_t st = c->hs[s];
+    const uint64_t* src;
+    if (format == LS_HOST_PLANES) {
+      // the slot's staging buffer is free once its previous H2D finished
+      if (j >= c->pipe && (e = cudaEventSynchronize(c->ev_in[s])) != cudaSuccess) {
+        rc = cuda_fail(e, "staging reuse");
+        break;
+      }
+      const uint8_t* planes = static_cast<const uint8_t*>(host_in) + off;
+      uint64_t* dst = c->hp_words[s];
+      const int parts = std::max(1, std::min<int>(c->pool->size() * 2, (int)(cnt / 8192)));
+      c->pool->run([&](int q) {
+        const int64_t lo = cnt * q / parts, hi = cnt * (q + 1) / parts;
+        pack_host_range(planes, stride, A, pk, lo, hi, dst + lo);
+      }, parts);
+      src = dst;
+    } else {
+      src = static_cast<const uint64_t*>(host_in) + off;
+    }
+    uint64_t* dwords = reinterpret_cast<uint64_t*>(c->h_planes[s]);
+    if ((e = cudaMemcpyAsync(dwords, src, sizeof(uint64_t) * (size_t)cnt, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess ||
+        (e = cudaEventRecord(c->ev_in[s], st)) != cudaSuccess) {
+      rc = cuda_fail(e, "H2D words");
+      break;
+    }
+    EvalArgs a{};
+    a.words = dwords;
+    a.n = cnt;
+    a.stride = cnt;
+    a.reason = c->h_reason[s];
+    a.thr = c->h_f[s][0];
+    a.sparse_thr = true;
+    LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
+    if ((e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, st, &pk)) !=
+            cudaSuccess ||
+        (e = launch_valid_compact(a.reason, a.thr, cnt, c->d_vraw[s], c->d_vcnt[s], c->d_cscr[s], st)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(reason_out + off, a.reason, (size_t)cnt, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(c->hp_cnt + s, c->d_vcnt[s], sizeof(int64_t), cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess ||
+        (e = cudaEventRecord(c->ev_cnt[s], st)) != cudaSuccess) {
+      rc = cuda_fail(e, "compact chunk");
+      break;
+    }
+    if (j >= 1) rc = finish(j - 1);
+  }
+  if (rc == LS_OK && nchunks > 0) rc = finish(nchunks - 1);
+  for (int s = 0; s < c->pipe; ++s) {
+    e = cudaStreamSynchronize(c->hs[s]);
+    if (rc == LS_OK && e != cudaSuccess) rc = cuda_fail(e, "pipeline sync");
+  }
+  if (valid_count) *valid_count = total;
+  return rc;
+}
+
+int ls_evaluate_host_compact(ls_ctx* c, int format, const void* host_in, int64_t n, int64_t plane_stride,
+                             uint8_t* reason_out, double* valid_raw, int64_t capacity, int64_t* valid_count) {
+  g_err.clear();
+  if (!c || n < 0 || capacity < 0 || (format != LS_HOST_PLANES && format != LS_HOST_WORDS))
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host_compact arguments");
+  if (valid_count) *valid_count = 0;
+  if (n == 0) return LS_OK;
+  if (!host_in || !reason_out || (capacity > 0 && !valid_raw) || (format == LS_HOST_PLANES && plane_stride < n))
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_host_compact arguments");
+  if (c->desc.vector_length > 16 || c->blocks_tma == 0)
+    return fail(LS_ERR_UNSUPPORTED, "compact host results need vectors of <= 16 heads");
+  if (format == LS_HOST_WORDS && ((uintptr_t)host_in % 8) != 0)
+    return fail(LS_ERR_INVALID_ARGUMENT, "packed words must be 8-byte aligned");
+  return host_pipeline_compact(c, format, host_in, plane_stride, n, reason_out, valid_raw, capacity, valid_count);
+}
+
 int ls_host_alloc(size_t bytes, void** out) {
   g_err.clear();
   if (!out) return fail(LS_ERR_INVALID_ARGUMENT, "null out");
@@ -688,6 +955,56 @@ int ls_env_step(ls_ctx* c, const ls_search_state* st, const int64_t* action, dou
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "env_step launch");
 }
 
+int ls_evaluate_one(ls_ctx* c, const uint8_t* vector, uint8_t* reason_out, double* fields_out) {
+  g_err.clear();
+  if (!c || !vector || !reason_out) return fail(LS_ERR_INVALID_ARGUMENT, "null evaluate_one argument");
+  std::lock_guard<std::mutex> lock(c->one_mu);
+  DeviceGuard g(c->device);
+  cudaError_t e;
+  if (!c->one) {
+    if ((e = cudaStreamCreateWithFlags(&c->one_stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream create");
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&c->one), sizeof(OneOut), cudaHostAllocMapped)) != cudaSuccess)
+      return cuda_fail(e, "mapped verdict block");
+    std::memset(c->one, 0, sizeof(OneOut));
+  }
+  OneArgs a{};
+  std::memcpy(a.vec, vector, (size_t)c->desc.vector_length);
+  a.out = c->one;
+  a.seq = ++c->one_seq;
+  if (a.seq == 0) a.seq = c->one_seq = 1;
+  if ((e = launch_eval_one(c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, c->one_stream)) !=
+      cudaSuccess)
+    return cuda_fail(e, "evaluate_one launch");
+  volatile OneOut* o = c->one;
+  for (uint64_t spins = 0; o->seq != a.seq; ++spins) {
+    if ((spins & 0xfff) == 0xfff) {  // a failed kernel never writes the word
+      e = cudaStreamQuery(c->one_stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_fail(e, "evaluate_one");
+      if (e == cudaSuccess && o->seq != a.seq) return fail(LS_ERR_CUDA, "evaluate_one: verdict never arrived");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  *reason_out = (uint8_t)o->reason;
+  if (fields_out)
+    for (int f = 0; f < 6; ++f) fields_out[f] = o->f[f];
+  return LS_OK;
+}
+
+int ls_sa_chain(ls_ctx* c, const ls_sa_plan* p, void* stream) {
+  g_err.clear();
+  if (!c || !p || p->steps < 1 || p->moves < 0 || !p->init || (p->steps > 1 && (!p->u || !p->temperature)) ||
+      (p->moves > 0 && p->steps > 1 && (!p->coords || !p->drawn)))
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad sa plan");
+  const ls_search_state& s = p->env;
+  if (!s.best_raw || !s.log_pos || !s.log_vec || !s.log_raw || !s.log_reward || !s.log_reason)
+    return fail(LS_ERR_INVALID_ARGUMENT, "incomplete search state");
+  DeviceGuard g(c->device);
+  cudaError_t e = launch_sa_chain(c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, *p,
+                                  static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "sa_chain launch");
+}
+
 int ls_policy_layout_of(const ls_policy_dims* dims, ls_policy_layout* out) {
   g_err.clear();
   if (!dims || !out || !ppo_layout(*dims, out)) return fail(LS_ERR_INVALID_ARGUMENT, "bad policy dims");
@@ -814,7 +1131,10 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
     return LS_OK;
   }
   LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
-  const int64_t grid = ws_grid(lp, n, mode);
+  const GenMeta& gen = c->gen[mode];
+  lp.sweep_fits = sweep_smem_bytes(c->L, gen.axis_size / gen.lo_size, gen.lo_size) <= c->sweep_smem;
+  if (lp.sweep_fits) lp.max_blocks = tma_grid_cap(c) / c->tma_per_sm;  // one sweep CTA per SM
+  const int64_t grid = lp.sweep_fits ? sweep_grid(lp, n) : ws_grid(lp, n, mode);
   TopkArgs tk = fused_topk_args(scratch, grid, k, start, topk_out, count_out);
   cudaError_t e;
   if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=

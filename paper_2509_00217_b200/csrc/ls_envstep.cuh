@@ -17,6 +17,41 @@
 
 namespace ls {
 
+// Score one index vector (A indices, each checked against its head size like
+// decode_strategy, strategy.py:245-263): gate() then full_path() — the same
+// code as the batched kernels. mem: memory_bytes as SimResult carries it.
+template <bool NEU, bool LDG, typename V>
+__device__ __forceinline__ void score_vector(const uint64_t* __restrict__ tab, const TabLayout& L,
+                                             const EvalMeta& M, const V* vec, Verdict& v, double& mem) {
+  uint32_t bad = 0, Y = 0;
+  int idx[4] = {0, 0, 0, 0};
+  for (int h = 0; h < M.A; ++h) {
+    const int x = (int)vec[h];
+    bad |= (x < 0 || x >= (int)M.head_size[h]) ? 1u : 0u;
+    const uint32_t byte = (uint32_t)(x & 0xff);
+    if (h < 4) {
+      idx[h] = (int)byte;
+    } else {
+      const int slot = M.head_slot[h];
+      if (slot >= 0) Y |= (byte & 3u) << (2 * slot);
+    }
+  }
+  v.thr = v.tpot = v.comp = v.comm = v.pipe = 0.0;
+  mem = 0.0;
+  if (bad) {
+    v.reason = LS_REASON_DECODE_ERROR;
+    return;
+  }
+  Decoded c;
+  c.t = idx[0];
+  c.e = idx[1];
+  c.p = idx[2];
+  c.b = idx[3];
+  c.Y = Y;
+  v.reason = gate(tab, L, M, c, mem);
+  if (v.reason == LS_REASON_NONE) full_path<NEU, LDG>(tab, L, M, c, v);
+}
+
 // Thread-0 core. ev/er: the elite buffer (shared-memory copy); returns true
 // when the buffer changed. tab is global (LDG) or a shared-memory copy.
 template <bool NEU, bool LDG>
@@ -30,35 +65,10 @@ __device__ __noinline__ bool env_step_core(const uint64_t* __restrict__ tab, con
     *reward_out = __longlong_as_double(0x7ff8000000000000LL);
     return false;
   }
-  // decode the action (indices in range for its head) into (t, e, p, b, Y)
-  uint32_t bad = 0, Y = 0;
-  int idx[4] = {0, 0, 0, 0};
-  for (int h = 0; h < A; ++h) {
-    const int v = action[h];
-    bad |= (v < 0 || v >= (int)M.head_size[h]) ? 1u : 0u;
-    const uint32_t byte = (uint32_t)(v & 0xff);
-    if (h < 4) {
-      idx[h] = (int)byte;
-    } else {
-      const int slot = M.head_slot[h];
-      if (slot >= 0) Y |= (byte & 3u) << (2 * slot);
-    }
-  }
   Verdict v;
-  v.thr = v.tpot = v.comp = v.comm = v.pipe = 0.0;
-  if (bad) {
-    v.reason = LS_REASON_DECODE_ERROR;
-  } else {
-    Decoded c;
-    c.t = idx[0];
-    c.e = idx[1];
-    c.p = idx[2];
-    c.b = idx[3];
-    c.Y = Y;
-    double mem = 0.0;
-    v.reason = gate(tab, L, M, c, mem);
-    if (v.reason == LS_REASON_NONE) full_path<NEU, LDG>(tab, L, M, c, v);
-  }
+  double mem;
+  score_vector<NEU, LDG>(tab, L, M, action, v, mem);
+  const bool bad = v.reason == LS_REASON_DECODE_ERROR;
   const bool valid = v.reason == LS_REASON_NONE;
   double raw = 0.0, reward;
   if (valid) {

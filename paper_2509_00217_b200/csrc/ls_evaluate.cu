@@ -331,23 +331,27 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
   }
 }
 
-// Named barrier 1 over the work warps (gate + fp64; the producer has exited).
-__device__ __forceinline__ void bar_work() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWorkWarps) : "memory"); }
+// Named barrier 1 over the NW work warps (in eval_ws_kernel the producer warp
+// has exited; the sweep kernel has no other warps).
+template <int NW>
+__device__ __forceinline__ void bar_n() { asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory"); }
+__device__ __forceinline__ void bar_work() { bar_n<kWorkWarps>(); }
 
 // Tree merge of the work warps' register lists through shared slots
-// ([kWorkWarps][32] Rec): log2(kWorkWarps) levels, warp 0 ends with the
-// merged list. Records below the floor (fk, fi) are skipped (at_least()).
+// ([NW][32] Rec): log2(NW) levels, warp 0 ends with the merged list. Records
+// below the floor (fk, fi) are skipped (at_least()).
+template <int NW>
 __device__ __forceinline__ void tree_merge(RegList& wl, Rec* slots, int* cnt, int warp, int k, double fk,
                                            int64_t fi = INT64_MAX) {
   wl.store(slots + warp * 32, &cnt[warp]);
-  bar_work();
+  bar_n<NW>();
 #pragma unroll 1
-  for (int st = 1; st < kWorkWarps; st <<= 1) {
-    if ((warp & (2 * st - 1)) == 0 && warp + st < kWorkWarps && cnt[warp + st] > 0) {
+  for (int st = 1; st < NW; st <<= 1) {
+    if ((warp & (2 * st - 1)) == 0 && warp + st < NW && cnt[warp + st] > 0) {
       wl.absorb(slots + (warp + st) * 32, cnt[warp + st], k, fk, fi);
       wl.store(slots + warp * 32, &cnt[warp]);
     }
-    bar_work();
+    bar_n<NW>();
   }
 }
 
@@ -459,23 +463,25 @@ __device__ __forceinline__ void warp_merge_lists(const Rec* win, int stride, con
 // window a single warp merges the lists (warp_merge_lists); otherwise the
 // window is cut by the exact (key, index) floor, every warp offers its share
 // to its own list and the warp lists tree-merge into tk.out.
+// NW work warps; smem: REGION bytes of shared memory free for the merge.
+template <int NW, uint32_t REGION>
 __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt, int warp, const TopkArgs& tk) {
-  constexpr int kThr = 32 * kWorkWarps;
+  constexpr int kThr = 32 * NW;
   const int lane = threadIdx.x & 31, tid = warp * 32 + lane, k = tk.k, m = (int)gridDim.x;
-  Rec* slots = reinterpret_cast<Rec*>(smem);  // [kWorkWarps][32]
-  int* wcnt = reinterpret_cast<int*>(smem + kWorkWarps * 32 * sizeof(Rec));
-  Rec* win = reinterpret_cast<Rec*>(smem + kWorkWarps * 32 * sizeof(Rec) + 512 * sizeof(int));
-  const int cap = (int)((kRingBytes - kWorkWarps * 32 * sizeof(Rec) - 512 * sizeof(int)) / sizeof(Rec));
+  Rec* slots = reinterpret_cast<Rec*>(smem);  // [NW][32]
+  int* wcnt = reinterpret_cast<int*>(smem + NW * 32 * sizeof(Rec));
+  Rec* win = reinterpret_cast<Rec*>(smem + NW * 32 * sizeof(Rec) + 512 * sizeof(int));
+  const int cap = (int)((REGION - NW * 32 * sizeof(Rec) - 512 * sizeof(int)) / sizeof(Rec));
   const int lists_per_win = cap / k < 512 ? cap / k : 512;
-  __shared__ double s_fk[kWorkWarps];
-  __shared__ int64_t s_fi[kWorkWarps];
+  __shared__ double s_fk[NW];
+  __shared__ int64_t s_fi[NW];
   double fk = m <= lists_per_win ? 0.0 : read_floor(tk.floor);
   int64_t fi = INT64_MAX;
   wl.init();
   for (int l0 = 0; l0 < m; l0 += lists_per_win) {
     const int nl = m - l0 < lists_per_win ? m - l0 : lists_per_win;
     for (int i = tid; i < nl; i += kThr) wcnt[i] = __ldcg(tk.part_counts + l0 + i);
-    bar_work();
+    bar_n<NW>();
     for (int i = tid; i < nl * k; i += kThr) {
       const int l = i / k, j = i - l * k;
       Rec r{-1.0e308, 0.0, INT64_MAX, 0};
@@ -487,7 +493,7 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
       }
       win[i] = r;
     }
-    bar_work();
+    bar_n<NW>();
     if (nl == m) {  // every list is staged: one warp merges them, no block-wide rounds
       if (tid == 0) LS_STAMP(8);
       if (warp == 0) {  // scratch for the heads: the (unused) warp-slot area
@@ -522,8 +528,8 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
       s_fk[warp] = fk;
       s_fi[warp] = fi;
     }
-    bar_work();
-    for (int o = 0; o < kWorkWarps; ++o)
+    bar_n<NW>();
+    for (int o = 0; o < NW; ++o)
       if (better(s_fk[o], s_fi[o], fk, fi)) {
         fk = s_fk[o];
         fi = s_fi[o];
@@ -538,12 +544,55 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
       }
       wl.offer(have, r, k);
     }
-    bar_work();
+    bar_n<NW>();
   }
-  tree_merge(wl, slots, cnt, warp, k, fk, fi);
+  tree_merge<NW>(wl, slots, cnt, warp, k, fk, fi);
   if (warp == 0) wl.emit(tk.out, tk.count_out);
 }
 
+
+// End of a fused evaluate + elite kernel (all NW work warps call it): every
+// warp's list to shared memory, warp 0 merges them into this CTA's list and
+// publishes it; the last CTA to finish merges every CTA's list into tk.out
+// and zeroes the sync words for the next call on this scratch.
+template <int NW, uint32_t REGION>
+__device__ __forceinline__ void elite_epilogue(RegList& wl, uint8_t* region, int* list_count, int warp,
+                                               const TopkArgs& tk) {
+  Rec* slots = reinterpret_cast<Rec*>(region);
+  wl.store(slots + warp * 32, &list_count[warp]);
+  bar_n<NW>();
+  __shared__ int s_cur[NW];
+  __shared__ double s_hk[NW];
+  __shared__ int64_t s_hx[NW];
+  __shared__ int s_last;
+  if (warp == 0) {
+    warp_merge_lists(slots, 32, list_count, NW, tk.k, tk.part + (int64_t)blockIdx.x * tk.k,
+                     tk.part_counts + blockIdx.x, s_cur, s_hk, s_hx);
+    if ((threadIdx.x & 31) == 0) LS_STAMP(5);
+    __threadfence();  // this CTA's list is visible device-wide before it is counted
+    unsigned t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(tk.done, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if ((threadIdx.x & 31) == 0) s_last = t == gridDim.x - 1;
+  }
+  bar_n<NW>();
+#ifdef LS_DIAG_NOFINAL
+  if (false) {
+#else
+  if (s_last) {  // the last CTA merges every CTA's list (L2-resident, no second launch)
+#endif
+    if (warp == 0 && (threadIdx.x & 31) == 0) LS_STAMP(6);
+    __threadfence();
+    final_merge<NW, REGION>(wl, region, list_count, warp, tk);
+    if (warp == 0 && (threadIdx.x & 31) == 0) {
+      LS_STAMP(7);
+      // every other CTA is past its last floor read and done increment:
+      // leave the sync words zero for the next call on this scratch
+      *tk.floor = 0ull;
+      *tk.done = 0u;
+    }
+  }
+}
 
 template <bool NEU, bool FULL, bool SMEM_GATE, bool TOPK, int MODE>
 __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
@@ -772,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         // coalesced 512-byte stores (every lane of a full tile has count 4;
         // survivors' values are stored later by the fp64 pass)
         const int64_t wz = base - 4 * lane + 2 * lane;
-        if (a.thr) {
+        if (a.thr && !a.sparse_thr) {
           st2(a.thr, wz, 0.0, 0.0);
           st2(a.thr, wz + 64, 0.0, 0.0);
         }
@@ -792,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
       } else {
         for (int j = 0; j < count; ++j) {
           a.reason[base + j] = (uint8_t)(r4 >> (8 * j));
-          if (a.thr) a.thr[base + j] = 0.0;
+          if (a.thr && !a.sparse_thr) a.thr[base + j] = 0.0;
           if (FULL) {
             if (a.mem) a.mem[base + j] = m[j];
             if (a.tpot) a.tpot[base + j] = 0.0;
@@ -918,40 +967,202 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     if (threadIdx.x == 0) LS_STAMP(4);
     // every warp's list (best-first, distinct vectors) to shared memory; warp 0
     // merges the kWorkWarps lists into this CTA's list (one list per lane)
-    wl.store(slots + warp * 32, &list_count[warp]);
-    bar_work();
-    __shared__ int s_cur[kWorkWarps];
-    __shared__ double s_hk[kWorkWarps];
-    __shared__ int64_t s_hx[kWorkWarps];
-    __shared__ int s_last;
-    if (warp == 0) {
-      warp_merge_lists(slots, 32, list_count, kWorkWarps, tk.k, tk.part + (int64_t)blockIdx.x * tk.k,
-                       tk.part_counts + blockIdx.x, s_cur, s_hk, s_hx);
-      if (lane == 0) LS_STAMP(5);
-      __threadfence();  // this CTA's list is visible device-wide before it is counted
-      unsigned t = 0;
-      if (lane == 0) t = atomicAdd(tk.done, 1u);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (lane == 0) s_last = t == gridDim.x - 1;
-    }
-    bar_work();
-#ifdef LS_DIAG_NOFINAL
-    if (false) {
-#else
-    if (s_last) {  // the last CTA merges every CTA's list (L2-resident, no second launch)
+    (void)slots;
+    elite_epilogue<kWorkWarps, kRingBytes>(wl, S.ring, list_count, warp, tk);
+  }
+}
+
+// ---- sweep_kernel: on-device candidate streams -> elite --------------------
+// The generated-candidate sweeps (ls_sweep: uniform stream, full and
+// admissible enumeration) read nothing per candidate, and in the enumeration
+// modes most candidates survive the gates (~60% of the admissible space takes
+// the full fp64 plan walk), so the warp-specialised streaming design of
+// eval_ws_kernel (TMA ring, gate warps handing survivors to a few fp64 warps
+// through mailboxes) does not fit. Here every warp does everything: it
+// generates 32 consecutive stream positions at a time (one per lane), gates
+// them from the shared-memory coarse words, appends the survivors to its own
+// shared-memory queue and scores 32 queued survivors at once in place
+// (full_path from the shared-memory table), offering the valid ones to its
+// register elite list. No ring, no mailboxes, no idle roles; one CTA of
+// kSwWarps warps per SM.
+#ifndef LS_SWEEP_WARPS
+#define LS_SWEEP_WARPS 24
 #endif
-      if (threadIdx.x == 0) LS_STAMP(6);
-      __threadfence();
-      final_merge(wl, S.ring, list_count, warp, tk);
-      if (threadIdx.x == 0) {
-        LS_STAMP(7);
-        // every other CTA is past its last floor read and done increment:
-        // leave the sync words zero for the next call on this scratch
-        *tk.floor = 0ull;
-        *tk.done = 0u;
+constexpr int kSwWarps = LS_SWEEP_WARPS;
+constexpr int kSwThreads = 32 * kSwWarps;
+constexpr int kSwChunk = 256;  // consecutive stream positions per warp chunk
+constexpr int kSwQueue = 64;   // survivor queue per warp (< 32 left over + 32 new)
+constexpr uint32_t kSwMergeBytes = 64 * 1024;  // shared memory the end-of-kernel merges use (aliases the tables)
+static_assert(kSwWarps * 32 * sizeof(Rec) + 512 * sizeof(int) + 64 * sizeof(Rec) <= kSwMergeBytes, "merge region");
+
+// Shared-memory layout of sweep_kernel: workload table, the stream's two
+// axis tables, per-warp survivor queues.
+struct SwLayout {
+  uint32_t tab, gen_hi, gen_lo, qkey, qy, bytes;
+};
+__host__ __device__ inline SwLayout sw_layout(const TabLayout& L, uint32_t hi_size, uint32_t lo_size) {
+  SwLayout o;
+  o.tab = 0;
+  o.gen_hi = (uint32_t)L.words * 8u;
+  o.gen_lo = o.gen_hi + 4u * hi_size;
+  o.qkey = (o.gen_lo + 4u * lo_size + 15u) & ~15u;
+  o.qy = o.qkey + 8u * kSwWarps * kSwQueue;
+  o.bytes = o.qy + 4u * kSwWarps * kSwQueue;
+  if (o.bytes < kSwMergeBytes) o.bytes = kSwMergeBytes;
+  return o;
+}
+
+// Coarse rank -> (t, e, p, b) with the stream's divisors (batch fastest).
+__device__ __forceinline__ void rank_split_g(const GenMeta& g, uint64_t coarse, Decoded& c) {
+  const uint64_t q1 = divq(coarse, g.m_b, g.nb);
+  c.b = (int)(coarse - q1 * g.nb);
+  const uint64_t q2 = divq(q1, g.m_p, g.np);
+  c.p = (int)(q1 - q2 * g.np);
+  const uint64_t q3 = divq(q2, g.m_e, g.ne);
+  c.e = (int)(q2 - q3 * g.ne);
+  c.t = (int)q3;
+}
+
+// gen_candidate with the axis tables in shared memory.
+template <int MODE>
+__device__ __forceinline__ void gen_candidate_s(const GenMeta& g, const uint32_t* hi_tab, const uint32_t* lo_tab,
+                                                uint64_t gidx, Decoded& c) {
+  uint64_t coarse, axis;
+  if (MODE == GEN_UNIFORM) {
+    const uint64_t r1 = splitmix64(g.seed ^ (2 * gidx)), r2 = splitmix64(g.seed ^ (2 * gidx + 1));
+    coarse = __umul64hi(r1, g.coarse_size);
+    axis = __umul64hi(r2, g.axis_size);
+  } else {
+    coarse = divq(gidx, g.m_axis, g.axis_size);
+    axis = gidx - coarse * g.axis_size;
+  }
+  const uint64_t hi = divq(axis, g.m_lo, g.lo_size), lo = axis - hi * g.lo_size;
+  c.Y = hi_tab[hi] | lo_tab[lo];
+  const uint64_t q1 = divq(coarse, g.m_b, g.nb);
+  c.b = (int)(coarse - q1 * g.nb);
+  const uint64_t q2 = divq(q1, g.m_p, g.np);
+  c.p = (int)(q1 - q2 * g.np);
+  const uint64_t q3 = divq(q2, g.m_e, g.ne);
+  c.e = (int)(q2 - q3 * g.ne);
+  c.t = (int)q3;
+}
+
+template <bool NEU, int MODE>
+__global__ void __launch_bounds__(kSwThreads, 1)
+    sweep_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const int64_t n,
+                 const TopkArgs tk, const GenMeta gm, const SwLayout SL) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t tab_bar;
+  __shared__ int list_count[kSwWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* T = reinterpret_cast<uint64_t*>(smem + SL.tab);
+  uint32_t* hi_s = reinterpret_cast<uint32_t*>(smem + SL.gen_hi);
+  uint32_t* lo_s = reinterpret_cast<uint32_t*>(smem + SL.gen_lo);
+  uint64_t* qkey = reinterpret_cast<uint64_t*>(smem + SL.qkey) + warp * kSwQueue;
+  uint32_t* qy = reinterpret_cast<uint32_t*>(smem + SL.qy) + warp * kSwQueue;
+  if (threadIdx.x == 0) {
+    mbar_init(&tab_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bytes = (uint32_t)L.words * 8u;
+    mbar_expect_tx(&tab_bar, bytes);
+    bulk_g2s(T, gtab, bytes, &tab_bar);
+  }
+  if (threadIdx.x < kSwWarps) list_count[threadIdx.x] = 0;
+  const uint32_t hi_size = (uint32_t)(gm.axis_size / gm.lo_size);
+  for (uint32_t i = threadIdx.x; i < hi_size; i += kSwThreads) hi_s[i] = gm.hi_tab[i];
+  for (uint32_t i = threadIdx.x; i < (uint32_t)gm.lo_size; i += kSwThreads) lo_s[i] = gm.lo_tab[i];
+  __syncthreads();
+  mbar_wait(&tab_bar, 0);
+  if (threadIdx.x == 0) LS_STAMP(1);
+
+  const uint32_t* Cg = reinterpret_cast<const uint32_t*>(T + L.coarse);
+  const bool coarse = L.coarse_words > 0;
+  EvalArgs a{};  // no per-candidate verdicts: only the elite leaves the SM
+  RegList wl;
+  wl.init();
+  double gfloor = -1.0e308, gpend = -1.0e308;
+  int qcount = 0;  // warp-uniform
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t nchunks = (n + kSwChunk - 1) / kSwChunk;
+  const uint32_t lo_size = (uint32_t)gm.lo_size;
+  for (int64_t ch = (int64_t)blockIdx.x * kSwWarps + warp; ch < nchunks; ch += (int64_t)gridDim.x * kSwWarps) {
+    const int64_t base = ch * kSwChunk;
+    // enumeration: decode the lane's first position once, then step the
+    // mixed-radix digits (coarse rank, high / low axis rank) by 32 per round
+    uint64_t crank = 0;
+    uint32_t ahi = 0, alo = 0;
+    Decoded c;
+    if (MODE != GEN_UNIFORM) {
+      const int64_t i0 = base + lane < n ? base + lane : n - 1;
+      const uint64_t g0 = (uint64_t)(gm.start + i0);
+      crank = divq(g0, gm.m_axis, gm.axis_size);
+      const uint64_t axis = g0 - crank * gm.axis_size;
+      const uint64_t hi = divq(axis, gm.m_lo, gm.lo_size);
+      ahi = (uint32_t)hi;
+      alo = (uint32_t)(axis - hi * gm.lo_size);
+      rank_split_g(gm, crank, c);
+    }
+#pragma unroll 1
+    for (int j = 0; j < kSwChunk / 32; ++j) {
+      const int64_t i = base + j * 32 + lane;
+      const bool in = i < n;
+      if (MODE == GEN_UNIFORM) {
+        gen_candidate_s<MODE>(gm, hi_s, lo_s, (uint64_t)(gm.start + (in ? i : n - 1)), c);
+      } else {
+        if (j > 0 && in) {  // advance by 32 positions (past-the-end lanes keep their last candidate)
+          alo += 32;
+          while (alo >= lo_size) {
+            alo -= lo_size;
+            if (++ahi * gm.lo_size >= gm.axis_size) {
+              ahi = 0;
+              rank_split_g(gm, ++crank, c);
+            }
+          }
+        }
+        c.Y = hi_s[ahi] | lo_s[alo];
+      }
+      uint32_t reason;
+      if (coarse) {
+        reason = MODE == GEN_UNIFORM ? gate_coarse(Cg, L, M, c) : gate_rank(Cg, M, (uint32_t)crank, c.Y);
+      } else {
+        double m;
+        reason = gate(T, L, M, c, m);
+      }
+      const bool sv = in && reason == LS_REASON_NONE;
+      const uint32_t b = __ballot_sync(0xffffffffu, sv);
+      if (b) {
+        if (sv) {
+          const int pos = qcount + __popc(b & lt);
+          qkey[pos] = pack_key(i, c);
+          qy[pos] = c.Y;
+        }
+        qcount += __popc(b);
+        if (qcount >= 32) {  // score the newest 32 in place
+          __syncwarp();
+          qcount -= 32;
+          fp64_batch<NEU, false, true, MODE, true>(T, L, M, a, tk, qkey + qcount, qy + qcount, 32, wl, gfloor, gpend,
+                                                  gm.pk);
+          __syncwarp();
+        }
       }
     }
   }
+  if (qcount > 0) {
+    __syncwarp();
+    fp64_batch<NEU, false, true, MODE, true>(T, L, M, a, tk, qkey, qy, qcount, wl, gfloor, gpend, gm.pk);
+  }
+  if (threadIdx.x == 0) LS_STAMP(2);
+  bar_n<kSwWarps>();  // the merge region aliases the tables every warp reads until here
+  elite_epilogue<kSwWarps, kSwMergeBytes>(wl, smem, list_count, warp, tk);
+}
+
+template <bool NEU, int MODE>
+void launch_sweep_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, int64_t n,
+                    const TopkArgs& tk, const GenMeta& gm, cudaStream_t s) {
+  const SwLayout SL = sw_layout(L, (uint32_t)(gm.axis_size / gm.lo_size), (uint32_t)gm.lo_size);
+  const int64_t blocks = sweep_grid(lp, n);
+  sweep_kernel<NEU, MODE><<<(unsigned)blocks, kSwThreads, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL);
 }
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
@@ -1163,6 +1374,34 @@ int generic_blocks_per_sm() {
   return nb;
 }
 
+int64_t sweep_grid(const LaunchPlan& lp, int64_t n) {
+  const int64_t chunks = (n + kSwChunk - 1) / kSwChunk;
+  int64_t blocks = (chunks + kSwWarps - 1) / kSwWarps;
+  if (blocks < 1) blocks = 1;
+  // one CTA per SM: the cap counts the eval_ws_kernel's CTAs per SM, the same or more
+  return blocks > lp.max_blocks ? lp.max_blocks : blocks;
+}
+
+size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size) {
+  return sw_layout(L, (uint32_t)hi_size, (uint32_t)lo_size).bytes;
+}
+
+// Opt every sweep kernel into the largest dynamic shared memory the device
+// allows beside its static shared memory; returns that dynamic budget.
+size_t prepare_sweep_kernels(size_t optin) {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, sweep_kernel<true, GEN_ENUM_ADMISSIBLE>);
+  const size_t budget = optin > fa.sharedSizeBytes + 1024 ? optin - fa.sharedSizeBytes - 1024 : 0;
+  const int b = (int)budget;
+  cudaFuncSetAttribute(sweep_kernel<true, GEN_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(sweep_kernel<true, GEN_ENUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(sweep_kernel<true, GEN_ENUM_ADMISSIBLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(sweep_kernel<false, GEN_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(sweep_kernel<false, GEN_ENUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(sweep_kernel<false, GEN_ENUM_ADMISSIBLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  return cudaGetLastError() == cudaSuccess ? budget : 0;
+}
+
 int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode) {
   // memory-fed modes: whole tiles (the ragged tail rides on one CTA); generated: ceil
   const int64_t ntiles = (mode == GEN_PLANES || mode == GEN_WORDS) ? n / kTile : (n + kTile - 1) / kTile;
@@ -1218,11 +1457,23 @@ cudaError_t launch_sweep(const LaunchPlan& lp, bool neumaier, int mode, const ui
                          const EvalMeta& M, int64_t n, const TopkArgs& tk, const GenMeta& gm, cudaStream_t s) {
   EvalArgs a{};
   a.n = n;  // no planes, no per-candidate verdicts: only the fused elite leaves the SMs
+  (void)a;
   auto go = [&](auto neu) {
     constexpr bool NEU = decltype(neu)::value;
+#ifndef LS_SWEEP_WS  // LS_SWEEP_WS: A/B builds of the streaming kernel's generator modes
+    if (!lp.sweep_fits)
+#endif
+    {
     if (mode == GEN_UNIFORM) launch_ws_t<NEU, false, true, GEN_UNIFORM>(lp, tab, L, M, a, tk, s, gm);
     else if (mode == GEN_ENUM) launch_ws_t<NEU, false, true, GEN_ENUM>(lp, tab, L, M, a, tk, s, gm);
     else launch_ws_t<NEU, false, true, GEN_ENUM_ADMISSIBLE>(lp, tab, L, M, a, tk, s, gm);
+    return;
+    }
+#ifndef LS_SWEEP_WS
+    if (mode == GEN_UNIFORM) launch_sweep_t<NEU, GEN_UNIFORM>(lp, tab, L, M, n, tk, gm, s);
+    else if (mode == GEN_ENUM) launch_sweep_t<NEU, GEN_ENUM>(lp, tab, L, M, n, tk, gm, s);
+    else launch_sweep_t<NEU, GEN_ENUM_ADMISSIBLE>(lp, tab, L, M, n, tk, gm, s);
+#endif
   };
   if (neumaier) go(std::true_type{});
   else go(std::false_type{});

@@ -23,17 +23,25 @@ struct Verdict {
 };
 
 // CPython builtin sum() over floats with int start 0: Neumaier compensation
-// from 3.12 (NEU) or the naive left fold before it.
+// from 3.12 (NEU) or the naive left fold before it. CPython adds the first
+// float to the int 0 exactly (0 + x == x) and compensates from the second
+// on; starting from f = c = 0 and compensating every add gives the same bits
+// (the first add's error is exactly 0), so there is no first-element case.
+// The compensation term is the exact rounding error of f + x. CPython gets it
+// with Fast2Sum after ordering the operands by magnitude
+// (fabs(f) >= fabs(x) ? (f - t) + x : (x - t) + f); Knuth's branch-free
+// TwoSum computes the same exact error (both are exact for finite sums under
+// round-to-nearest), without the compare and selects. Adding 0.0 leaves both
+// f and c unchanged, so an absent term can be added as 0.0 (branch-free).
 template <bool NEU>
 struct PySum {
-  double f, c;
-  __device__ __forceinline__ void first(double x) {
-    f = 0.0 + x;
-    c = 0.0;
-  }
+  double f = 0.0, c = 0.0;
   __device__ __forceinline__ void add(double x) {
     const double t = f + x;
-    if (NEU) c += fabs(f) >= fabs(x) ? (f - t) + x : (x - t) + f;
+    if (NEU) {
+      const double xp = t - f, fp = t - xp;
+      c += (f - fp) + (x - xp);
+    }
     f = t;
   }
   __device__ __forceinline__ double result() const {
@@ -42,25 +50,13 @@ struct PySum {
   }
 };
 
-template <bool NEU>
-struct Accum {
-  PySum<NEU> s;
-  int n;
-  __device__ __forceinline__ void init() { n = 0; }
-  __device__ __forceinline__ void push(double x) {
-    if (n++ == 0) s.first(x);
-    else s.add(x);
-  }
-  __device__ __forceinline__ double result() const { return n ? s.result() : 0.0; }
-};
-
 // Collective family of reconciling producer state `from` to demand `to`
 // (transition, layout.py:119-155; states are axis codes, see ST_*):
 // R->* none, S->S none, S->R all_gather, P->S reduce_scatter, P->R all_reduce.
+// As a 2-bit table indexed by 3*from + to: (P,R) -> AR, (P,S) -> ONCE, (S,R) -> ONCE.
 __device__ __forceinline__ int fam(int from, int to) {
-  if (from == ST_R) return FAM_NONE;
-  if (from == ST_S) return to == ST_S ? FAM_NONE : FAM_ONCE;
-  return to == ST_S ? FAM_ONCE : FAM_AR;
+  constexpr uint32_t kFam = (FAM_AR << 6) | (FAM_ONCE << 10) | (FAM_ONCE << 12);
+  return (int)((kFam >> (2 * (3 * from + to))) & 3u);
 }
 // Input demanded by a matmul under `axis` (_required_input, layout.py:194-197).
 __device__ __forceinline__ int req(int axis) { return axis == 1 ? ST_S : ST_R; }
@@ -161,60 +157,63 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   const bool tp_gt1 = tpv > 1, ep_gt1 = epv > 1;
 
   // layer plan compute: qkv, kv, attn, out, router, ffn1, ffn2[, sh1, sh2]
-  Accum<NEU> lc;
-  lc.init();
-  lc.push(tget<LDG>(T, L.opt_qkv + ax_qkv * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_kv + a2 * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_attn + a2 * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_out + ax_out * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_router + b));
-  lc.push(tget<LDG>(T, L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
-  lc.push(tget<LDG>(T, L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
+  PySum<NEU> lc;
+  lc.add(tget<LDG>(T, L.opt_qkv + ax_qkv * nt * nb + tb));
+  lc.add(tget<LDG>(T, L.opt_kv + a2 * nt * nb + tb));
+  lc.add(tget<LDG>(T, L.opt_attn + a2 * nt * nb + tb));
+  lc.add(tget<LDG>(T, L.opt_out + ax_out * nt * nb + tb));
+  lc.add(tget<LDG>(T, L.opt_router + b));
+  lc.add(tget<LDG>(T, L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
+  lc.add(tget<LDG>(T, L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
   if (L.has_shared) {
-    lc.push(tget<LDG>(T, L.opt_sh1 + ax_s1 * nt * nb + tb));
-    lc.push(tget<LDG>(T, L.opt_sh2 + ax_s2 * nt * nb + tb));
+    lc.add(tget<LDG>(T, L.opt_sh1 + ax_s1 * nt * nb + tb));
+    lc.add(tget<LDG>(T, L.opt_sh2 + ax_s2 * nt * nb + tb));
   }
-  // layer plan collectives in all_collectives() order (layout.py:270-275)
-  Accum<NEU> lm;
-  lm.init();
-#define LS_TP_COLL(cls, f) tget<LDG>(T, L.coll + ((cls) * 2 + ((f) - 1)) * nt * nb + tb)
+  // layer plan collectives in all_collectives() order (layout.py:270-275);
+  // a collective that is not emitted is added as 0.0 (an exact no-op of the
+  // sum), so the walk is branch-free: (f) ? time : 0.0 from an in-range slot
+  PySum<NEU> lm;
+#define LS_TP_COLL(cls, f) tget<LDG>(T, L.coll + ((cls) * 2 + ((f) - 1 + ((f) == 0))) * nt * nb + tb)
+#define LS_OPT(f, x) ((f) ? (x) : 0.0)
   const int st_attn = a2 ? ST_S : ST_R;
-  if (tp_gt1) {
-    int f;
-    if ((f = fam(ax_qkv, st_attn))) lm.push(LS_TP_COLL(CLS_QKV, f));     // feed attn_core
-    if ((f = fam(st_attn, req(ax_out)))) lm.push(LS_TP_COLL(CLS_H, f));  // feed attn_out_proj
-    if ((f = fam(ax_out, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));          // attention residual
-  }
+  const int tpm = tp_gt1 ? 3 : 0;  // with tp == 1 no TP collective is emitted (fam & 0)
+  int f;
+  f = fam(ax_qkv, st_attn) & tpm;
+  lm.add(LS_OPT(f, LS_TP_COLL(CLS_QKV, f)));  // feed attn_core
+  f = fam(st_attn, req(ax_out)) & tpm;
+  lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));  // feed attn_out_proj
+  f = fam(ax_out, ST_R) & tpm;
+  lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));  // attention residual
   const double a2a = ep_gt1 ? tget<LDG>(T, L.a2a + teb) : 0.0;
-  if (ep_gt1) lm.push(a2a);  // expert dispatch
-  if (tp_gt1) {
-    int f;
-    if ((f = fam(ax_f1, req(ax_f2)))) lm.push(tget<LDG>(T, L.rtf + (f - 1) * nt * ne * nb + teb));  // feed ffn2
-    if (L.has_shared && (f = fam(ax_s1, req(ax_s2)))) lm.push(LS_TP_COLL(CLS_F, f));        // feed sh2
+  lm.add(a2a);  // expert dispatch (0.0 when ep == 1)
+  f = fam(ax_f1, req(ax_f2)) & tpm;
+  lm.add(LS_OPT(f, tget<LDG>(T, L.rtf + (f - 1 + (f == 0)) * nt * ne * nb + teb)));  // feed ffn2
+  if (L.has_shared) {
+    f = fam(ax_s1, req(ax_s2)) & tpm;
+    lm.add(LS_OPT(f, LS_TP_COLL(CLS_F, f)));  // feed sh2
   }
-  if (ep_gt1) lm.push(a2a);  // expert combine
-  if (tp_gt1) {
-    int f;
-    if (L.has_shared && ax_s2 != ax_f2) {  // branch outputs disagree: align both
-      if ((f = fam(ax_f2, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));
-      if ((f = fam(ax_s2, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));
-    } else if ((f = fam(ax_f2, ST_R))) {  // layer exit
-      lm.push(LS_TP_COLL(CLS_H, f));
-    }
+  lm.add(a2a);  // expert combine
+  if (L.has_shared && ax_s2 != ax_f2) {  // branch outputs disagree: align both
+    f = fam(ax_f2, ST_R) & tpm;
+    lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));
+    f = fam(ax_s2, ST_R) & tpm;
+    lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));
+  } else {  // layer exit
+    f = fam(ax_f2, ST_R) & tpm;
+    lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));
   }
   const double layer_c = lc.result(), layer_m = lm.result();
 
   // pre plan (embedding) and post plan (final_norm, lm_head)
   const double pre_c = 0.0 + tget<LDG>(T, L.opt_emb + ax_emb * nt * nb + tb);
-  double pre_m = 0.0, post_m = 0.0;
-  if (tp_gt1) {
-    int f;
-    if ((f = fam(ax_emb, ST_R))) pre_m = 0.0 + LS_TP_COLL(CLS_H, f);
-    if ((f = fam(ax_lmh, ST_R))) post_m = 0.0 + LS_TP_COLL(CLS_V, f);
-  }
+  f = fam(ax_emb, ST_R) & tpm;
+  const double pre_m = 0.0 + LS_OPT(f, LS_TP_COLL(CLS_H, f));
+  f = fam(ax_lmh, ST_R) & tpm;
+  const double post_m = 0.0 + LS_OPT(f, LS_TP_COLL(CLS_V, f));
 #undef LS_TP_COLL
+#undef LS_OPT
   PySum<NEU> po;
-  po.first(tget<LDG>(T, L.opt_norm + b));
+  po.add(tget<LDG>(T, L.opt_norm + b));
   po.add(tget<LDG>(T, L.opt_lmh + ax_lmh * nt * nb + tb));
   const double post_c = po.result();
 

@@ -15,12 +15,14 @@ struct EvalArgs {
   int64_t stride;
   uint8_t* reason;
   double *thr, *tpot, *mem, *comp, *comm, *pipe;
+  bool sparse_thr;  // throughput written for gate survivors only (compact results read it where reason == 0)
 };
 
 struct LaunchPlan {
   bool tma;        // TMA-ring two-pass kernel (aligned planes, A <= 16)
   bool smem_gate;  // gate tables staged into shared memory
   int64_t max_blocks;
+  bool sweep_fits = false;  // ls_sweep: sweep_kernel's tables fit in shared memory (else eval_ws_kernel)
 };
 
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
@@ -74,6 +76,9 @@ cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8
 cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
                         cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode);  // CTAs of one eval_ws_kernel launch
+int64_t sweep_grid(const LaunchPlan& lp, int64_t n);         // CTAs of one sweep_kernel launch (ls_sweep)
+size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size);
+size_t prepare_sweep_kernels(size_t optin);  // -> dynamic shared memory budget of sweep_kernel
 int fused_k_max();
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,
                                  const EvalMeta& M, const EvalArgs& a, const TopkArgs& tk, cudaStream_t s,
@@ -92,6 +97,12 @@ cudaError_t launch_reward_scan(const uint8_t* reason, const double* thr, int64_t
                                double beta, double penalty, double* reward, double* best_out, void* scratch,
                                int num_sms, cudaStream_t s);
 
+// Valid-raw compaction (ls_select.cu): raws of the reason == 0 candidates in
+// index order -> out[0..count), *count_out = count (device int64).
+size_t compact_scratch_bytes(int64_t n);
+cudaError_t launch_valid_compact(const uint8_t* reason, const double* thr, int64_t n, double* out, int64_t* count_out,
+                                 void* scratch, cudaStream_t s);
+
 // Top-k (ls_select.cu)
 struct TopkMeta {
   int A;
@@ -104,6 +115,23 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);
+
+// Scalar seam (ls_search.cu): one vector in the launch parameters, the
+// verdict in host-mapped memory followed by the sequence word.
+struct OneOut {
+  double f[6];  // throughput, tpot, memory, compute, comm, pipeline
+  uint32_t reason;
+  uint32_t seq;
+};
+struct OneArgs {
+  uint8_t vec[LS_MAX_HEADS];
+  OneOut* out;
+  uint32_t seq;
+};
+cudaError_t launch_eval_one(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
+                            const OneArgs& a, cudaStream_t s);
+cudaError_t launch_sa_chain(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
+                            const ls_sa_plan& p, cudaStream_t s);
 
 // Search-loop environment step (ls_search.cu)
 cudaError_t launch_env_step(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,

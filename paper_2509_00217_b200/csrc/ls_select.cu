@@ -401,7 +401,104 @@ __global__ void __launch_bounds__(kMergeThreads) topk_merge_fast_kernel(const ls
   if (w == 0) wl.emit(out, count_out);
 }
 
+// ---- valid-raw compaction (compact host results) --------------------------
+// SearchEnv.step keeps only reason and raw (env.py:165-172), and raw is 0 for
+// every invalid candidate, so a host result is complete as the reason bytes
+// plus the raws of the valid candidates in index order (the host recovers
+// their positions from the reason bytes). Two passes over the reason bytes:
+// per-tile valid counts, then every tile sums the counts before it (<= a few
+// thousand L2-resident ints) and writes its valid raws at that offset.
+constexpr int kCmpThreads = 256;
+constexpr int kCmpPer = 16;  // reason bytes per thread (one 16-byte load)
+constexpr int kCmpTile = kCmpThreads * kCmpPer;
+
+__device__ __forceinline__ uint32_t zero_bytes4(uint32_t w) { return __vcmpeq4(w, 0u) & 0x01010101u; }
+
+// lane's valid count over its 16 bytes (bytes past n count as invalid)
+__device__ __forceinline__ uint32_t load16(const uint8_t* __restrict__ reason, int64_t i0, int64_t n, uint4& w) {
+  if (i0 + 16 <= n && ((uintptr_t)(reason + i0) & 15) == 0) {
+    w = *reinterpret_cast<const uint4*>(reason + i0);
+  } else {
+    uint32_t b[4] = {0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u};
+    for (int j = 0; j < 16; ++j)
+      if (i0 + j < n) b[j >> 2] = (b[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)reason[i0 + j] << (8 * (j & 3)));
+    w = make_uint4(b[0], b[1], b[2], b[3]);
+  }
+  const uint32_t z = zero_bytes4(w.x) + zero_bytes4(w.y) + zero_bytes4(w.z) + zero_bytes4(w.w);
+  return (z * 0x01010101u) >> 24;
+}
+
+__device__ __forceinline__ int block_excl_scan(int x, int* warp_sums, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < kCmpThreads / 32 ? warp_sums[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_sums[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  total = warp_sums[kCmpThreads / 32 - 1];
+  return incl - x + (wid ? warp_sums[wid - 1] : 0);
+}
+
+__global__ void __launch_bounds__(kCmpThreads) valid_count_kernel(const uint8_t* __restrict__ reason, int64_t n,
+                                                                   int* __restrict__ tile_count) {
+  __shared__ int ws[32];
+  uint4 w;
+  const int c = (int)load16(reason, (int64_t)blockIdx.x * kCmpTile + 16 * threadIdx.x, n, w);
+  int total;
+  block_excl_scan(c, ws, total);
+  if (threadIdx.x == 0) tile_count[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kCmpThreads) valid_compact_kernel(const uint8_t* __restrict__ reason,
+                                                                     const double* __restrict__ thr, int64_t n,
+                                                                     const int* __restrict__ tile_count,
+                                                                     double* __restrict__ out, int64_t* count_out) {
+  __shared__ int ws[32];
+  __shared__ int s_base;
+  // offset of this tile: the counts of every tile before it
+  int part = 0;
+  for (int t = threadIdx.x; t < (int)blockIdx.x; t += kCmpThreads) part += tile_count[t];
+  int tot_before;
+  block_excl_scan(part, ws, tot_before);
+  if (threadIdx.x == 0) s_base = tot_before;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * kCmpTile + 16 * threadIdx.x;
+  uint4 w;
+  const int c = (int)load16(reason, i0, n, w);
+  int total;
+  int pos = s_base + block_excl_scan(c, ws, total);
+  if (c) {
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+    for (int j = 0; j < 16; ++j)
+      if (((ww[j >> 2] >> (8 * (j & 3))) & 0xffu) == 0 && i0 + j < n) out[pos++] = thr[i0 + j];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *count_out = s_base + total;
+}
+
 }  // namespace
+
+size_t compact_scratch_bytes(int64_t n) { return sizeof(int) * (size_t)((n + kCmpTile - 1) / kCmpTile + 1); }
+
+cudaError_t launch_valid_compact(const uint8_t* reason, const double* thr, int64_t n, double* out, int64_t* count_out,
+                                 void* scratch, cudaStream_t s) {
+  if (n <= 0) return cudaMemsetAsync(count_out, 0, sizeof(int64_t), s);
+  const int64_t tiles = (n + kCmpTile - 1) / kCmpTile;
+  int* tc = static_cast<int*>(scratch);
+  valid_count_kernel<<<(unsigned)tiles, kCmpThreads, 0, s>>>(reason, n, tc);
+  valid_compact_kernel<<<(unsigned)tiles, kCmpThreads, 0, s>>>(reason, thr, n, tc, out, count_out);
+  return cudaGetLastError();
+}
 
 size_t scan_scratch_bytes(int64_t n) {
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;

@@ -19,6 +19,7 @@ of the evaluator's device, so they order naturally with surrounding torch work.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -103,6 +104,7 @@ class Evaluator:
         self.head_sizes = tuple(int(self.desc.domain_len[h]) if h < 4 else 3 for h in range(self.vector_length))
         self.space_size = int(self._lib.ls_space_size(self._ctx))
         self._scratch: dict[int, torch.Tensor] = {}  # fused-call scratch per CUDA stream
+        self._one_bufs = threading.local()
 
     # -- lifecycle ----------------------------------------------------------
 
@@ -142,6 +144,26 @@ class Evaluator:
         check(self._lib.ls_reserve_sms(self._ctx, int(sms)))
 
     # -- evaluation ---------------------------------------------------------
+
+    def evaluate_one(self, vector) -> tuple[int, tuple[float, ...]]:
+        """One strategy, host in / host out, lowest latency (ls_evaluate_one):
+        (reason code, (throughput, tpot_s, memory_bytes, compute_s, comm_s, pipeline_s))."""
+        a = self.vector_length
+        if len(vector) != a:
+            raise ValueError(f"vector has {len(vector)} heads, the action space has {a}")
+        try:
+            raw = bytes(vector) if isinstance(vector, (tuple, list)) else np.asarray(vector).astype(np.uint8).tobytes()
+            if not isinstance(vector, (tuple, list)) and np.any(np.asarray(vector) > 255):
+                raise ValueError
+        except (ValueError, TypeError):
+            if any(not 0 <= int(x) <= 255 for x in vector):
+                return 255, (0.0,) * 6  # decode error, like an out-of-range plane byte
+            raw = bytes(int(x) for x in vector)
+        buf = self._one_bufs
+        if not hasattr(buf, "reason"):  # per-thread verdict buffers
+            buf.reason, buf.fields = ctypes.c_uint8(), (ctypes.c_double * 6)()
+        check(self._lib.ls_evaluate_one(self._ctx, raw, ctypes.byref(buf.reason), buf.fields))
+        return buf.reason.value, tuple(buf.fields)
 
     def evaluate(self, planes: torch.Tensor, fields=("throughput",), out: BatchResult | None = None) -> BatchResult:
         """Score candidates resident on the device. ``fields``: subset of FIELDS or "all"."""
@@ -190,6 +212,33 @@ class Evaluator:
         check(self._lib.ls_evaluate_host(self._ctx, ctypes.c_void_p(arr.ctypes.data), n, max(stride, n),
                                          ctypes.byref(soa)))
         return out
+
+    def sa_chain(self, init, coords, drawn, u, temperature, moves: int, best_raw: float, alpha: float, beta: float,
+                 penalty: float):
+        """One simulated-annealing chain of len(u) + 1 evaluations in ONE kernel
+        (ls_sa_chain). Returns numpy (vectors [n, A] u8, raws, rewards, reasons u8)
+        and the best raw afterwards."""
+        steps = len(u) + 1
+        dev = self.device
+        a = self.vector_length
+        t_i32 = lambda x: torch.as_tensor(np.asarray(x, dtype=np.int32).reshape(-1)).to(dev)  # noqa: E731
+        t_f64 = lambda x: torch.as_tensor(np.asarray(x, dtype=np.float64).reshape(-1)).to(dev)  # noqa: E731
+        init_d, coords_d, drawn_d = t_i32(init), t_i32(coords), t_i32(drawn)
+        u_d, temp_d = t_f64(u), t_f64(temperature)
+        best = torch.tensor([best_raw], dtype=torch.float64, device=dev)
+        pos = torch.zeros(1, dtype=torch.int64, device=dev)
+        log_vec = torch.zeros(steps * a, dtype=torch.uint8, device=dev)
+        log_raw = torch.zeros(steps, dtype=torch.float64, device=dev)
+        log_reward = torch.zeros(steps, dtype=torch.float64, device=dev)
+        log_reason = torch.zeros(steps, dtype=torch.uint8, device=dev)
+        env = _native.SearchState(_ptr(best), None, None, 0, _ptr(pos), steps, _ptr(log_vec), _ptr(log_raw),
+                                  _ptr(log_reward), _ptr(log_reason), float(alpha), float(beta), float(penalty))
+        plan = _native.SaPlan(steps, int(moves), _ptr(init_d), _ptr(coords_d) if coords_d.numel() else None,
+                              _ptr(drawn_d) if drawn_d.numel() else None, _ptr(u_d) if steps > 1 else None,
+                              _ptr(temp_d) if steps > 1 else None, env)
+        check(self._lib.ls_sa_chain(self._ctx, ctypes.byref(plan), self._stream()))
+        return (log_vec.view(steps, a).cpu().numpy(), log_raw.cpu().numpy(), log_reward.cpu().numpy(),
+                log_reason.cpu().numpy(), float(best.item()))
 
     # -- reward shaping + elites -------------------------------------------
 
@@ -357,6 +406,48 @@ class Evaluator:
         soa = ResultSoA(ctypes.c_void_p(out["reason"].ctypes.data),
                         *(ctypes.c_void_p(out[f].ctypes.data) if f in out else None for f in FIELDS))
         check(self._lib.ls_evaluate_host_packed(self._ctx, ctypes.c_void_p(arr.ctypes.data), n, ctypes.byref(soa)))
+        return out
+
+    # -- compact host results -------------------------------------------------
+
+    def evaluate_host_compact(self, candidates: np.ndarray, reason: np.ndarray | None = None,
+                              valid_raw: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """Score HOST candidates — [A, N] uint8 planes (the reference's index
+        vectors; packed on host threads inside the call) or N packed 64-bit words —
+        and return (reason [N] uint8, raws of the valid candidates in index order).
+        ~1 B per candidate crosses PCIe back (ls_evaluate_host_compact);
+        ``scatter_raw`` rebuilds the dense raw array. Pinned buffers copy fastest."""
+        arr = np.asarray(candidates)
+        if arr.ndim == 2:
+            if arr.dtype != np.uint8 or arr.shape[0] != self.vector_length:
+                raise ValueError(f"expected uint8 planes of shape [{self.vector_length}, N]")
+            if arr.shape[1] and arr.strides[1] != 1:
+                arr = np.ascontiguousarray(arr)
+            fmt, n = 0, arr.shape[1]
+            stride = arr.strides[0] if arr.shape[0] > 1 else max(n, 1)
+        elif arr.ndim == 1 and arr.dtype in (np.uint64, np.int64):
+            arr = np.ascontiguousarray(arr)
+            fmt, n, stride = 1, arr.shape[0], arr.shape[0]
+        else:
+            raise ValueError("candidates must be [A, N] uint8 planes or N packed 64-bit words")
+        if reason is None:
+            reason = np.empty(n, dtype=np.uint8)
+        if valid_raw is None:
+            valid_raw = np.empty(max(n, 1), dtype=np.float64)
+        if len(reason) < n:
+            raise ValueError("reason buffer is shorter than the batch")
+        count = ctypes.c_int64()
+        check(self._lib.ls_evaluate_host_compact(self._ctx, fmt, ctypes.c_void_p(arr.ctypes.data), n,
+                                                 max(int(stride), n), ctypes.c_void_p(reason.ctypes.data),
+                                                 ctypes.c_void_p(valid_raw.ctypes.data), len(valid_raw),
+                                                 ctypes.byref(count)))
+        return reason[:n], valid_raw[: count.value]
+
+    @staticmethod
+    def scatter_raw(reason: np.ndarray, valid_raw: np.ndarray) -> np.ndarray:
+        """Dense raw array (0 for invalid candidates) from compact host results."""
+        out = np.zeros(len(reason), dtype=np.float64)
+        out[np.flatnonzero(reason == 0)] = valid_raw
         return out
 
     # -- on-device candidate streams ----------------------------------------

@@ -18,8 +18,6 @@ import threading
 from dataclasses import dataclass
 from enum import Enum
 
-import numpy as np
-import torch
 
 from .evaluator import Evaluator
 from .spec import HardwareSpec, ModelSpec
@@ -135,16 +133,23 @@ def layout_error_detail(model, strategy) -> str:
     return "layout error"
 
 
+_FIELDS = ("throughput", "tpot_s", "memory_bytes", "compute_s", "comm_s", "pipeline_s")
+
+
 def result_from_row(row: dict, i: int, model=None, hw=None, strategy=None, slo=None) -> SimResult:
     """SimResult of candidate i of a numpy result dict (reason + six fields)."""
-    code = int(row["reason"][i])
+    return result_from_verdict(int(row["reason"][i]), tuple(float(row[k][i]) if k in row else 0.0 for k in _FIELDS),
+                               model, hw, strategy, slo)
+
+
+def result_from_verdict(code: int, fields, model=None, hw=None, strategy=None, slo=None) -> SimResult:
+    """SimResult of one verdict: reason code + the six numbers in _FIELDS order."""
     if code == 255:
         from .strategy import DecodingError
 
         raise DecodingError("index vector out of range for the action space")
     reason = _BY_CODE[code]
-    f = {k: float(row[k][i]) if k in row else 0.0
-         for k in ("throughput", "tpot_s", "memory_bytes", "compute_s", "comm_s", "pipeline_s")}
+    f = dict(zip(_FIELDS, fields))
     detail = ""
     if strategy is not None:
         if reason is InvalidReason.OVER_DEVICE_BUDGET:
@@ -194,12 +199,13 @@ class _FacadeCache:
                 space = ActionSpaceSpec(tuple(doms[0]), tuple(doms[1]), tuple(doms[2]), tuple(doms[3]),
                                         op_names=tuple(s.op_names) if s.op_names else ("embedding",),
                                         pinned=tuple(s.pinned_dims))
-                if ent is not None:
-                    ent[0].close()
+                # a replaced evaluator is not closed here: another thread may be
+                # scoring with it; reference counting frees it
                 ev = Evaluator(Workload(req.model, req.hw, space, req.context_len, req.slo_tpot))
                 ent = (ev, doms)
                 self._entries[key] = ent
-            return ent[0], doms
+            # the domains frozen into this evaluator (a later growth builds a new one)
+            return ent[0], tuple(tuple(d) for d in doms)
 
 
 _CACHE = _FacadeCache()
@@ -211,18 +217,15 @@ def simulate(req: SimRequest) -> SimResult:
     s = req.strategy
     vec = [doms[0].index(s.tp), doms[1].index(s.ep), doms[2].index(s.pp), doms[3].index(s.batch)]
     vec += [int(a) for a in s.op_dims] if s.op_names else [0]
-    row = _eval_one(ev, vec)
-    return result_from_row(row, 0, req.model, req.hw, s, req.slo_tpot)
-
-
-def _eval_one(ev: Evaluator, vec) -> dict:
-    planes = torch.tensor(np.asarray(vec, dtype=np.uint8).reshape(-1, 1), device=ev.device)
-    return ev.evaluate(planes, fields="all").numpy()
+    code, fields = ev.evaluate_one(vec)
+    return result_from_verdict(code, fields, req.model, req.hw, s, req.slo_tpot)
 
 
 def simulate_vector(ev: Evaluator, vector, model=None, hw=None, strategy=None, slo=None) -> SimResult:
-    """Score one index vector of ``ev``'s action space."""
-    return result_from_row(_eval_one(ev, vector), 0, model, hw, strategy, slo)
+    """Score one index vector of ``ev``'s action space (ls_evaluate_one: no
+    allocation, no copy, no stream sync — the scalar seam's fast path)."""
+    code, fields = ev.evaluate_one(vector)
+    return result_from_verdict(code, fields, model, hw, strategy, slo)
 
 
 def explain(req: SimRequest) -> str:
