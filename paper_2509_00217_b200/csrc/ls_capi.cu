@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ls_eval.h"
@@ -179,6 +180,10 @@ struct ls_ctx {
   int64_t* hp_cnt = nullptr;       // pinned [kPipe]
   cudaEvent_t ev_in[kPipe] = {}, ev_cnt[kPipe] = {};
   HostPool* pool = nullptr;
+  // fused evaluate + elite: PDL between consecutive launches, scratch half per buffer
+  bool pdl = true;
+  std::mutex parity_mu;
+  std::unordered_map<uintptr_t, uint8_t> parity;
 };
 
 namespace {
@@ -430,6 +435,7 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
     const int l = atoi(v);
     if (l >= 16 && l <= 26) c->host_chunk = int64_t(1) << l;
   }
+  if (const char* v = getenv("LS_PDL")) c->pdl = atoi(v) != 0;
   if (const char* v = getenv("LS_HOST_PIPE")) {
     const int p = atoi(v);
     if (p >= 2 && p <= kPipe) c->pipe = p;
@@ -629,33 +635,53 @@ static int host_pipeline(ls_ctx* c, const uint8_t* host_planes, int64_t plane_st
 }
 
 // Host planes -> packed candidate words (the ls_pack / pack4_kernel rule:
-// a head out of range gives an all-ones word, which decodes as an error),
-// vectorisable blocks of 256 candidates.
+// a head out of range gives an all-ones word, which decodes as an error).
+// SWAR over 8 candidates per step: one 8-byte load per plane, per-byte range
+// checks, the axis heads folded four per byte (2-bit fields), then per
+// candidate the coarse rank and the Y word from byte extracts.
+static inline uint64_t ld64(const uint8_t* p) {
+  uint64_t v;
+  std::memcpy(&v, p, 8);
+  return v;
+}
 static void pack_host_range(const uint8_t* planes, int64_t stride, int A, const PackMeta& pk, int64_t lo, int64_t hi,
                             uint64_t* out) {
-  constexpr int B = 256;
-  uint64_t y[B];
-  uint32_t bad[B];
-  for (int64_t i0 = lo; i0 < hi; i0 += B) {
-    const int m = (int)std::min<int64_t>(B, hi - i0);
-    const uint8_t* t = planes + i0;
-    const uint8_t* e = planes + stride + i0;
-    const uint8_t* p = planes + 2 * stride + i0;
-    const uint8_t* b = planes + 3 * stride + i0;
-    for (int j = 0; j < m; ++j) {
-      bad[j] = (uint32_t)(t[j] >= pk.nt) | (uint32_t)(e[j] >= pk.ne) | (uint32_t)(p[j] >= pk.np) |
-               (uint32_t)(b[j] >= pk.nb);
-      y[j] = (uint64_t)(((t[j] * pk.ne + e[j]) * pk.np + p[j]) * pk.nb + b[j]) << 24;
+  constexpr uint64_t kOnes = 0x0101010101010101ull, kHigh = 0x8080808080808080ull, kM3 = 0x0303030303030303ull;
+  const uint64_t sz[4] = {pk.nt * kOnes, pk.ne * kOnes, pk.np * kOnes, pk.nb * kOnes};
+  auto word = [&](uint32_t t, uint32_t e, uint32_t p, uint32_t b, uint64_t y, bool bad) {
+    const uint64_t rank = ((uint64_t)(t * pk.ne + e) * pk.np + p) * pk.nb + b;
+    return bad ? ~0ull : (y | rank << 24);
+  };
+  int64_t i = lo;
+  for (; i + 8 <= hi; i += 8) {
+    uint64_t w[16];
+    for (int h = 0; h < 16; ++h) w[h] = h < A ? ld64(planes + (int64_t)h * stride + i) : 0;
+    uint64_t bad = 0;  // per byte: bit 7 set when that candidate has a head out of range
+    for (int h = 0; h < 4; ++h) bad |= (((w[h] | kHigh) - sz[h]) | w[h]) & kHigh;
+    uint64_t q[3];
+    for (int g = 0; g < 3; ++g) {
+      const uint64_t a = w[4 + 4 * g], b = w[5 + 4 * g], c = w[6 + 4 * g], d = w[7 + 4 * g];
+      bad |= ((((a | kHigh) - 3 * kOnes) | a) | (((b | kHigh) - 3 * kOnes) | b) | (((c | kHigh) - 3 * kOnes) | c) |
+              (((d | kHigh) - 3 * kOnes) | d)) & kHigh;
+      q[g] = (a & kM3) | (b & kM3) << 2 | (c & kM3) << 4 | (d & kM3) << 6;
     }
-    for (int h = 4; h < A; ++h) {
-      const uint8_t* v = planes + (int64_t)h * stride + i0;
-      const int sh = 2 * (h - 4);
-      for (int j = 0; j < m; ++j) {
-        bad[j] |= (uint32_t)(v[j] > 2);
-        y[j] |= (uint64_t)(v[j] & 3u) << sh;
-      }
+    for (int j = 0; j < 8; ++j) {
+      const int sh = 8 * j;
+      const uint64_t y = ((q[0] >> sh) & 255) | ((q[1] >> sh) & 255) << 8 | ((q[2] >> sh) & 255) << 16;
+      out[i - lo + j] = word((uint32_t)(w[0] >> sh) & 255, (uint32_t)(w[1] >> sh) & 255, (uint32_t)(w[2] >> sh) & 255,
+                             (uint32_t)(w[3] >> sh) & 255, y, (bad >> sh) & 0x80);
     }
-    for (int j = 0; j < m; ++j) out[i0 - lo + j] = bad[j] ? ~0ull : y[j];
+  }
+  for (; i < hi; ++i) {  // the < 8 tail
+    uint32_t v[16] = {};
+    for (int h = 0; h < A; ++h) v[h] = planes[(int64_t)h * stride + i];
+    bool bad = v[0] >= pk.nt || v[1] >= pk.ne || v[2] >= pk.np || v[3] >= pk.nb;
+    uint64_t y = 0;
+    for (int h = 4; h < 16; ++h) {
+      bad |= v[h] > 2;
+      y |= (uint64_t)(v[h] & 3u) << (2 * (h - 4));
+    }
+    out[i - lo] = word(v[0], v[1], v[2], v[3], y, bad);
   }
 }
 
@@ -834,19 +860,36 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
-// Scratch of the fused evaluate + top-k: 32 bytes of sync words (the global
-// pruning floor and the finished-CTA counter) at a fixed offset, then the
-// per-CTA lists and counts. The sync words must be zero before the first call
-// on a scratch buffer; the kernel's last CTA leaves them zero again, so a call
+// Scratch of the fused evaluate + top-k: two halves, used by alternate calls
+// on the same buffer (consecutive fused launches overlap under PDL, so one
+// launch's last CTA still merges in its half while the next fills the
+// other). A half: 32 bytes of sync words at a fixed offset (the global pruning
+// floor, the finished-CTA counter, the tile claim counter), then the per-CTA
+// lists and counts. The sync words must be zero before the first call on a
+// buffer; each launch's last CTA leaves its half's words zero again, so a call
 // is one launch (no per-call memset).
-static TopkArgs fused_topk_args(void* scratch, int64_t grid, int k, int64_t index_base, ls_elite_rec* out,
+static size_t fused_half_bytes(const ls_ctx* c, int k) {
+  const size_t lists = (size_t)c->blocks_tma;
+  return (32 + lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4 + 255) & ~size_t(255);
+}
+
+static uint8_t* fused_half(ls_ctx* c, void* scratch, int k) {
+  std::lock_guard<std::mutex> l(c->parity_mu);
+  uint8_t& p = c->parity[reinterpret_cast<uintptr_t>(scratch)];
+  uint8_t* h = static_cast<uint8_t*>(scratch) + (p ? fused_half_bytes(c, k) : 0);
+  p ^= 1;
+  return h;
+}
+
+static TopkArgs fused_topk_args(void* half, int64_t grid, int k, int64_t index_base, ls_elite_rec* out,
                                 int32_t* count_out) {
   TopkArgs tk{};
   tk.k = k;
   tk.index_base = index_base;
-  tk.floor = static_cast<unsigned long long*>(scratch);
+  tk.floor = static_cast<unsigned long long*>(half);
   tk.done = reinterpret_cast<unsigned int*>(tk.floor + 1);
-  tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(scratch) + 32);
+  tk.tile_ctr = tk.done + 1;
+  tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(half) + 32);
   tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
   tk.out = out;
   tk.count_out = count_out;
@@ -855,9 +898,7 @@ static TopkArgs fused_topk_args(void* scratch, int64_t grid, int k, int64_t inde
 
 size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
   if (!c || k < 1) return 0;
-  const size_t lists = (size_t)c->blocks_tma;
-  const size_t fused = 32 + lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4;
-  return std::max(fused, topk_scratch_bytes(n, k, 0));
+  return std::max(2 * fused_half_bytes(c, k), topk_scratch_bytes(n, k, 0));
 }
 
 static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
@@ -906,8 +947,9 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   cudaError_t e;
   if (k <= fused_k_max() && c->blocks_tma > 0 && tma_eligible(a, c->M.A)) {
     LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
+    lp.pdl = c->pdl;
     const int64_t grid = ws_grid(lp, n, words ? GEN_WORDS : GEN_PLANES);
-    TopkArgs tk = fused_topk_args(scratch, grid, k, index_base, topk_out, count_out);
+    TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, index_base, topk_out, count_out);
     if (n == 0) {
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
       return LS_OK;
@@ -930,6 +972,7 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   e = launch_topk(c->TM, planes, plane_stride, a.reason, a.thr, a.thr, n, k, index_base, topk_out, count_out, scratch,
                   c->num_sms, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 32, s);  // the fused path's sync words, zero again
+  if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(scratch) + fused_half_bytes(c, k), 0, 32, s);
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
@@ -1135,7 +1178,7 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   lp.sweep_fits = sweep_smem_bytes(c->L, gen.axis_size / gen.lo_size, gen.lo_size) <= c->sweep_smem;
   if (lp.sweep_fits) lp.max_blocks = tma_grid_cap(c) / c->tma_per_sm;  // one sweep CTA per SM
   const int64_t grid = lp.sweep_fits ? sweep_grid(lp, n) : ws_grid(lp, n, mode);
-  TopkArgs tk = fused_topk_args(scratch, grid, k, start, topk_out, count_out);
+  TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, start, topk_out, count_out);
   cudaError_t e;
   if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=
       cudaSuccess)

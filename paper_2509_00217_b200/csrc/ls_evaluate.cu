@@ -34,11 +34,18 @@ namespace {
 
 #ifdef LS_DIAG_TIMES
 // diagnostic build only: per-CTA phase stamps (globaltimer ns), read by ls_diag_times()
+// rows: 256 per launch, four launches in a row (launch = CTAs entered / grid)
 __device__ unsigned long long g_diag_t[1024][16];
+__device__ unsigned int g_diag_entries;
+__shared__ int s_diag_launch;
+__device__ __forceinline__ void diag_enter() {
+  if (threadIdx.x == 0) s_diag_launch = (int)(atomicAdd(&g_diag_entries, 1u) / gridDim.x);
+  __syncthreads();
+}
 __device__ __forceinline__ void diag_stamp(int slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  g_diag_t[blockIdx.x & 1023][slot] = t;
+  g_diag_t[((blockIdx.x & 255) + 256 * s_diag_launch) & 1023][slot] = t;
 }
 #define LS_STAMP(slot) diag_stamp(slot)
 #else
@@ -452,7 +459,7 @@ __device__ __forceinline__ void warp_merge_lists(const Rec* win, int stride, con
 #ifdef LS_DIAG_TIMES
   if (lane == 0 && stamp) {
     LS_STAMP(10);
-    g_diag_t[blockIdx.x & 1023][11] = rounds;
+    g_diag_t[((blockIdx.x & 255) + 256 * s_diag_launch) & 1023][11] = rounds;
   }
 #endif
 }
@@ -590,6 +597,7 @@ __device__ __forceinline__ void elite_epilogue(RegList& wl, uint8_t* region, int
       // leave the sync words zero for the next call on this scratch
       *tk.floor = 0ull;
       *tk.done = 0u;
+      if (tk.tile_ctr) *tk.tile_ctr = 0u;
     }
   }
 }
@@ -604,6 +612,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t gate_bar;
+  __shared__ volatile int64_t stage_tile[kMaxStages];  // tile in each ring stage; -1 ends the stream
   __shared__ int mb_n[kGateWarps][kSlots];
   __shared__ volatile int mb_state[kGateWarps][kSlots];  // 0 empty, 1 full
   __shared__ volatile int gates_done;
@@ -648,6 +657,9 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+#ifdef LS_DIAG_TIMES
+  diag_enter();
+#endif
   if (threadIdx.x == 0) LS_STAMP(0);
 
   if (warp == kWorkWarps) {  // ---------------- producer warp
@@ -657,20 +669,32 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         mbar_expect_tx(&gate_bar, bytes);
         bulk_g2s(S.gate, gtab, bytes, &gate_bar);
       }
-      int i = 0;
-      for (int64_t tile = blockIdx.x; (MODE == GEN_PLANES || MODE == GEN_WORDS) && tile < ntiles;
-           tile += gridDim.x, ++i) {
+      // tiles 0..ntiles-1 are whole (TMA); tile ntiles is the ragged tail
+      // (< kTile candidates, read by the gate warps directly). Each CTA takes
+      // tile blockIdx.x first; later tiles come from the launch's claim
+      // counter (tk.tile_ctr: a CTA that starts late — e.g. behind the
+      // previous launch's final merge under PDL — simply claims fewer) or,
+      // without one, every gridDim.x-th tile. Stage tile -1 ends the stream.
+      const int64_t last = a.n > ntiles * kTile ? ntiles : ntiles - 1;
+      int64_t tile = blockIdx.x;
+      for (int i = 0; MODE == GEN_PLANES || MODE == GEN_WORDS; ++i) {
         const int s = i % NST, k = i / NST;
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
-        uint8_t* dst = S.ring + s * STB;
-        if (MODE == GEN_WORDS) {  // one contiguous 8 KB tile of candidate words
+        const bool valid = tile <= last;
+        stage_tile[s] = valid ? tile : -1;
+        if (!valid || tile == ntiles) {  // end marker or the ragged tail: no copy
+          mbar_arrive(&full_bar[s]);
+          if (!valid) break;
+        } else if (MODE == GEN_WORDS) {  // one contiguous 16 KB tile of candidate words
           mbar_expect_tx(&full_bar[s], 8u * kTile);
-          bulk_g2s(dst, a.words + tile * kTile, 8u * kTile, &full_bar[s]);
+          bulk_g2s(S.ring + s * STB, a.words + tile * kTile, 8u * kTile, &full_bar[s]);
         } else {
           mbar_expect_tx(&full_bar[s], stage_bytes);
           const uint8_t* src = a.planes + tile * kTile;
+          uint8_t* dst = S.ring + s * STB;
           for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
         }
+        tile = tk.tile_ctr ? (int64_t)gridDim.x + atomicAdd(tk.tile_ctr, 1u) : tile + gridDim.x;
       }
     }
     return;
@@ -856,10 +880,31 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 
     const int lane_off = warp * kWarpCands + 4 * lane;
     if (MODE == GEN_PLANES) {
-      int i = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      for (int i = 0;; ++i) {
         const int s = i % NST;
         mbar_wait(&full_bar[s], (uint32_t)((i / NST) & 1));
+        const int64_t tile = stage_tile[s];
+        if (tile < 0) break;
+        if (tile == ntiles) {  // ragged tail (< one tile), read directly
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[s]);
+          const int64_t base = ntiles * kTile + lane_off;
+          const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+          uint32_t w[16];
+#pragma unroll
+          for (int h = 0; h < 16; ++h) {
+            w[h] = 0;
+            if (h < A)
+              for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
+          }
+          uint32_t q[3];
+          const uint32_t badb = swar_decode(w, M, q);
+          Decoded cs[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
+          pass_a(cs, badb, base, count, nullptr, false);
+          continue;
+        }
         uint32_t w[16];
         const uint32_t st = ring_base + (uint32_t)s * STB + (uint32_t)lane_off;
 #pragma unroll
@@ -873,33 +918,28 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
         pass_a(cs, badb, tile * kTile + lane_off, 4, nullptr, true);
       }
-      // ragged tail (< one tile): the CTA that would own the next tile
-      const int64_t tail0 = ntiles * kTile;
-      if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
-        const int64_t base = tail0 + lane_off;
-        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
-        uint32_t w[16];
-#pragma unroll
-        for (int h = 0; h < 16; ++h) {
-          w[h] = 0;
-          if (h < A)
-            for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
-        }
-        uint32_t q[3];
-        const uint32_t badb = swar_decode(w, M, q);
-        Decoded cs[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
-        pass_a(cs, badb, base, count, nullptr, false);
-      }
     } else if (MODE == GEN_WORDS) {  // 4 consecutive 8-byte candidate words per lane
       // shared addresses hoisted out of the loop (barriers are 8 B apart)
       const uint32_t st0 = ring_base + 8u * (uint32_t)lane_off;
       const uint32_t fb0 = smem_u32(&full_bar[0]), eb0 = smem_u32(&empty_bar[0]);
-      int i = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      for (int i = 0;; ++i) {
         const uint32_t s = (uint32_t)(i % NST);
         mbar_wait_a(fb0 + 8u * s, (uint32_t)((i / NST) & 1));
+        const int64_t tile = stage_tile[s];
+        if (tile < 0) break;
+        if (tile == ntiles) {  // ragged tail (< one tile), read directly
+          __syncwarp();
+          if (lane == 0) mbar_arrive_a(eb0 + 8u * s);
+          const int64_t base = ntiles * kTile + lane_off;
+          const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+          Decoded cs[4];
+          uint32_t badb = 0, rk[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, rk[j], cs[j].Y) << (8 * j);
+          pass_a(cs, badb, base, count, rk, false);
+          continue;
+        }
         uint64_t w[4];
         const uint32_t st = st0 + s * STB;
         lds_u64x2(st, w[0], w[1]);
@@ -911,17 +951,6 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 #pragma unroll
         for (int j = 0; j < 4; ++j) badb |= word_decode(w[j], gm.pk, rk[j], cs[j].Y) << (8 * j);
         pass_a(cs, badb, tile * kTile + lane_off, 4, rk, true);
-      }
-      const int64_t tail0 = ntiles * kTile;
-      if (tail0 < a.n && blockIdx.x == (unsigned)(ntiles % gridDim.x)) {
-        const int64_t base = tail0 + lane_off;
-        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
-        Decoded cs[4];
-        uint32_t badb = 0, rk[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, rk[j], cs[j].Y) << (8 * j);
-        pass_a(cs, badb, base, count, rk, false);
       }
     } else {  // candidates generated in registers: nothing read from HBM
       const int64_t gtiles = (a.n + kTile - 1) / kTile;
@@ -968,6 +997,14 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     // every warp's list (best-first, distinct vectors) to shared memory; warp 0
     // merges the kWorkWarps lists into this CTA's list (one list per lane)
     (void)slots;
+    // Programmatic dependent launch: this CTA's verdicts are written; the
+    // next launch on the stream (the next step) may start on SMs as they
+    // free up. Before its elite epilogue each CTA waits for the previous
+    // launch to complete (its last CTA's merge and tk.out writes, which may
+    // share buffers with this one). Both are no-ops without PDL.
+    __threadfence();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     elite_epilogue<kWorkWarps, kRingBytes>(wl, S.ring, list_count, warp, tk);
   }
 }
@@ -1226,10 +1263,24 @@ void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, 
   const int64_t ntiles = (MODE == GEN_PLANES || MODE == GEN_WORDS) ? a.n / kTile : (a.n + kTile - 1) / kTile;
   const size_t smem = ws_dynamic_bytes(M.A, stage_words(L), lp.smem_gate);
   const int64_t blocks = ws_grid(lp, a.n, MODE);
-  if (lp.smem_gate)
-    eval_ws_kernel<NEU, FULL, true, TOPK, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
-  else
-    eval_ws_kernel<NEU, FULL, false, TOPK, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
+  auto kern = lp.smem_gate ? eval_ws_kernel<NEU, FULL, true, TOPK, MODE> : eval_ws_kernel<NEU, FULL, false, TOPK, MODE>;
+  if (TOPK && (MODE == GEN_WORDS || MODE == GEN_PLANES) && lp.pdl) {
+    // fused steps on one stream overlap: the next launch starts while this
+    // one's last CTAs merge (eval_ws_kernel's griddepcontrol)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, tab, L, M, a, ntiles, tk, gm);
+  } else {
+    kern<<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
+  }
 }
 
 // Write the generated stream as SoA planes (tests, users who want the vectors).
@@ -1497,6 +1548,8 @@ cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8
 
 #ifdef LS_DIAG_TIMES
 extern "C" int ls_diag_times(unsigned long long* host, int rows) {
+  const unsigned zero = 0;
+  cudaMemcpyToSymbol(ls::g_diag_entries, &zero, sizeof(zero));
   return (int)cudaMemcpyFromSymbol(host, ls::g_diag_t, sizeof(unsigned long long) * 16 * (rows < 1024 ? rows : 1024));
 }
 #endif

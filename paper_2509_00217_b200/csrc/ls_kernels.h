@@ -23,6 +23,7 @@ struct LaunchPlan {
   bool smem_gate;  // gate tables staged into shared memory
   int64_t max_blocks;
   bool sweep_fits = false;  // ls_sweep: sweep_kernel's tables fit in shared memory (else eval_ws_kernel)
+  bool pdl = false;         // fused evaluate + elite: programmatic dependent launch
 };
 
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
@@ -37,6 +38,7 @@ struct TopkArgs {
   int32_t* part_counts;
   unsigned long long* floor;  // device word, zeroed before launch
   unsigned int* done;         // CTAs finished (zeroed before launch): the last one merges every CTA list
+  unsigned int* tile_ctr;     // dynamic tile claims after each CTA's first (zero before launch), or null
   ls_elite_rec* out;          // final top-k and its count
   int32_t* count_out;
 };
