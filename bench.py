@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-search", action="store_true", help="skip the PPO search wall-time line")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed batch")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (end-to-end) measurement")
     ap.add_argument("--no-pyref", action="store_true", help="skip timing the reference's Python evaluator")
     ap.add_argument("--pyref-n", type=int, default=1 << 19, help="candidates for the Python reference timing")
     ap.add_argument("--format", default="packed", choices=["packed", "planes"],
@@ -483,35 +484,40 @@ def run_ours(args, rank, world, local_rank):
     # reference's wire format (uint8 index-vector planes), packed into 8-byte words
     # on host threads, H2D, evaluate, D2H of the reason bytes + the valid raws —
     # all inside the timed region; the same from host packed words as a second figure
-    e2e_n = min(args.e2e_n, n)
-    host_planes = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
-    host_planes.copy_(planes[:, :e2e_n].cpu())
-    host_words = torch.empty(e2e_n, dtype=torch.int64).pin_memory()
-    host_words.copy_(cands[:e2e_n].cpu() if cands.dim() == 1 else ev.pack(planes[:, :e2e_n]).cpu())
-    del planes
-    reason_h = torch.empty(e2e_n, dtype=torch.uint8).pin_memory().numpy()
-    vraw_h = torch.empty(e2e_n, dtype=torch.float64).pin_memory().numpy()
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_value = e2e_words = None
+    nvalid, e2e_check, e2e_n = 0, None, min(args.e2e_n, n)
+    if args.no_e2e:
+        del planes
+    else:
+        e2e_n = min(args.e2e_n, n)
+        host_planes = torch.empty((len(sizes), e2e_n), dtype=torch.uint8).pin_memory()
+        host_planes.copy_(planes[:, :e2e_n].cpu())
+        host_words = torch.empty(e2e_n, dtype=torch.int64).pin_memory()
+        host_words.copy_(cands[:e2e_n].cpu() if cands.dim() == 1 else ev.pack(planes[:, :e2e_n]).cpu())
+        del planes
+        reason_h = torch.empty(e2e_n, dtype=torch.uint8).pin_memory().numpy()
+        vraw_h = torch.empty(e2e_n, dtype=torch.float64).pin_memory().numpy()
+        e2e_steps = max(3, min(args.steps, 10))
 
-    def e2e_run(src):
-        ev.evaluate_host_compact(src, reason_h, vraw_h)  # warm: allocates the pipeline buffers
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        nv = 0
-        for _ in range(e2e_steps):
-            r, v = ev.evaluate_host_compact(src, reason_h, vraw_h)
-            nv = len(v)
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t[0])
-        return world * e2e_n * e2e_steps / el, nv
+        def e2e_run(src):
+            ev.evaluate_host_compact(src, reason_h, vraw_h)  # warm: allocates the pipeline buffers
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            nv = 0
+            for _ in range(e2e_steps):
+                r, v = ev.evaluate_host_compact(src, reason_h, vraw_h)
+                nv = len(v)
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t[0])
+            return world * e2e_n * e2e_steps / el, nv
 
-    e2e_value, nvalid = e2e_run(host_planes.numpy())
-    e2e_words, _ = e2e_run(host_words.numpy())
-    e2e_check = bool(np.array_equal(reason_h, out.reason[:e2e_n].cpu().numpy()))
+        e2e_value, nvalid = e2e_run(host_planes.numpy())
+        e2e_words, _ = e2e_run(host_words.numpy())
+        e2e_check = bool(np.array_equal(reason_h, out.reason[:e2e_n].cpu().numpy()))
 
     if rank != 0:
         return

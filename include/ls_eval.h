@@ -186,10 +186,12 @@ int ls_evaluate_host_packed(ls_ctx* ctx, const uint64_t* host_words, int64_t n, 
  * candidate, and the valid positions are the zero reason bytes). About 1 B
  * per candidate comes back instead of 9. Input `format`:
  *   LS_HOST_PLANES  A uint8 planes plane_stride apart (the reference's index
- *                   vectors, SoA); packed into 8-byte candidate words on host
- *                   worker threads inside the call (chunk by chunk, beside the
- *                   copies and kernels of earlier chunks), so 8 B/candidate
- *                   cross PCIe instead of A;
+ *                   vectors, SoA), copied as they are (A B/candidate over
+ *                   PCIe); with LS_HOST_PACK=1 in the environment at context
+ *                   creation they are instead packed into 8-byte candidate
+ *                   words on host worker threads inside the call (chunk by
+ *                   chunk, beside the copies and kernels of earlier chunks),
+ *                   which wins only when the host has cores to spare;
  *   LS_HOST_WORDS   packed candidate words, as ls_evaluate_packed takes them.
  * valid_raw holds up to `capacity` doubles; *valid_count receives the number
  * of valid candidates (LS_ERR_INVALID_ARGUMENT when it exceeds capacity).
@@ -408,6 +410,19 @@ int ls_ppo_round(ls_ctx* ctx, const ls_ppo_plan* plan, int n, void* stream);
 int ls_ppo_forward(ls_ctx* ctx, const ls_ppo_plan* plan, int n, double* logp_out, double* value_out, void* stream);
 /* Tests: `epochs` updates on the batch_* arrays as given (no sampling). */
 int ls_ppo_update(ls_ctx* ctx, const ls_ppo_plan* plan, int n, void* stream);
+
+/* ---- Completion signal of a fused launch ----------------------------------
+ * ls_evaluate_packed_topk, plus: once the launch's last CTA has written
+ * topk_out / count_out it stores `seq` to *signal (device memory, release
+ * semantics). Another stream waits for that elite with ls_stream_wait_signal
+ * (cuStreamWaitValue32, *signal >= seq) instead of an event recorded between
+ * two fused launches — a stream operation there would serialise launches that
+ * otherwise overlap (programmatic dependent launch). Used for the cross-rank
+ * elite exchange that runs beside the next batch. */
+int ls_evaluate_packed_topk_signal(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
+                                   int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                                   uint32_t* signal, uint32_t seq, void* stream);
+int ls_stream_wait_signal(void* stream, const uint32_t* signal, uint32_t seq);
 
 #ifdef __cplusplus
 }

@@ -161,6 +161,11 @@ _SIGS = {
     "ls_evaluate_packed_topk": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                                ctypes.POINTER(ResultSoA), ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ls_evaluate_packed_topk_signal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                                      ctypes.POINTER(ResultSoA), ctypes.c_int, ctypes.c_int64,
+                                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                      ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
+    "ls_stream_wait_signal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32]),
     "ls_env_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SearchState), ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p]),
     "ls_evaluate_one": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_void_p]),
@@ -190,7 +195,10 @@ def lib(require_gpu: bool = False):
             handle = ctypes.CDLL(str(path))
         except OSError as err:
             raise NativeUnavailable(f"cannot load {path}: {err}") from err
+        tolerant = "LS_EVAL_LIB" in os.environ  # A/B builds of other revisions may lack newer entry points
         for name, (res, args) in _SIGS.items():
+            if tolerant and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

@@ -182,6 +182,7 @@ struct ls_ctx {
   HostPool* pool = nullptr;
   // fused evaluate + elite: PDL between consecutive launches, scratch half per buffer
   bool pdl = true;
+  bool host_pack = false;  // LS_HOST_PLANES: pack on host threads (8 B/candidate over PCIe) instead of raw planes
   std::mutex parity_mu;
   std::unordered_map<uintptr_t, uint8_t> parity;
 };
@@ -436,6 +437,7 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
     if (l >= 16 && l <= 26) c->host_chunk = int64_t(1) << l;
   }
   if (const char* v = getenv("LS_PDL")) c->pdl = atoi(v) != 0;
+  if (const char* v = getenv("LS_HOST_PACK")) c->host_pack = atoi(v) != 0;
   if (const char* v = getenv("LS_HOST_PIPE")) {
     const int p = atoi(v);
     if (p >= 2 && p <= kPipe) c->pipe = p;
@@ -712,7 +714,7 @@ static int host_pipeline_compact(ls_ctx* c, int format, const void* host_in, int
           (e = cudaEventCreateWithFlags(&c->ev_cnt[s], cudaEventDisableTiming)) != cudaSuccess)
         return cuda_fail(e, "compact buffers");
     }
-    if (format == LS_HOST_PLANES && !c->hp_words[s] &&
+    if (format == LS_HOST_PLANES && c->host_pack && !c->hp_words[s] &&
         (e = cudaHostAlloc(reinterpret_cast<void**>(&c->hp_words[s]), sizeof(uint64_t) * chunk_n,
                            cudaHostAllocPortable)) != cudaSuccess)
       return cuda_fail(e, "pinned staging");
@@ -720,7 +722,7 @@ static int host_pipeline_compact(ls_ctx* c, int format, const void* host_in, int
   if (!c->hp_cnt && (e = cudaHostAlloc(reinterpret_cast<void**>(&c->hp_cnt), sizeof(int64_t) * kPipe,
                                        cudaHostAllocPortable)) != cudaSuccess)
     return cuda_fail(e, "pinned counts");
-  if (format == LS_HOST_PLANES && !c->pool) {
+  if (format == LS_HOST_PLANES && c->host_pack && !c->pool) {
     int w = (int)std::thread::hardware_concurrency() - 1;
     if (const char* v = getenv("LS_HOST_THREADS")) w = atoi(v) - 1;
     c->pool = new HostPool(std::max(0, std::min(w, 255)));
@@ -749,7 +751,17 @@ static int host_pipeline_compact(ls_ctx* c, int format, const void* host_in, int
     const int64_t off = j * chunk_n, cnt = std::min<int64_t>(chunk_n, n - off);
     cudaStream_t st = c->hs[s];
     const uint64_t* src;
-    if (format == LS_HOST_PLANES) {
+    const bool raw_planes = format == LS_HOST_PLANES && !c->host_pack;
+    const int64_t dstride = (cnt + 15) & ~int64_t(15);  // device plane stride: TMA-aligned
+    if (raw_planes) {  // the planes themselves cross PCIe (A B/candidate); the device reads them directly
+      if ((e = cudaMemcpy2DAsync(c->h_planes[s], (size_t)dstride, static_cast<const uint8_t*>(host_in) + off,
+                                 (size_t)stride, (size_t)cnt, A, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+          (e = cudaEventRecord(c->ev_in[s], st)) != cudaSuccess) {
+        rc = cuda_fail(e, "H2D planes");
+        break;
+      }
+      src = nullptr;
+    } else if (format == LS_HOST_PLANES) {
       // the slot's staging buffer is free once its previous H2D finished
       if (j >= c->pipe && (e = cudaEventSynchronize(c->ev_in[s])) != cudaSuccess) {
         rc = cuda_fail(e, "staging reuse");
@@ -767,21 +779,28 @@ static int host_pipeline_compact(ls_ctx* c, int format, const void* host_in, int
       src = static_cast<const uint64_t*>(host_in) + off;
     }
     uint64_t* dwords = reinterpret_cast<uint64_t*>(c->h_planes[s]);
-    if ((e = cudaMemcpyAsync(dwords, src, sizeof(uint64_t) * (size_t)cnt, cudaMemcpyHostToDevice, st)) !=
-            cudaSuccess ||
-        (e = cudaEventRecord(c->ev_in[s], st)) != cudaSuccess) {
+    if (!raw_planes && ((e = cudaMemcpyAsync(dwords, src, sizeof(uint64_t) * (size_t)cnt, cudaMemcpyHostToDevice,
+                                             st)) != cudaSuccess ||
+                        (e = cudaEventRecord(c->ev_in[s], st)) != cudaSuccess)) {
       rc = cuda_fail(e, "H2D words");
       break;
     }
     EvalArgs a{};
-    a.words = dwords;
+    if (raw_planes) {
+      a.planes = c->h_planes[s];
+      a.stride = dstride;
+    } else {
+      a.words = dwords;
+      a.stride = cnt;
+    }
     a.n = cnt;
-    a.stride = cnt;
     a.reason = c->h_reason[s];
     a.thr = c->h_f[s][0];
     a.sparse_thr = true;
-    LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
-    if ((e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, st, &pk)) !=
+    LaunchPlan lp{tma_eligible(a, A), c->smem_gate, tma_grid_cap(c)};
+    if (!lp.tma) lp.max_blocks = c->blocks_generic;
+    if ((e = launch_evaluate(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, a, st,
+                             raw_planes ? nullptr : &pk)) !=
             cudaSuccess ||
         (e = launch_valid_compact(a.reason, a.thr, cnt, c->d_vraw[s], c->d_vcnt[s], c->d_cscr[s], st)) !=
             cudaSuccess ||
@@ -888,7 +907,11 @@ static TopkArgs fused_topk_args(void* half, int64_t grid, int k, int64_t index_b
   tk.index_base = index_base;
   tk.floor = static_cast<unsigned long long*>(half);
   tk.done = reinterpret_cast<unsigned int*>(tk.floor + 1);
+#ifdef LS_STATIC_TILES
+  tk.tile_ctr = nullptr;
+#else
   tk.tile_ctr = tk.done + 1;
+#endif
   tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(half) + 32);
   tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
   tk.out = out;
@@ -903,7 +926,8 @@ size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
 
 static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
                               int64_t plane_stride, const ls_result_soa* out, int k, int64_t index_base,
-                              ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream);
+                              ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream,
+                              uint32_t* signal = nullptr, uint32_t seq = 0);
 
 int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_stride, const ls_result_soa* out,
                      int k, int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
@@ -913,6 +937,38 @@ int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_
     return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_topk arguments");
   return evaluate_topk_impl(c, planes, nullptr, n, plane_stride, out, k, index_base, topk_out, count_out, scratch,
                             stream);
+}
+
+int ls_evaluate_packed_topk_signal(ls_ctx* c, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
+                                   int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                                   uint32_t* signal, uint32_t seq, void* stream) {
+  g_err.clear();
+  if (!c || n < 0 || k < 1 || k > fused_k_max() || !topk_out || !count_out || !scratch || (n > 0 && !words) ||
+      !signal)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_packed_topk_signal arguments");
+  return evaluate_topk_impl(c, nullptr, words, n, n, out, k, index_base, topk_out, count_out, scratch, stream, signal,
+                            seq);
+}
+
+// cuStreamWaitValue32 from the driver (resolved once through the runtime: no -lcuda)
+typedef int (*StreamWaitValue32Fn)(void* stream, unsigned long long addr, uint32_t value, unsigned int flags);
+
+int ls_stream_wait_signal(void* stream, const uint32_t* signal, uint32_t seq) {
+  g_err.clear();
+  static StreamWaitValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitValue32Fn>(p);
+  });
+  if (!signal) return fail(LS_ERR_INVALID_ARGUMENT, "null signal");
+  if (!fn) return fail(LS_ERR_UNSUPPORTED, "cuStreamWaitValue32 is not available");
+  constexpr unsigned kGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
+  const int r = fn(stream, reinterpret_cast<unsigned long long>(signal), seq, kGeq);
+  return r == 0 ? LS_OK : fail(LS_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
 }
 
 int ls_evaluate_packed_topk(ls_ctx* c, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
@@ -926,7 +982,8 @@ int ls_evaluate_packed_topk(ls_ctx* c, const uint64_t* words, int64_t n, const l
 
 static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
                               int64_t plane_stride, const ls_result_soa* out, int k, int64_t index_base,
-                              ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream) {
+                              ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream,
+                              uint32_t* signal, uint32_t seq) {
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   EvalArgs a{};
@@ -950,8 +1007,11 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
     lp.pdl = c->pdl;
     const int64_t grid = ws_grid(lp, n, words ? GEN_WORDS : GEN_PLANES);
     TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, index_base, topk_out, count_out);
+    tk.signal = signal;
+    tk.seq = seq;
     if (n == 0) {
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
+      if (signal) cudaMemcpyAsync(signal, &seq, sizeof(seq), cudaMemcpyHostToDevice, s);
       return LS_OK;
     }
     const PackMeta pk = pack_meta(c->desc);

@@ -60,10 +60,13 @@ __device__ __forceinline__ void diag_stamp(int slot) {
 #define LS_FP_WARPS 4
 #endif
 #ifndef LS_RING_KB
-#define LS_RING_KB 64
+#define LS_RING_KB 80
 #endif
 #ifndef LS_MIN_BLOCKS
 #define LS_MIN_BLOCKS 1
+#endif
+#ifndef LS_CLAIM_GROUP
+#define LS_CLAIM_GROUP 4  // tiles per dynamic claim of the fused kernels
 #endif
 #ifndef LS_BACKOFF_MAX
 #define LS_BACKOFF_MAX 512
@@ -81,7 +84,7 @@ constexpr int kGenericThreads = 256;
 constexpr int kFusedK = 32;  // max elite size of the fused evaluate + top-k path
 constexpr uint32_t kStageBytes = 16 * kTile;  // 16 plane slices per stage (planes >= A stay zero)
 constexpr uint32_t kRingBytes = LS_RING_KB * 1024;
-static_assert(kRingBytes % kStageBytes == 0 && kRingBytes / kStageBytes >= 2, "ring holds whole plane stages");
+static_assert(kRingBytes / kStageBytes >= 2, "ring holds two plane stages");
 // packed words are 8 B per candidate: the same ring holds twice the stages,
 // keeping the bytes in flight per SM (and so the HBM pipe) as full as for planes
 constexpr int kMaxStages = kRingBytes / (8 * kTile);
@@ -142,6 +145,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// The same for candidate tiles, read exactly once: L2 evict-first (LS_EVICT_FIRST tuning builds).
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#ifdef LS_EVICT_FIRST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
+}
 
 __device__ __forceinline__ uint64_t pack_key(int64_t idx, const Decoded& c) {
   return (uint64_t)idx | ((uint64_t)c.t << 40) | ((uint64_t)c.e << 46) | ((uint64_t)c.p << 52) |
@@ -156,8 +173,21 @@ __device__ __forceinline__ void unpack_key(uint64_t k, uint32_t Y, int64_t& idx,
   c.Y = Y;
 }
 
+// Verdict stores are written once and never re-read by the kernel: streaming
+// (evict-first) stores when LS_STCS is set (tuning builds).
 __device__ __forceinline__ void st2(double* base, int64_t i, double x, double y) {
+#ifdef LS_STCS
+  __stcs(reinterpret_cast<double2*>(base + i), make_double2(x, y));
+#else
   *reinterpret_cast<double2*>(base + i) = make_double2(x, y);
+#endif
+}
+__device__ __forceinline__ void st_reason4(uint8_t* p, uint32_t v) {
+#ifdef LS_STCS
+  __stcs(reinterpret_cast<unsigned int*>(p), v);
+#else
+  *reinterpret_cast<uint32_t*>(p) = v;
+#endif
 }
 
 template <bool FULL>
@@ -598,6 +628,10 @@ __device__ __forceinline__ void elite_epilogue(RegList& wl, uint8_t* region, int
       *tk.floor = 0ull;
       *tk.done = 0u;
       if (tk.tile_ctr) *tk.tile_ctr = 0u;
+      if (tk.signal) {  // the elite is complete: release it to a waiting stream
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(tk.signal), "r"(tk.seq) : "memory");
+      }
     }
   }
 }
@@ -675,11 +709,18 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
       // counter (tk.tile_ctr: a CTA that starts late — e.g. behind the
       // previous launch's final merge under PDL — simply claims fewer) or,
       // without one, every gridDim.x-th tile. Stage tile -1 ends the stream.
+      // Claims are groups of G consecutive tiles (G = 4 with the counter, so
+      // one atomic round trip covers several microseconds of streaming), and
+      // the next group's claim is issued when the current group starts.
       const int64_t last = a.n > ntiles * kTile ? ntiles : ntiles - 1;
-      int64_t tile = blockIdx.x;
+      const int G = tk.tile_ctr ? LS_CLAIM_GROUP : 1;
+      int64_t grp = blockIdx.x;
+      int64_t nxt = tk.tile_ctr ? (int64_t)gridDim.x + atomicAdd(tk.tile_ctr, 1u) : grp + gridDim.x;
+      int j = 0;
       for (int i = 0; MODE == GEN_PLANES || MODE == GEN_WORDS; ++i) {
         const int s = i % NST, k = i / NST;
         if (k > 0) mbar_wait(&empty_bar[s], (uint32_t)((k - 1) & 1));
+        const int64_t tile = grp * G + j;
         const bool valid = tile <= last;
         stage_tile[s] = valid ? tile : -1;
         if (!valid || tile == ntiles) {  // end marker or the ragged tail: no copy
@@ -687,14 +728,18 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
           if (!valid) break;
         } else if (MODE == GEN_WORDS) {  // one contiguous 16 KB tile of candidate words
           mbar_expect_tx(&full_bar[s], 8u * kTile);
-          bulk_g2s(S.ring + s * STB, a.words + tile * kTile, 8u * kTile, &full_bar[s]);
+          bulk_g2s_stream(S.ring + s * STB, a.words + tile * kTile, 8u * kTile, &full_bar[s]);
         } else {
           mbar_expect_tx(&full_bar[s], stage_bytes);
           const uint8_t* src = a.planes + tile * kTile;
           uint8_t* dst = S.ring + s * STB;
           for (int h = 0; h < A; ++h) bulk_g2s(dst + h * kTile, src + (int64_t)h * a.stride, kTile, &full_bar[s]);
         }
-        tile = tk.tile_ctr ? (int64_t)gridDim.x + atomicAdd(tk.tile_ctr, 1u) : tile + gridDim.x;
+        if (++j == G || tile == last) {  // next group (its claim was issued a group ago)
+          j = 0;
+          grp = nxt;
+          nxt = tk.tile_ctr ? (int64_t)gridDim.x + atomicAdd(tk.tile_ctr, 1u) : grp + gridDim.x;
+        }
       }
     }
     return;
@@ -840,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
       if (!a.reason) {
         // sweep mode: no per-candidate verdicts, only the fused elite
       } else if (whole) {
-        *reinterpret_cast<uint32_t*>(a.reason + base) = r4;
+        st_reason4(a.reason + base, r4);
         // zero fields: the warp's 128 consecutive doubles as two fully
         // coalesced 512-byte stores (every lane of a full tile has count 4;
         // survivors' values are stored later by the fp64 pass)
@@ -879,30 +924,17 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
     };
 
     const int lane_off = warp * kWarpCands + 4 * lane;
+    bool tail = false;  // this CTA drew the ragged tail tile
     if (MODE == GEN_PLANES) {
       for (int i = 0;; ++i) {
         const int s = i % NST;
         mbar_wait(&full_bar[s], (uint32_t)((i / NST) & 1));
         const int64_t tile = stage_tile[s];
         if (tile < 0) break;
-        if (tile == ntiles) {  // ragged tail (< one tile), read directly
+        if (tile == ntiles) {  // ragged tail: processed after the stream (cold code off the hot loop)
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty_bar[s]);
-          const int64_t base = ntiles * kTile + lane_off;
-          const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
-          uint32_t w[16];
-#pragma unroll
-          for (int h = 0; h < 16; ++h) {
-            w[h] = 0;
-            if (h < A)
-              for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
-          }
-          uint32_t q[3];
-          const uint32_t badb = swar_decode(w, M, q);
-          Decoded cs[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
-          pass_a(cs, badb, base, count, nullptr, false);
+          tail = true;
           continue;
         }
         uint32_t w[16];
@@ -918,6 +950,23 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
         pass_a(cs, badb, tile * kTile + lane_off, 4, nullptr, true);
       }
+      if (tail) {  // ragged tail (< one tile), read directly
+        const int64_t base = ntiles * kTile + lane_off;
+        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+        uint32_t w[16];
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          w[h] = 0;
+          if (h < A)
+            for (int j = 0; j < count; ++j) w[h] |= (uint32_t)a.planes[(int64_t)h * a.stride + base + j] << (8 * j);
+        }
+        uint32_t q[3];
+        const uint32_t badb = swar_decode(w, M, q);
+        Decoded cs[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) extract(w, q, j, cs[j]);
+        pass_a(cs, badb, base, count, nullptr, false);
+      }
     } else if (MODE == GEN_WORDS) {  // 4 consecutive 8-byte candidate words per lane
       // shared addresses hoisted out of the loop (barriers are 8 B apart)
       const uint32_t st0 = ring_base + 8u * (uint32_t)lane_off;
@@ -927,17 +976,10 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         mbar_wait_a(fb0 + 8u * s, (uint32_t)((i / NST) & 1));
         const int64_t tile = stage_tile[s];
         if (tile < 0) break;
-        if (tile == ntiles) {  // ragged tail (< one tile), read directly
+        if (tile == ntiles) {  // ragged tail: processed after the stream (cold code off the hot loop)
           __syncwarp();
           if (lane == 0) mbar_arrive_a(eb0 + 8u * s);
-          const int64_t base = ntiles * kTile + lane_off;
-          const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
-          Decoded cs[4];
-          uint32_t badb = 0, rk[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, rk[j], cs[j].Y) << (8 * j);
-          pass_a(cs, badb, base, count, rk, false);
+          tail = true;
           continue;
         }
         uint64_t w[4];
@@ -951,6 +993,16 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 #pragma unroll
         for (int j = 0; j < 4; ++j) badb |= word_decode(w[j], gm.pk, rk[j], cs[j].Y) << (8 * j);
         pass_a(cs, badb, tile * kTile + lane_off, 4, rk, true);
+      }
+      if (tail) {  // ragged tail (< one tile), read directly
+        const int64_t base = ntiles * kTile + lane_off;
+        const int count = base < a.n ? (a.n - base < 4 ? (int)(a.n - base) : 4) : 0;
+        Decoded cs[4];
+        uint32_t badb = 0, rk[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          badb |= word_decode(j < count ? a.words[base + j] : 0ull, gm.pk, rk[j], cs[j].Y) << (8 * j);
+        pass_a(cs, badb, base, count, rk, false);
       }
     } else {  // candidates generated in registers: nothing read from HBM
       const int64_t gtiles = (a.n + kTile - 1) / kTile;

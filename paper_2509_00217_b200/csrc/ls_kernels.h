@@ -39,6 +39,8 @@ struct TopkArgs {
   unsigned long long* floor;  // device word, zeroed before launch
   unsigned int* done;         // CTAs finished (zeroed before launch): the last one merges every CTA list
   unsigned int* tile_ctr;     // dynamic tile claims after each CTA's first (zero before launch), or null
+  uint32_t* signal;           // optional: the last CTA stores seq here (release) once out / count_out are written
+  uint32_t seq;
   ls_elite_rec* out;          // final top-k and its count
   int32_t* count_out;
 };

@@ -74,7 +74,7 @@ class ShardedSweep:
         dev = evaluator.device
         self.transport = "local" if self.world == 1 else "nccl"
         self.overlap = bool(overlap) and self.world > 1
-        nbuf = 2 if self.overlap else 1
+        nbuf = 4 if self.overlap else 1
         # one message per rank: k records + a 32-byte row holding the count
         self._sends = [torch.zeros((self.k + 1, 32), dtype=torch.uint8, device=dev) for _ in range(nbuf)]
         self._gathered = [torch.empty((self.world * (self.k + 1), 32), dtype=torch.uint8, device=dev)
@@ -83,6 +83,8 @@ class ShardedSweep:
                          torch.zeros(1, dtype=torch.int32, device=dev)) for _ in range(nbuf)]
         self._free = [None] * nbuf  # side-stream event: slot's buffers no longer read
         self._slot = 0
+        self._seq = 0
+        self._signal = torch.zeros(1, dtype=torch.int32, device=dev)  # last fused launch whose elite is written
         self._side = torch.cuda.Stream(dev) if self.overlap else None
         if self.overlap:
             evaluator.reserve_sms(1)
@@ -98,20 +100,30 @@ class ShardedSweep:
         ``candidates``: [A, n] uint8 planes, or n packed 64-bit words.
         Returns (out, recs, count) with recs/count the merged global top-k on device
         (with ``overlap``, valid on the caller's stream only after ``wait()``).
+
+        With ``overlap`` and packed words, nothing but the fused launch is put on the
+        caller's stream: the side stream waits for the launch's completion signal
+        (ls_stream_wait_signal), so consecutive launches keep overlapping (PDL).
         """
-        if self.world > 1 and self._free[self._slot] is not None:
-            torch.cuda.current_stream(self.ev.device).wait_event(self._free[self._slot])
+        cur = torch.cuda.current_stream(self.ev.device)
+        free = self._free[self._slot]
+        if self.world > 1 and free is not None and not free.query():
+            cur.wait_event(free)  # the slot's previous exchange is still reading it (rare)
         into = self._send if self.world > 1 else None
         if candidates.dim() == 1:
+            sig = None
+            if self.overlap:
+                self._seq += 1
+                sig = self._signal
             out, recs, count = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
-                                                            verdicts=verdicts, into=into)
+                                                            verdicts=verdicts, into=into, signal=sig, seq=self._seq)
         else:
             out, recs, count = self.ev.evaluate_topk(candidates, k=self.k, index_base=index_base, out=out,
                                                      verdicts=verdicts, into=into)
-        recs, count = self.merge(recs, count)
+        recs, count = self.merge(recs, count, signalled=candidates.dim() == 1)
         return out, recs, count
 
-    def merge(self, recs: torch.Tensor, count: torch.Tensor):
+    def merge(self, recs: torch.Tensor, count: torch.Tensor, signalled: bool = False):
         """All-gather every rank's device top-k (k x 32 B + count) in ONE collective and merge on device."""
         if self.world == 1:
             return recs, count
@@ -120,14 +132,18 @@ class ShardedSweep:
         if recs.data_ptr() != send.data_ptr():  # not produced in place by run()
             send[: self.k].copy_(recs)
             send[self.k, :4].view(torch.int32).copy_(count)
+            signalled = False
         gathered = self._gathered[slot]
         cur = torch.cuda.current_stream(self.ev.device)
         if self._side is None:
             dist.all_gather_into_tensor(gathered, send, group=self.group)
             return self._merge_gathered(gathered, self._merged[slot])
-        ready = torch.cuda.Event()
-        ready.record(cur)
-        self._side.wait_event(ready)
+        if signalled and self.overlap:
+            self.ev.wait_signal(self._signal, self._seq, stream=self._side)
+        else:
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            self._side.wait_event(ready)
         with torch.cuda.stream(self._side):
             dist.all_gather_into_tensor(gathered, send, group=self.group)
             res = self._merge_gathered(gathered, self._merged[slot])

@@ -139,6 +139,11 @@ class Evaluator:
         stride = planes.stride(0) if planes.shape[0] > 1 else max(n, 1)
         return n, max(stride, n)
 
+    def wait_signal(self, signal: torch.Tensor, seq: int, stream=None) -> None:
+        """Make ``stream`` (default: the current one) wait until ``signal`` >= seq."""
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(self._lib.ls_stream_wait_signal(ctypes.c_void_p(st.cuda_stream), _ptr(signal), int(seq)))
+
     def reserve_sms(self, sms: int) -> None:
         """Leave ``sms`` SMs free of the persistent evaluate kernels (ls_reserve_sms)."""
         check(self._lib.ls_reserve_sms(self._ctx, int(sms)))
@@ -375,18 +380,27 @@ class Evaluator:
 
     def evaluate_packed_topk(self, words: torch.Tensor, k: int = 3, index_base: int = 0,
                              out: BatchResult | None = None, fields=("throughput",), verdicts: bool = True,
-                             into: torch.Tensor | None = None):
-        """Fused evaluate + top-k by raw over packed words. Returns (out, records, count)."""
+                             into: torch.Tensor | None = None, signal: torch.Tensor | None = None, seq: int = 0):
+        """Fused evaluate + top-k by raw over packed words. Returns (out, records, count).
+
+        ``signal`` (a device uint32/int32 tensor of one element): the launch stores ``seq``
+        there once the records are written, for ``wait_signal`` on another stream."""
         n = self._check_words(words)
         if verdicts and out is None:
             out = self._alloc(n, fields)
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
         recs, count = self._elite_out(k, into)
         scratch = self._fused_scratch(n, k)
-        check(self._lib.ls_evaluate_packed_topk(self._ctx, ctypes.c_void_p(words.data_ptr()), n,
-                                                ctypes.byref(soa) if soa is not None else None, int(k),
-                                                int(index_base), _ptr(recs), _ptr(count), _ptr(scratch),
-                                                self._stream()))
+        if signal is not None:
+            check(self._lib.ls_evaluate_packed_topk_signal(
+                self._ctx, ctypes.c_void_p(words.data_ptr()), n, ctypes.byref(soa) if soa is not None else None,
+                int(k), int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), _ptr(signal), int(seq),
+                self._stream()))
+        else:
+            check(self._lib.ls_evaluate_packed_topk(self._ctx, ctypes.c_void_p(words.data_ptr()), n,
+                                                    ctypes.byref(soa) if soa is not None else None, int(k),
+                                                    int(index_base), _ptr(recs), _ptr(count), _ptr(scratch),
+                                                    self._stream()))
         return (out if verdicts else None), recs, count
 
     def evaluate_host_packed(self, words: np.ndarray, fields=("throughput",), out: dict | None = None) -> dict:

@@ -44,6 +44,22 @@ def test_compact_equals_full_host_path(name, n):
     assert np.array_equal(r2, reason) and np.array_equal(v2.view(np.uint64), vraw.view(np.uint64))
 
 
+def test_compact_host_packing_equals_raw_planes(monkeypatch):
+    """LS_HOST_PACK=1: planes packed on host worker threads (SWAR packer) give the
+    same results as copying the planes (ragged sizes, decode errors)."""
+    from paper_2509_00217_b200.evaluator import Evaluator
+
+    wl, _, _ = load_eval("moe_1p6t_2048")
+    raw = Evaluator(wl, device=0)
+    monkeypatch.setenv("LS_HOST_PACK", "1")
+    packed = Evaluator(wl, device=0)
+    for n in (7, 8, 4099, (1 << 22) + 13):
+        planes = _planes(raw, n, n, bad=min(n, 40))
+        r1, v1 = raw.evaluate_host_compact(planes)
+        r2, v2 = packed.evaluate_host_compact(planes)
+        assert np.array_equal(r1, r2) and np.array_equal(v1.view(np.uint64), v2.view(np.uint64)), n
+
+
 def test_compact_strided_planes_and_capacity():
     from paper_2509_00217_b200._native import NativeError
     from paper_2509_00217_b200.evaluator import Evaluator
