@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--no-search", action="store_true", help="skip the PPO search wall-time line")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed batch")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (end-to-end) measurement")
+    ap.add_argument("--diag-no-exchange", action="store_true", help=argparse.SUPPRESS)  # N>1 diagnostics only
+    ap.add_argument("--diag-reserve", type=int, default=None, help=argparse.SUPPRESS)
     ap.add_argument("--no-pyref", action="store_true", help="skip timing the reference's Python evaluator")
     ap.add_argument("--pyref-n", type=int, default=1 << 19, help="candidates for the Python reference timing")
     ap.add_argument("--format", default="packed", choices=["packed", "planes"],
@@ -428,6 +430,11 @@ def run_ours(args, rank, world, local_rank):
     # N > 1: each step's elite all-gather + merge runs on a side stream beside the
     # next step's evaluate (which leaves one SM free for it)
     sweep = ShardedSweep(ev, k=ELITE_K, overlap=world > 1)
+    if args.diag_reserve is not None:
+        ev.reserve_sms(args.diag_reserve)
+    if args.diag_no_exchange:  # diagnostics: each rank's fused launches alone (no elite exchange)
+        sweep = ShardedSweep(ev, k=ELITE_K, overlap=False)
+        sweep.world = 1
     stream = torch.cuda.current_stream(dev)
 
     def step():

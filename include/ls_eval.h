@@ -413,12 +413,14 @@ int ls_ppo_update(ls_ctx* ctx, const ls_ppo_plan* plan, int n, void* stream);
 
 /* ---- Completion signal of a fused launch ----------------------------------
  * ls_evaluate_packed_topk, plus: once the launch's last CTA has written
- * topk_out / count_out it stores `seq` to *signal (device memory, release
- * semantics). Another stream waits for that elite with ls_stream_wait_signal
- * (cuStreamWaitValue32, *signal >= seq) instead of an event recorded between
- * two fused launches — a stream operation there would serialise launches that
- * otherwise overlap (programmatic dependent launch). Used for the cross-rank
- * elite exchange that runs beside the next batch. */
+ * topk_out / count_out it stores `seq` to *signal (device memory or pinned,
+ * mapped host memory; system-scope release, so a host thread polling the
+ * word sees the records complete). Another stream waits for that elite with ls_stream_wait_signal
+ * (cuStreamWaitValue32 until *signal >= seq; LS_WAIT_MEMOP=0 or a driver
+ * without it: a one-thread polling kernel, giving up after ~10 s) rather than
+ * an event recorded between two fused launches — a stream operation there
+ * would serialise launches that otherwise overlap (programmatic dependent
+ * launch). Used for the cross-rank elite exchange beside the next batch. */
 int ls_evaluate_packed_topk_signal(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
                                    int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
                                    uint32_t* signal, uint32_t seq, void* stream);

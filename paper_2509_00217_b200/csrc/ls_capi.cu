@@ -263,6 +263,25 @@ void build_meta(ls_ctx* c) {
     M.op_src[k] = (int8_t)(h >= 0 ? 2 * slot[h] : -1);
     M.op_pin[k] = (int8_t)(h >= 0 ? 0 : d.op_pinned[k]);
   }
+  M.canon_runs = 0;
+  M.canon_or = 0;
+  for (int k = 0; k < LS_NUM_OPS; ++k) {
+    if (M.op_src[k] < 0) {
+      M.canon_or |= (uint32_t)M.op_pin[k] << (2 * k);
+      continue;
+    }
+    const int r = M.canon_runs - 1;
+    if (r >= 0 && M.canon_shl[r] + M.canon_len[r] == 2 * k && M.canon_shr[r] + M.canon_len[r] == M.op_src[k]) {
+      M.canon_len[r] += 2;  // extends the run
+    } else {
+      M.canon_shr[M.canon_runs] = (uint8_t)M.op_src[k];
+      M.canon_len[M.canon_runs] = 2;
+      M.canon_shl[M.canon_runs] = (uint8_t)(2 * k);
+      ++M.canon_runs;
+    }
+  }
+  M.canon_ident = M.canon_or == 0 && M.canon_runs == 1 && M.canon_shr[0] == 0 && M.canon_shl[0] == 0 &&
+                  M.canon_len[0] == 2 * LS_NUM_OPS;
   M.attn_src = M.op_src[LS_OP_ATTN_CORE];
   M.attn_pin = M.op_pin[LS_OP_ATTN_CORE];
   M.attn_shift = M.attn_src >= 0 ? M.attn_src + 1 : 31;
@@ -907,11 +926,7 @@ static TopkArgs fused_topk_args(void* half, int64_t grid, int k, int64_t index_b
   tk.index_base = index_base;
   tk.floor = static_cast<unsigned long long*>(half);
   tk.done = reinterpret_cast<unsigned int*>(tk.floor + 1);
-#ifdef LS_STATIC_TILES
-  tk.tile_ctr = nullptr;
-#else
   tk.tile_ctr = tk.done + 1;
-#endif
   tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(half) + 32);
   tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
   tk.out = out;
@@ -965,7 +980,14 @@ int ls_stream_wait_signal(void* stream, const uint32_t* signal, uint32_t seq) {
       fn = reinterpret_cast<StreamWaitValue32Fn>(p);
   });
   if (!signal) return fail(LS_ERR_INVALID_ARGUMENT, "null signal");
-  if (!fn) return fail(LS_ERR_UNSUPPORTED, "cuStreamWaitValue32 is not available");
+  static const bool mem_op = [] {
+    const char* v = getenv("LS_WAIT_MEMOP");
+    return !v || atoi(v) != 0;
+  }();
+  if (!mem_op || !fn) {  // a one-thread polling kernel on the waiting stream instead
+    cudaError_t e = launch_wait_signal(signal, seq, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? LS_OK : cuda_fail(e, "wait_signal launch");
+  }
   constexpr unsigned kGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
   const int r = fn(stream, reinterpret_cast<unsigned long long>(signal), seq, kGeq);
   return r == 0 ? LS_OK : fail(LS_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");

@@ -628,9 +628,9 @@ __device__ __forceinline__ void elite_epilogue(RegList& wl, uint8_t* region, int
       *tk.floor = 0ull;
       *tk.done = 0u;
       if (tk.tile_ctr) *tk.tile_ctr = 0u;
-      if (tk.signal) {  // the elite is complete: release it to a waiting stream
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(tk.signal), "r"(tk.seq) : "memory");
+      if (tk.signal) {  // the elite is complete: release it (the word may be host-mapped memory)
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(tk.signal), "r"(tk.seq) : "memory");
       }
     }
   }
@@ -1175,7 +1175,14 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   const uint32_t lt = (1u << lane) - 1u;
   const int64_t nchunks = (n + kSwChunk - 1) / kSwChunk;
   const uint32_t lo_size = (uint32_t)gm.lo_size;
-  for (int64_t ch = (int64_t)blockIdx.x * kSwWarps + warp; ch < nchunks; ch += (int64_t)gridDim.x * kSwWarps) {
+  // chunks: each warp's first one static, the rest claimed from the launch's
+  // counter (survivor-heavy chunks cost several times the others, so a static
+  // deal leaves SMs idle at the end); the next claim is issued a chunk ahead
+  const int64_t nwarps = (int64_t)gridDim.x * kSwWarps;
+  uint32_t claim = 0;
+  if (lane == 0) claim = atomicAdd(tk.tile_ctr, 1u);
+  int64_t nxt = nwarps + __shfl_sync(0xffffffffu, claim, 0);
+  for (int64_t ch = (int64_t)blockIdx.x * kSwWarps + warp; ch < nchunks;) {
     const int64_t base = ch * kSwChunk;
     // enumeration: decode the lane's first position once, then step the
     // mixed-radix digits (coarse rank, high / low axis rank) by 32 per round
@@ -1235,6 +1242,11 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           __syncwarp();
         }
       }
+    }
+    ch = nxt;
+    if (ch < nchunks) {
+      if (lane == 0) claim = atomicAdd(tk.tile_ctr, 1u);
+      nxt = nwarps + __shfl_sync(0xffffffffu, claim, 0);
     }
   }
   if (qcount > 0) {

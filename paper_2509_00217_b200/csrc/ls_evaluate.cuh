@@ -22,40 +22,6 @@ struct Verdict {
   double thr, tpot, comp, comm, pipe;
 };
 
-#ifdef LS_OLD_WALK
-// CPython builtin sum() over floats with int start 0: Neumaier compensation
-// from 3.12 (NEU) or the naive left fold before it.
-template <bool NEU>
-struct PySum {
-  double f, c;
-  __device__ __forceinline__ void first(double x) {
-    f = 0.0 + x;
-    c = 0.0;
-  }
-  __device__ __forceinline__ void add(double x) {
-    const double t = f + x;
-    if (NEU) c += fabs(f) >= fabs(x) ? (f - t) + x : (x - t) + f;
-    f = t;
-  }
-  __device__ __forceinline__ double result() const {
-    if (NEU && c != 0.0 && isfinite(c)) return f + c;
-    return f;
-  }
-};
-
-template <bool NEU>
-struct Accum {
-  PySum<NEU> s;
-  int n;
-  __device__ __forceinline__ void init() { n = 0; }
-  __device__ __forceinline__ void push(double x) {
-    if (n++ == 0) s.first(x);
-    else s.add(x);
-  }
-  __device__ __forceinline__ double result() const { return n ? s.result() : 0.0; }
-};
-
-#else
 // CPython builtin sum() over floats with int start 0: Neumaier compensation
 // from 3.12 (NEU) or the naive left fold before it. CPython adds the first
 // float to the int 0 exactly (0 + x == x) and compensates from the second
@@ -84,23 +50,14 @@ struct PySum {
   }
 };
 
-#endif
 // Collective family of reconciling producer state `from` to demand `to`
 // (transition, layout.py:119-155; states are axis codes, see ST_*):
 // R->* none, S->S none, S->R all_gather, P->S reduce_scatter, P->R all_reduce.
-#ifdef LS_OLD_WALK
-__device__ __forceinline__ int fam(int from, int to) {
-  if (from == ST_R) return FAM_NONE;
-  if (from == ST_S) return to == ST_S ? FAM_NONE : FAM_ONCE;
-  return to == ST_S ? FAM_ONCE : FAM_AR;
-}
-#else
 // As a 2-bit table indexed by 3*from + to: (P,R) -> AR, (P,S) -> ONCE, (S,R) -> ONCE.
 __device__ __forceinline__ int fam(int from, int to) {
   constexpr uint32_t kFam = (FAM_AR << 6) | (FAM_ONCE << 10) | (FAM_ONCE << 12);
   return (int)((kFam >> (2 * (3 * from + to))) & 3u);
 }
-#endif
 // Input demanded by a matmul under `axis` (_required_input, layout.py:194-197).
 __device__ __forceinline__ int req(int axis) { return axis == 1 ? ST_S : ST_R; }
 
@@ -129,12 +86,18 @@ struct Decoded {
   uint32_t Y;
 };
 
-// Axis of canonical op k (Strategy.axis_of, strategy.py:209-214): its head's
-// field in Y, or its pin / UNSHARDED.
-__device__ __forceinline__ int op_axis(const EvalMeta& M, uint32_t Y, int k) {
-  const int src = M.op_src[k];
-  return src >= 0 ? (int)((Y >> src) & 3u) : (int)M.op_pin[k];
+// The 12 canonical ops' axes as 2-bit fields in canonical op order (op k at
+// bits 2k): the head fields of Y moved by the workload's runs of consecutive
+// controlled ops, pinned ops' axes OR-ed in (EvalMeta canon_*). For the
+// default 12-op spaces this is one run, Y itself.
+__device__ __forceinline__ uint32_t canon_y(const EvalMeta& M, uint32_t Y) {
+  if (M.canon_ident) return Y;  // one run from bit 0, nothing pinned
+  uint32_t yc = M.canon_or;
+  for (int r = 0; r < M.canon_runs; ++r)
+    yc |= ((Y >> M.canon_shr[r]) & ((1u << M.canon_len[r]) - 1u)) << M.canon_shl[r];
+  return yc;
 }
+__device__ __forceinline__ int cax(uint32_t yc, int k) { return (int)((yc >> (2 * k)) & 3u); }
 
 // attn_core sharded on DIM1 (the high bit of its 2-bit field), or its pin.
 __device__ __forceinline__ uint32_t attn_dim1(const EvalMeta& M, uint32_t Y) {
@@ -182,124 +145,17 @@ __device__ __forceinline__ uint32_t gate_rank(const uint32_t* C, const EvalMeta&
   return coarse_reason(C[rank], Y, attn_dim1(M, Y));
 }
 
-#ifdef LS_OLD_WALK
 // fp64 pass for a candidate that passed gate(). T: the full table (global).
 template <bool NEU, bool LDG = true>
 __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
                                           const Decoded& c, Verdict& v) {
   const int t = c.t, e = c.e, p = c.p, b = c.b;
-  const int ax_emb = op_axis(M, c.Y, LS_OP_EMBEDDING), ax_qkv = op_axis(M, c.Y, LS_OP_QKV_PROJ);
-  const int ax_attn = op_axis(M, c.Y, LS_OP_ATTN_CORE), ax_out = op_axis(M, c.Y, LS_OP_ATTN_OUT_PROJ);
-  const int ax_f1 = op_axis(M, c.Y, LS_OP_EXPERT_FFN1), ax_f2 = op_axis(M, c.Y, LS_OP_EXPERT_FFN2);
-  const int ax_s1 = op_axis(M, c.Y, LS_OP_SHARED_FFN1), ax_s2 = op_axis(M, c.Y, LS_OP_SHARED_FFN2);
-  const int ax_lmh = op_axis(M, c.Y, LS_OP_LM_HEAD);
-  const int a2 = ax_attn == 2;
-  const int nt = L.nt, ne = L.ne, nb = L.nb;
-  const int tb = t * nb + b, teb = (t * ne + e) * nb + b;
-  const int64_t tpv = (int64_t)tword<LDG>(T, L.tpv + t), epv = (int64_t)tword<LDG>(T, L.epv + e);
-  const int64_t ppv = (int64_t)tword<LDG>(T, L.ppv + p);
-  const bool tp_gt1 = tpv > 1, ep_gt1 = epv > 1;
-
-  // layer plan compute: qkv, kv, attn, out, router, ffn1, ffn2[, sh1, sh2]
-  Accum<NEU> lc;
-  lc.init();
-  lc.push(tget<LDG>(T, L.opt_qkv + ax_qkv * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_kv + a2 * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_attn + a2 * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_out + ax_out * nt * nb + tb));
-  lc.push(tget<LDG>(T, L.opt_router + b));
-  lc.push(tget<LDG>(T, L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
-  lc.push(tget<LDG>(T, L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
-  if (L.has_shared) {
-    lc.push(tget<LDG>(T, L.opt_sh1 + ax_s1 * nt * nb + tb));
-    lc.push(tget<LDG>(T, L.opt_sh2 + ax_s2 * nt * nb + tb));
-  }
-  // layer plan collectives in all_collectives() order (layout.py:270-275)
-  Accum<NEU> lm;
-  lm.init();
-#define LS_TP_COLL(cls, f) tget<LDG>(T, L.coll + ((cls) * 2 + ((f) - 1)) * nt * nb + tb)
-  const int st_attn = a2 ? ST_S : ST_R;
-  if (tp_gt1) {
-    int f;
-    if ((f = fam(ax_qkv, st_attn))) lm.push(LS_TP_COLL(CLS_QKV, f));     // feed attn_core
-    if ((f = fam(st_attn, req(ax_out)))) lm.push(LS_TP_COLL(CLS_H, f));  // feed attn_out_proj
-    if ((f = fam(ax_out, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));          // attention residual
-  }
-  const double a2a = ep_gt1 ? tget<LDG>(T, L.a2a + teb) : 0.0;
-  if (ep_gt1) lm.push(a2a);  // expert dispatch
-  if (tp_gt1) {
-    int f;
-    if ((f = fam(ax_f1, req(ax_f2)))) lm.push(tget<LDG>(T, L.rtf + (f - 1) * nt * ne * nb + teb));  // feed ffn2
-    if (L.has_shared && (f = fam(ax_s1, req(ax_s2)))) lm.push(LS_TP_COLL(CLS_F, f));        // feed sh2
-  }
-  if (ep_gt1) lm.push(a2a);  // expert combine
-  if (tp_gt1) {
-    int f;
-    if (L.has_shared && ax_s2 != ax_f2) {  // branch outputs disagree: align both
-      if ((f = fam(ax_f2, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));
-      if ((f = fam(ax_s2, ST_R))) lm.push(LS_TP_COLL(CLS_H, f));
-    } else if ((f = fam(ax_f2, ST_R))) {  // layer exit
-      lm.push(LS_TP_COLL(CLS_H, f));
-    }
-  }
-  const double layer_c = lc.result(), layer_m = lm.result();
-
-  // pre plan (embedding) and post plan (final_norm, lm_head)
-  const double pre_c = 0.0 + tget<LDG>(T, L.opt_emb + ax_emb * nt * nb + tb);
-  double pre_m = 0.0, post_m = 0.0;
-  if (tp_gt1) {
-    int f;
-    if ((f = fam(ax_emb, ST_R))) pre_m = 0.0 + LS_TP_COLL(CLS_H, f);
-    if ((f = fam(ax_lmh, ST_R))) post_m = 0.0 + LS_TP_COLL(CLS_V, f);
-  }
-#undef LS_TP_COLL
-  PySum<NEU> po;
-  po.first(tget<LDG>(T, L.opt_norm + b));
-  po.add(tget<LDG>(T, L.opt_lmh + ax_lmh * nt * nb + tb));
-  const double post_c = po.result();
-
-  // totals and pipeline stages (simulator.py:286-323)
-  const int64_t world = tpv * epv * ppv;
-  const double hop = ppv > 1 ? tget<LDG>(T, L.hop + (world <= M.node_size ? nb : 0) + b) : 0.0;
-  const double compute = (M.num_layers_d * layer_c + pre_c) + post_c;
-  const double comm = (M.num_layers_d * layer_m + pre_m) + post_m;
-  const double pipe = tget<LDG>(T, L.ppm1_d + p) * hop;
-  const double tpot = (compute + comm) + pipe;
-  const double body = tget<LDG>(T, L.lps_d + p) * (layer_c + layer_m);
-  const double c0 = body + (pre_c + pre_m);
-  double cmax;
-  if (ppv == 1) {
-    cmax = c0 + (post_c + post_m);
-  } else {
-    cmax = c0 + hop;
-    if (ppv > 2) cmax = py_max(cmax, body + hop);
-    cmax = py_max(cmax, body + (post_c + post_m));
-  }
-  v.tpot = tpot;
-  v.comp = compute;
-  v.comm = comm;
-  v.pipe = pipe;
-  // gate 4: tpot > slo_tpot (simulator.py:325)
-  if (tpot > M.slo_tpot) {
-    v.reason = LS_REASON_SLO_VIOLATION;
-    v.thr = 0.0;
-    return;
-  }
-  v.reason = LS_REASON_NONE;
-  v.thr = (tget<LDG>(T, L.batch_d + b) / cmax) / (double)world;
-}
-
-#else
-// fp64 pass for a candidate that passed gate(). T: the full table (global).
-template <bool NEU, bool LDG = true>
-__device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
-                                          const Decoded& c, Verdict& v) {
-  const int t = c.t, e = c.e, p = c.p, b = c.b;
-  const int ax_emb = op_axis(M, c.Y, LS_OP_EMBEDDING), ax_qkv = op_axis(M, c.Y, LS_OP_QKV_PROJ);
-  const int ax_attn = op_axis(M, c.Y, LS_OP_ATTN_CORE), ax_out = op_axis(M, c.Y, LS_OP_ATTN_OUT_PROJ);
-  const int ax_f1 = op_axis(M, c.Y, LS_OP_EXPERT_FFN1), ax_f2 = op_axis(M, c.Y, LS_OP_EXPERT_FFN2);
-  const int ax_s1 = op_axis(M, c.Y, LS_OP_SHARED_FFN1), ax_s2 = op_axis(M, c.Y, LS_OP_SHARED_FFN2);
-  const int ax_lmh = op_axis(M, c.Y, LS_OP_LM_HEAD);
+  const uint32_t yc = canon_y(M, c.Y);
+  const int ax_emb = cax(yc, LS_OP_EMBEDDING), ax_qkv = cax(yc, LS_OP_QKV_PROJ);
+  const int ax_attn = cax(yc, LS_OP_ATTN_CORE), ax_out = cax(yc, LS_OP_ATTN_OUT_PROJ);
+  const int ax_f1 = cax(yc, LS_OP_EXPERT_FFN1), ax_f2 = cax(yc, LS_OP_EXPERT_FFN2);
+  const int ax_s1 = cax(yc, LS_OP_SHARED_FFN1), ax_s2 = cax(yc, LS_OP_SHARED_FFN2);
+  const int ax_lmh = cax(yc, LS_OP_LM_HEAD);
   const int a2 = ax_attn == 2;
   const int nt = L.nt, ne = L.ne, nb = L.nb;
   const int tb = t * nb + b, teb = (t * ne + e) * nb + b;
@@ -399,5 +255,4 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   v.thr = (tget<LDG>(T, L.batch_d + b) / cmax) / (double)world;
 }
 
-#endif
 }  // namespace ls

@@ -134,6 +134,7 @@ struct OneArgs {
 };
 cudaError_t launch_eval_one(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
                             const OneArgs& a, cudaStream_t s);
+cudaError_t launch_wait_signal(const uint32_t* sig, uint32_t seq, cudaStream_t s);
 cudaError_t launch_sa_chain(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
                             const ls_sa_plan& p, cudaStream_t s);
 

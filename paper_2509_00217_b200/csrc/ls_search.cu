@@ -102,7 +102,41 @@ __global__ void sa_chain_kernel(const uint64_t* __restrict__ tab, const __grid_c
   *S.log_pos = pos;
 }
 
+// A stream waits for another stream's completion signal: one thread polls
+// the word (acquire loads, backing off with __nanosleep) until it reaches seq.
+// The fallback of ls_stream_wait_signal when cuStreamWaitValue32 is missing
+// (LS_WAIT_MEMOP=0 selects it). Gives up after ~10 s (no hang if the signal
+// never comes).
+__global__ void wait_signal_kernel(const uint32_t* __restrict__ sig, uint32_t seq) {
+  unsigned ns = 128;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sig) : "memory");
+    if ((int32_t)(v - seq) >= 0) return;
+    __nanosleep(ns);
+    if (ns < 4096) ns *= 2;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) return;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_wait_signal(const uint32_t* sig, uint32_t seq, cudaStream_t s) {
+  // the SM this thread spins on keeps the shared-memory carve-out the
+  // evaluate kernels need, so their CTAs can still land beside it
+  static const bool attr = [] {
+    cudaFuncSetAttribute(wait_signal_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    return true;
+  }();
+  (void)attr;
+  wait_signal_kernel<<<1, 1, 0, s>>>(sig, seq);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_eval_one(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M,
                             const OneArgs& a, cudaStream_t s) {

@@ -99,6 +99,12 @@ struct EvalMeta {
   double slo_tpot;
   double hbm_capacity;
   int64_t code_stride[LS_MAX_HEADS];  // mixed-radix place value per head
+  // canonical axis word (canon_y): runs of consecutive controlled ops whose
+  // head fields are consecutive too: bits [shr, shr + len) of Y -> bit shl
+  int canon_runs;
+  uint8_t canon_shr[LS_NUM_OPS], canon_len[LS_NUM_OPS], canon_shl[LS_NUM_OPS];
+  uint32_t canon_or;  // pinned ops' axes at their canonical fields
+  int canon_ident;    // canon_y(Y) == Y (12 controlled ops, heads in canonical order)
 };
 
 __host__ __device__ inline int round2(int w) { return (w + 1) & ~1; }

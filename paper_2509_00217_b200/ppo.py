@@ -43,11 +43,11 @@ from .baselines import cosine_decay
 from .env import EvalRecord, SearchEnv
 from .evaluator import REASON_NAMES
 from .knobs import PpoConfig
-from .policy import NumericsError, TorchPolicy, sample_actions
+from .policy import NumericsError, TorchPolicy
 from .report import SearchReport, build_report
 from .strategy import DecodingError, canonical_fused_ops
 
-__all__ = ["PpoConfig", "ChunkExit", "ChunkOutcome", "GpuSearch", "ppo_loss", "run_search"]
+__all__ = ["PpoConfig", "ChunkExit", "ChunkOutcome", "GpuSearch", "run_search"]
 
 _CONFIDENT, _NONFINITE = 1, 2
 
@@ -63,32 +63,13 @@ class ChunkOutcome:
     evals_used: int
 
 
-def ppo_loss(pol: TorchPolicy, obs, act, logp_old, value_old, reward, cfg: PpoConfig) -> torch.Tensor:
-    """Clipped-surrogate PPO loss over a rollout batch (reference loss_and_grads,
-    ppo.py:203-294): per sample -min(rho*A, clip(rho)*A) + value_coef*(v - r)^2
-    - entropy_coef*H, averaged; A = reward - value_old. Its autograd gradient is
-    the reference's hand-written one (the unclipped branch carries the
-    gradient on ties, the clamped branch is constant outside the band)."""
-    n = obs.shape[0]
-    log_probs, probs, value = pol(obs)
-    logp_new = log_probs.gather(2, act.unsqueeze(2)).sum(dim=(1, 2))
-    entropy = pol.entropy(log_probs, probs)
-    ratio = torch.exp(logp_new - logp_old)
-    advantage = reward - value_old
-    unclipped = ratio * advantage
-    clamped = ratio.clamp(1.0 - cfg.clip_eps, 1.0 + cfg.clip_eps) * advantage
-    surrogate = torch.where(unclipped <= clamped, unclipped, clamped)
-    err = value - reward
-    return (-surrogate / n).sum() + (cfg.value_coef * err * err / n).sum() - cfg.entropy_coef * (entropy / n).sum()
-
-
 class GpuSearch:
     """Device-resident state of one PPO search over ``env``."""
 
-    def __init__(self, env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True,
-                 engine: str = "fused") -> None:
-        if engine not in ("fused", "torch"):
-            raise ValueError(f"unknown PPO engine {engine!r}")
+    # rounds run eagerly (per round size) before one is captured into a CUDA graph
+    capture_warmup = 0
+
+    def __init__(self, env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True) -> None:
         if env.budget_left < cfg.budget:
             raise ValueError(f"environment has {env.budget_left} evals left, need {cfg.budget}")
         self.env, self.cfg, self.seed = env, cfg, seed
@@ -133,10 +114,6 @@ class GpuSearch:
         self.action = torch.zeros(H, **i64)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
-        self.opt = None  # torch engine only (importing torch.optim costs seconds)
-        if engine == "torch":
-            self.opt = torch.optim.Adam(self.policy.parameters(), lr=self.lr, betas=(0.9, 0.999), eps=1e-8,
-                                        capturable=True, foreach=True)
         self.use_graphs = use_graphs
         self.stream = torch.cuda.Stream(device=dev)
         self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
@@ -144,11 +121,9 @@ class GpuSearch:
         self._lib = _native.lib(require_gpu=True)
         self.rounds = 0
         self.round_events: list | None = None  # set to [] to record (start, end) CUDA events per round
-        self.engine = engine
-        if engine == "fused":
-            self._init_fused()
+        self._init_engine()
 
-    def _init_fused(self) -> None:
+    def _init_engine(self) -> None:
         """Buffers and the ls_ppo_plan of the fused-kernel engine (ls_policy.cu)."""
         cfg, pol, dev = self.cfg, self.policy, self.device
         dims = _native.PolicyDims(self.H, cfg.width, cfg.ffn_width, cfg.history_len, pol.num_heads, pol.kmax,
@@ -159,7 +134,7 @@ class GpuSearch:
             raise RuntimeError("policy arena layout disagrees with ls_policy_layout_of")
         ws = int(self._lib.ls_ppo_workspace_bytes(ctypes.byref(dims)))
         if ws == 0:
-            raise _native.NativeError(4, "policy dims unsupported by the fused PPO kernels; use engine='torch'")
+            raise _native.NativeError(4, "policy dims unsupported by the fused PPO kernels")
         self.adam_m = torch.zeros_like(pol.flat)
         self.adam_v = torch.zeros_like(pol.flat)
         self.adam_step = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -179,49 +154,17 @@ class GpuSearch:
 
     # -- one round (graph-capturable: no host syncs, static shapes) ----------
 
-    def _sample_and_step(self, j: int) -> None:
-        pol, H = self.policy, self.H
-        obs = pol.observation(self.elite_vec, self.elite_reward)
-        with torch.no_grad():
-            log_probs, probs, value = pol(obs)
-            u = self.uniforms.index_select(0, self.spent * H + self.head_offsets)
-            act = sample_actions(probs, u, self.size_cap)
-            self.b_obs[j].copy_(obs)
-            self.b_act[j].copy_(act)
-            self.action.copy_(act)
-            self.b_logp[j:j + 1].copy_(log_probs.gather(1, act.unsqueeze(1)).sum().reshape(1))
-            self.b_value[j:j + 1].copy_(value.reshape(1))
-        _native.check(self._lib.ls_env_step(self.ev._ctx, ctypes.byref(self._state), ctypes.c_void_p(self.action.data_ptr()),
-                                            ctypes.c_void_p(self.b_reward.data_ptr() + 8 * j),
-                                            ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
-        self.spent.add_(1)
-
-    def _update(self, n: int) -> torch.Tensor:
-        cfg, pol = self.cfg, self.policy
-        obs, act = self.b_obs[:n], self.b_act[:n]
-        logp_old, value_old, reward = self.b_logp[:n], self.b_value[:n], self.b_reward[:n]
-        bad = ~(torch.isfinite(reward) & torch.isfinite(value_old) & torch.isfinite(logp_old)).all()
-        for _ in range(cfg.epochs_per_update):
-            loss = ppo_loss(pol, obs, act, logp_old, value_old, reward, cfg)
-            loss.backward()
-            self.opt.step()
-            self.opt.zero_grad(set_to_none=False)
-            bad = bad | ~torch.isfinite(loss)
-        norms = torch._foreach_norm(list(pol.parameters()), float("inf"))
-        return bad | ~torch.isfinite(torch.stack(norms)).all()
-
-    def _round(self, n: int) -> None:
-        self.lr.copy_(self.lr_table.index_select(0, self.spent).reshape(()))
-        for j in range(n):
-            self._sample_and_step(j)
-        bad = self._update(n)
-        with torch.no_grad():
-            _, probs, _ = self.policy(self.policy.observation(self.elite_vec, self.elite_reward))
-            confident = (self.policy.confidence(probs) >= self.cfg.tau).all()
-        self.status.copy_((confident.int() * _CONFIDENT + bad.int() * _NONFINITE).reshape(1))
-
-    def _fused_round(self, n: int) -> None:
+    def _engine_round(self, n: int) -> None:
+        """n samples (each: sample, env step, elite offer), the updates and the
+        confidence check: ls_ppo_round, a fixed sequence of fused kernels."""
         _native.check(self._lib.ls_ppo_round(self.ev._ctx, ctypes.byref(self.plan), n, self._stream_ptr()))
+
+    def _engine_start_chunk(self) -> None:
+        """Fresh optimizer state; sample slot 0 <- forward of the current observation."""
+        self.adam_m.zero_()
+        self.adam_v.zero_()
+        self.adam_step.zero_()
+        _native.check(self._lib.ls_ppo_prime(self.ev._ctx, ctypes.byref(self.plan), self._stream_ptr()))
 
     def _run_round(self, n: int) -> int:
         """One round (replayed graph once warm); returns the status word."""
@@ -232,24 +175,16 @@ class GpuSearch:
             ev[0].record()
         if g is not None:
             g.replay()
-        elif self.engine == "fused":
-            if self.use_graphs:  # kernels need no warm-up: capture at once, then replay
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=self.stream):
-                    self._fused_round(n)
-                self._graphs[n] = g
-                g.replay()
-            else:
-                self._fused_round(n)
+        elif self.use_graphs and self._eager_rounds.get(n, 0) >= self.capture_warmup:
+            # the fused kernels need no warm-up: captured at once, then replayed
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._engine_round(n)
+            self._graphs[n] = g
+            g.replay()
         else:
-            self._round(n)
-            if self.use_graphs:
-                self._eager_rounds[n] = self._eager_rounds.get(n, 0) + 1
-                if self._eager_rounds[n] >= 3:  # warm (autograd, cuBLAS, Adam state) -> capture
-                    g = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g, stream=self.stream):
-                        self._round(n)
-                    self._graphs[n] = g
+            self._engine_round(n)
+            self._eager_rounds[n] = self._eager_rounds.get(n, 0) + 1
         self.rounds += 1
         if ev is not None:
             ev[1].record()
@@ -262,22 +197,13 @@ class GpuSearch:
 
     def _start_chunk(self, allowance: int) -> None:
         self.policy.reset_parameters(self.rng)  # the reference's PolicyNetwork(rng=rng)
-        if self.opt is not None:  # fresh optimizer
-            for st in self.opt.state.values():
-                for v in st.values():
-                    v.zero_()
-        if self.engine == "fused":
-            self.adam_m.zero_()
-            self.adam_v.zero_()
-            self.adam_step.zero_()
         self._rng_mark = self.rng.bit_generator.state
         draws = self.rng.random(allowance * self.H)
         self.uniforms[: draws.size].copy_(torch.from_numpy(draws))
         lrs = np.array([cosine_decay(self.cfg.lr_initial, s / allowance) for s in range(allowance)])
         self.lr_table[:allowance].copy_(torch.from_numpy(lrs))
         self.spent.zero_()
-        if self.engine == "fused":  # sample slot 0 <- forward of the current observation
-            _native.check(self._lib.ls_ppo_prime(self.ev._ctx, ctypes.byref(self.plan), self._stream_ptr()))
+        self._engine_start_chunk()
 
     def _end_chunk(self, spent: int) -> None:
         self.rng.bit_generator.state = self._rng_mark
@@ -332,14 +258,14 @@ class GpuSearch:
 
 
 def run_search(env: SearchEnv, cfg: PpoConfig, seed: int, *, use_graphs: bool = True,
-               engine: str = "fused", stats: dict | None = None) -> SearchReport:
+               stats: dict | None = None, search_cls=None) -> SearchReport:
     """Full chunked-restart PPO search on the GPU; consumes exactly ``cfg.budget`` evals.
 
     Appends the eval records to ``env`` (and its NDJSON sink) when the search
     ends and leaves ``env.best_raw`` where the reference's would be.
     """
     start = time.perf_counter()
-    search = GpuSearch(env, cfg, seed, use_graphs=use_graphs, engine=engine)
+    search = (search_cls or GpuSearch)(env, cfg, seed, use_graphs=use_graphs)
     if stats is not None:
         search.round_events = []
     restarts, evals_done = search.run()

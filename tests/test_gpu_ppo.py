@@ -21,6 +21,7 @@ from paper_2509_00217_b200.env import SearchEnv, replay_eval_log  # noqa: E402
 from paper_2509_00217_b200.knobs import PpoConfig  # noqa: E402
 from paper_2509_00217_b200.policy import EliteBuffer  # noqa: E402
 from paper_2509_00217_b200.ppo import GpuSearch, run_search  # noqa: E402
+from ppo_torch_engine import ppo_loss, run_search_torch  # noqa: E402
 
 GOLD = np.load(Path(__file__).parent / "golden" / "ppo_reference.npz")
 META = json.loads(str(GOLD["meta"]))
@@ -51,7 +52,7 @@ def test_tiny_search_reproduces_reference_trajectory(case, engine):
     name, seed = case.rsplit("_", 1)
     m = META[case]
     env, _ = make_env(name, m["evals"])
-    rep = run_search(env, PpoConfig(budget=m["evals"]), int(seed), engine=engine)
+    rep = (run_search if engine == "fused" else run_search_torch)(env, PpoConfig(budget=m["evals"]), int(seed))
     assert rep.evals == m["evals"] == len(env.eval_log)
     k = prefix(env, case)
     if engine == "torch":
@@ -164,8 +165,9 @@ def test_early_exits_roll_budget_forward_and_still_spend_all():
 def test_graphs_and_eager_agree(engine):
     a, _ = make_env("tiny", 60)
     b, _ = make_env("tiny", 60)
-    ra = run_search(a, PpoConfig(budget=60), 4, use_graphs=True, engine=engine)
-    rb = run_search(b, PpoConfig(budget=60), 4, use_graphs=False, engine=engine)
+    run = run_search if engine == "fused" else run_search_torch
+    ra = run(a, PpoConfig(budget=60), 4, use_graphs=True)
+    rb = run(b, PpoConfig(budget=60), 4, use_graphs=False)
     assert ra.rewards == rb.rewards and ra.restarts == rb.restarts
 
 
@@ -231,7 +233,6 @@ def test_fused_forward_matches_autograd_policy():
 def test_fused_gradient_and_adam_match_autograd():
     import ctypes
     from paper_2509_00217_b200 import _native
-    from paper_2509_00217_b200.ppo import ppo_loss
 
     search, _ = _search(epochs_per_update=1)
     rng = _randomize(search, 1)
@@ -274,8 +275,8 @@ def test_fused_gradient_and_adam_match_autograd():
 def test_fused_and_torch_engines_agree_on_early_trajectory():
     a, _ = make_env("moe_1p2t_h100", 200)
     b, _ = make_env("moe_1p2t_h100", 200)
-    ra = run_search(a, PpoConfig(budget=200), 7, engine="fused")
-    rb = run_search(b, PpoConfig(budget=200), 7, engine="torch")
+    ra = run_search(a, PpoConfig(budget=200), 7)
+    rb = run_search_torch(b, PpoConfig(budget=200), 7)
     same = 0
     for x, y in zip(a.eval_log, b.eval_log):
         if x.vector != y.vector or x.reward != y.reward:

@@ -20,7 +20,7 @@ from paper_2509_00217_b200.config import load_workload
 from paper_2509_00217_b200.knobs import PpoConfig
 from paper_2509_00217_b200.policy import (CheckpointError, EliteBuffer, TorchPolicy, build_observation, head_masks,
                                           load_checkpoint, sample_actions, save_checkpoint)
-from paper_2509_00217_b200.ppo import ppo_loss
+from ppo_torch_engine import ppo_loss
 from paper_2509_00217_b200.strategy import canonical_fused_ops
 
 GOLD = np.load(Path(__file__).parent / "golden" / "policy_reference.npz")

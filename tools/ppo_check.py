@@ -51,8 +51,7 @@ def main():
             env = SearchEnv(wl.model, wl.hw, wl.space, wl.context_len, m["evals"], slo_tpot=wl.slo_tpot)
             env.evaluator  # build tables outside the timed search
             t0 = time.perf_counter()
-            report = run_search(env, PpoConfig(budget=m["evals"]), int(seed), use_graphs=not args.no_graphs,
-                                engine=args.engine)
+            report = run_search(env, PpoConfig(budget=m["evals"]), int(seed), use_graphs=not args.no_graphs)
             wall = time.perf_counter() - t0
             vecs = np.asarray([r.vector for r in env.eval_log], dtype=np.uint8)
             rews = np.asarray([r.reward for r in env.eval_log])

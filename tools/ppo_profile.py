@@ -31,8 +31,7 @@ def main():
     env.evaluator
     stats = {}
     t0 = time.perf_counter()
-    rep = run_search(env, PpoConfig(budget=args.budget, chunks=args.chunks), 0, use_graphs=not args.no_graphs,
-                     engine=args.engine, stats=stats)
+    rep = run_search(env, PpoConfig(budget=args.budget, chunks=args.chunks), 0, use_graphs=not args.no_graphs, stats=stats)
     print(f"budget {args.budget} wall {time.perf_counter() - t0:.4f}s best {rep.best_raw} {stats}")
 
 
