@@ -290,11 +290,15 @@ def ppo_search_line():
         return time.perf_counter() - t0, rep
 
     cold, rep0 = one(4000)
-    wall, rep = one(4000)
+    warm = [one(4000) for _ in range(3)]
+    wall = statistics.median(w for w, _ in warm)
+    rep = warm[0][1]
     return {"workload": "moe_1p2t_h100 PPO run_search, budget 4000, seed 0 (fused policy kernels + CUDA graphs)",
-            "wall_s": wall, "cold_wall_s": cold, "evals": rep.evals, "evals_per_s": rep.evals / wall,
+            "wall_s": wall, "wall_s_runs": [w for w, _ in warm], "cold_wall_s": cold,
+            "cold": "first run_search of the bench process: its context, tables, buffers and graph captures",
+            "evals": rep.evals, "evals_per_s": rep.evals / wall,
             "best_raw": rep.best_raw, "reference_wall_s": REF_SEARCH_WALL_S, "reference_best_raw": REF_SEARCH_BEST_RAW,
-            "same_best_as_reference": rep.best_raw == REF_SEARCH_BEST_RAW == rep0.best_raw}
+            "same_best_as_reference": all(r.best_raw == REF_SEARCH_BEST_RAW for r in [rep0] + [r for _, r in warm])}
 
 
 # reference per-call costs on this workload family (63-85 us per
@@ -550,8 +554,7 @@ def run_ours(args, rank, world, local_rank):
         "config": cfg,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * e2e_n * 8,
                 "d2h_bytes_per_step": world * (e2e_n + 8 * nvalid), "candidates_per_gpu": e2e_n,
-                "input": "pinned host uint8 planes [16, n] (the reference's index vectors), packed to 8-byte "
-                         "words on host threads inside the timed region",
+                "input": "pinned host uint8 planes [16, n] (the reference's index vectors), copied as they are",
                 "output": "reason byte per candidate + raw of the valid ones (compact host results)",
                 "api": "Evaluator.evaluate_host_compact -> ls_evaluate_host_compact(LS_HOST_PLANES)",
                 "from_packed_words": e2e_words, "reason_equal_device_batch": e2e_check},
