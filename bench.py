@@ -433,7 +433,7 @@ def run_ours(args, rank, world, local_rank):
                       throughput=torch.empty(n, dtype=torch.float64, device=dev))
     # N > 1: each step's elite all-gather + merge runs on a side stream beside the
     # next step's evaluate (which leaves one SM free for it)
-    sweep = ShardedSweep(ev, k=ELITE_K, overlap=world > 1)
+    sweep = ShardedSweep(ev, k=ELITE_K, overlap=world > 1, group_steps=int(os.environ.get("LS_XCHG_GROUP", "4")))
     if args.diag_reserve is not None:
         ev.reserve_sms(args.diag_reserve)
     if args.diag_no_exchange:  # diagnostics: each rank's fused launches alone (no elite exchange)
@@ -446,8 +446,8 @@ def run_ours(args, rank, world, local_rank):
         # stream operation between them would serialise them
         _, recs, count = sweep.run(cands, index_base=base, out=out)
         # our kernels per step: the fused evaluate (its last CTA merges the CTA lists);
-        # N > 1: + the NCCL all-gather and the cross-rank merge (side stream)
-        return recs, count, 1 + (sweep.launches_per_merge if world > 1 else 0)
+        # N > 1: + per group of steps one NCCL all-gather and one merge launch (side stream)
+        return recs, count, 1 + ((2 / sweep.group_steps) if world > 1 else 0)
 
     for _ in range(args.warmup):
         step()
@@ -461,7 +461,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize(dev)
     t_start.record(stream)
-    launches = 0
+    launches = 0.0
     for _ in range(args.steps):
         recs, count, nl = step()
         launches += nl
@@ -566,7 +566,7 @@ def run_ours(args, rank, world, local_rank):
                      "kernel_ms_avg": kern_avg, "peak_source": f"{pk_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "timing": "CUDA events around the K back-to-back fused launches on their stream, / K "
                                "(consecutive launches overlap under programmatic dependent launch)"},
-        "gpu_launches": launches,
+        "gpu_launches": int(round(launches)),
         "clocks": clk,
         "parity": parity,
         "elite_best": {"vector": list(elite[0].vector), "raw": elite[0].raw, "index": elite[0].index} if elite else None,

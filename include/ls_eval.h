@@ -268,9 +268,18 @@ int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int
              int32_t* count_out, void* scratch, void* stream);
 
 /* Merge m device-resident record lists (e.g. the all-gathered per-rank top-k)
- * into the global top-k with the same ordering and dedupe rule. */
+ * into the global top-k with the same ordering and dedupe rule. List l starts
+ * at recs[l * k_in] (k_in: the list stride in records, >= its count). */
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                   ls_elite_rec* out, int32_t* count_out, void* stream);
+/* The cross-rank merge of a group of exchanged steps in one launch: `blocks`
+ * holds, for rank r and step j, the (k + 1) x 32 B exchange block (k records,
+ * then a row starting with the int32 count) at record (r * steps + j) * (k + 1)
+ * — the layout of one all-gather of each rank's consecutive blocks. Step j's
+ * merged top-k goes to out[j * k ..], its count to counts_out[j]. k <= 32. */
+int ls_topk_merge_steps(const void* blocks, int world, int steps, int k, ls_elite_rec* out, int32_t* counts_out,
+                        void* stream);
+
 /* ls_evaluate_topk over packed words (fused path only: k <= 32). */
 int ls_evaluate_packed_topk(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
                             int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,

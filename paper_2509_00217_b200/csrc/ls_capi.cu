@@ -1058,10 +1058,20 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 
+int ls_topk_merge_steps(const void* blocks, int world, int steps, int k, ls_elite_rec* out, int32_t* counts_out,
+                        void* stream) {
+  g_err.clear();
+  if (!blocks || world < 1 || world > 1024 || steps < 1 || k < 1 || k > 32 || !out || !counts_out)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad topk_merge_steps arguments");
+  cudaError_t e = launch_topk_merge_steps(static_cast<const ls_elite_rec*>(blocks), world, steps, k, out, counts_out,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge_steps launch");
+}
+
 int ls_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k, ls_elite_rec* out,
                   int32_t* count_out, void* stream) {
   g_err.clear();
-  if (!recs || !counts || m < 1 || k_in < 1 || k_in > 64 || k < 1 || k > 64 || !out || !count_out)
+  if (!recs || !counts || m < 1 || k_in < 1 || k_in > (1 << 20) || k < 1 || k > 64 || !out || !count_out)
     return fail(LS_ERR_INVALID_ARGUMENT, "bad topk_merge arguments");
   cudaError_t e =
       launch_topk_merge(recs, counts, m, k_in, k, nullptr, out, count_out, static_cast<cudaStream_t>(stream));

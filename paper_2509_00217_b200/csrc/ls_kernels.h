@@ -116,6 +116,8 @@ size_t topk_scratch_bytes(int64_t n, int k, int num_sms);
 cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t stride, const uint8_t* reason,
                         const double* thr, const double* key, int64_t n, int k, int64_t index_base,
                         ls_elite_rec* out, int32_t* count_out, void* scratch, int num_sms, cudaStream_t s);
+cudaError_t launch_topk_merge_steps(const ls_elite_rec* blocks, int world, int steps, int k, ls_elite_rec* out,
+                                    int32_t* counts_out, cudaStream_t s);
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);

@@ -318,13 +318,29 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const ls_elite
 constexpr int kMergeThreads = 1024;
 constexpr int kMergeWarps = kMergeThreads / 32;
 
+// ROWS: list l's count is the int32 at the start of record k of that list (the
+// exchange block layout: k records + a count row) instead of counts[l]; block b
+// merges the lists starting at recs + b * step_stride into out + b * k,
+// count_out[b] (one launch for a group of steps).
+template <bool ROWS>
 __global__ void __launch_bounds__(kMergeThreads) topk_merge_fast_kernel(const ls_elite_rec* __restrict__ recs,
                                                                         const int32_t* __restrict__ counts, int m,
                                                                         int k_in, int k,
                                                                         const unsigned long long* floor,
                                                                         ls_elite_rec* __restrict__ out,
-                                                                        int32_t* __restrict__ count_out) {
+                                                                        int32_t* __restrict__ count_out,
+                                                                        int64_t step_stride = 0) {
   __shared__ Rec slots[kMergeWarps][32];
+  __shared__ int s_counts[ROWS ? 1024 : 1];
+  if (ROWS) {
+    recs += (int64_t)blockIdx.x * step_stride;
+    out += (int64_t)blockIdx.x * k;
+    count_out += blockIdx.x;
+    for (int l = threadIdx.x; l < m; l += kMergeThreads)
+      s_counts[l] = *reinterpret_cast<const int32_t*>(recs + (int64_t)l * k_in + k);
+    __syncthreads();
+    counts = s_counts;
+  }
   __shared__ int slot_count[kMergeWarps];
   __shared__ double s_fk[kMergeWarps];
   __shared__ int64_t s_fi[kMergeWarps];
@@ -334,7 +350,7 @@ __global__ void __launch_bounds__(kMergeThreads) topk_merge_fast_kernel(const ls
   double fk = floor ? read_floor(floor) : -1.0e308;
   int64_t fi = INT64_MAX;
   for (int l = threadIdx.x; l < m; l += kMergeThreads)
-    if (__ldg(counts + l) >= k && k <= k_in) {
+    if ((ROWS ? counts[l] : __ldg(counts + l)) >= k && k <= k_in) {
       const ls_elite_rec& e = recs[(int64_t)l * k_in + k - 1];
       if (better(e.key, e.index, fk, fi)) {
         fk = e.key;
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(kMergeThreads) topk_merge_fast_kernel(const ls
   wl.init();
   for (int l0 = w * 32; l0 < m; l0 += kMergeThreads) {
     const int l = l0 + lane;
-    const int c = l < m ? min(__ldg(counts + l), k_in) : 0;
+    const int c = l < m ? min(ROWS ? counts[l] : __ldg(counts + l), k_in) : 0;
     int cmax = c;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
@@ -500,6 +516,14 @@ cudaError_t launch_valid_compact(const uint8_t* reason, const double* thr, int64
   return cudaGetLastError();
 }
 
+cudaError_t launch_topk_merge_steps(const ls_elite_rec* blocks, int world, int steps, int k, ls_elite_rec* out,
+                                    int32_t* counts_out, cudaStream_t s) {
+  // rank r's block of step j: blocks + (r * steps + j) * (k + 1) records
+  topk_merge_fast_kernel<true><<<steps, kMergeThreads, 0, s>>>(blocks, nullptr, world, steps * (k + 1), k, nullptr, out,
+                                                              counts_out, (int64_t)(k + 1));
+  return cudaGetLastError();
+}
+
 size_t scan_scratch_bytes(int64_t n) {
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   return (size_t)(2 * (tiles > 0 ? tiles : 1)) * sizeof(double);
@@ -545,7 +569,7 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
   if (k <= 32) {
     topk_local_kernel<RegList><<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k,
                                                           index_base, part, counts);
-    topk_merge_fast_kernel<<<1, kMergeThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
+    topk_merge_fast_kernel<false><<<1, kMergeThreads, 0, s>>>(part, counts, c, k, k, nullptr, out, count_out);
   } else {
     topk_local_kernel<WarpList><<<c, kTopkThreads, 0, s>>>(tm, planes, stride, reason, thr, key, n > 0 ? n : 0, k,
                                                            index_base, part, counts);
@@ -558,7 +582,7 @@ cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, i
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s) {
   if (k <= 32)
-    topk_merge_fast_kernel<<<1, kMergeThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
+    topk_merge_fast_kernel<false><<<1, kMergeThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
   else
     topk_merge_kernel<WarpList><<<1, kTopkThreads, 0, s>>>(recs, counts, m, k_in, k, floor, out, count_out);
   return cudaGetLastError();

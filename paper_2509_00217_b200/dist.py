@@ -25,6 +25,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
+from ._native import check
+
 __all__ = ["shard_range", "exclusive_prefix_best", "ShardedSweep", "SweepResult"]
 
 
@@ -61,11 +63,16 @@ class SweepResult:
 class ShardedSweep:
     """Evaluate a globally indexed batch split across ranks and merge the elite."""
 
-    launches_per_merge = 2  # the NCCL all-gather kernel + ls_topk_merge
+    launches_per_merge = 2  # without grouping: the NCCL all-gather kernel + ls_topk_merge (per step)
 
-    def __init__(self, evaluator, k: int = 8, group=None, overlap: bool = False):
-        """``overlap``: run each step's exchange on a side stream so the caller's
-        stream goes straight on to the next batch; ``wait()`` joins it."""
+    def __init__(self, evaluator, k: int = 8, group=None, overlap: bool = False, group_steps: int = 4):
+        """``overlap``: run the exchanges on a side stream so the caller's stream goes
+        straight on to the next batch; ``wait()`` joins it. With packed words the
+        exchange is batched: every ``group_steps`` steps the side stream waits ONCE
+        for the last launch's completion signal (ls_stream_wait_signal), all-gathers
+        the group's per-rank lists in one collective and merges each step's — a wait
+        on the side stream costs ~15 us of the next fused launch's overlap, so it is
+        paid once per group. The global elite of a step is ready at ``wait()``."""
         self.ev = evaluator
         self.k = int(k)
         self.group = group
@@ -74,15 +81,21 @@ class ShardedSweep:
         dev = evaluator.device
         self.transport = "local" if self.world == 1 else "nccl"
         self.overlap = bool(overlap) and self.world > 1
-        nbuf = 4 if self.overlap else 1
-        # one message per rank: k records + a 32-byte row holding the count
-        self._sends = [torch.zeros((self.k + 1, 32), dtype=torch.uint8, device=dev) for _ in range(nbuf)]
-        self._gathered = [torch.empty((self.world * (self.k + 1), 32), dtype=torch.uint8, device=dev)
-                          for _ in range(nbuf)]
-        self._merged = [(torch.empty((self.k, 32), dtype=torch.uint8, device=dev),
-                         torch.zeros(1, dtype=torch.int32, device=dev)) for _ in range(nbuf)]
-        self._free = [None] * nbuf  # side-stream event: slot's buffers no longer read
-        self._slot = 0
+        G = max(1, int(group_steps)) if self.overlap else 1
+        self.group_steps = G
+        nbuf = 2 * G if self.overlap else 1  # two groups in flight
+        rows = self.k + 1  # one message per rank and step: k records + a row holding the count
+        self._sendbuf = torch.zeros((nbuf, rows, 32), dtype=torch.uint8, device=dev)
+        self._sends = [self._sendbuf[i] for i in range(nbuf)]
+        self._gathered = [torch.empty((self.world * G * rows, 32), dtype=torch.uint8, device=dev)
+                          for _ in range(2 if self.overlap else 1)]
+        self._mrecs = torch.zeros((nbuf, self.k, 32), dtype=torch.uint8, device=dev)
+        self._mcount = torch.zeros(nbuf, dtype=torch.int32, device=dev)
+        self._merged = [(self._mrecs[i], self._mcount[i:i + 1]) for i in range(nbuf)]
+        self._free = [None, None]  # side-stream event per group: its buffers no longer read
+        self._grp = 0       # group being filled
+        self._in_grp = 0    # steps launched into it
+        self._last = 0      # slot of the last launched step
         self._seq = 0
         self._signal = torch.zeros(1, dtype=torch.int32, device=dev)  # last fused launch whose elite is written
         self._side = torch.cuda.Stream(dev) if self.overlap else None
@@ -92,7 +105,7 @@ class ShardedSweep:
     @property
     def _send(self) -> torch.Tensor:
         """The send block the next evaluation writes into (k records + count row)."""
-        return self._sends[self._slot]
+        return self._sends[self._grp * self.group_steps + self._in_grp]
 
     def run(self, candidates: torch.Tensor, index_base: int, out=None, verdicts: bool = True):
         """Score this rank's candidates (global indices index_base..) and return the global elite.
@@ -100,57 +113,77 @@ class ShardedSweep:
         ``candidates``: [A, n] uint8 planes, or n packed 64-bit words.
         Returns (out, recs, count) with recs/count the merged global top-k on device
         (with ``overlap``, valid on the caller's stream only after ``wait()``).
-
-        With ``overlap`` and packed words, nothing but the fused launch is put on the
-        caller's stream: the side stream waits for the launch's completion signal
-        (ls_stream_wait_signal), so consecutive launches keep overlapping (PDL).
         """
+        if self.world == 1:
+            if candidates.dim() == 1:
+                return self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
+                                                    verdicts=verdicts)
+            return self.ev.evaluate_topk(candidates, k=self.k, index_base=index_base, out=out, verdicts=verdicts)
         cur = torch.cuda.current_stream(self.ev.device)
-        free = self._free[self._slot]
-        if self.world > 1 and free is not None and not free.query():
-            cur.wait_event(free)  # the slot's previous exchange is still reading it (rare)
-        into = self._send if self.world > 1 else None
+        if self._in_grp == 0 and self._free[self._grp] is not None and not self._free[self._grp].query():
+            cur.wait_event(self._free[self._grp])  # the group's previous exchange still reads it (rare)
+        slot = self._grp * self.group_steps + self._in_grp
+        into = self._sends[slot]
+        self._last = slot
+        if candidates.dim() == 1 and self.overlap:
+            self._seq += 1
+            out, _, _ = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
+                                                     verdicts=verdicts, into=into, signal=self._signal,
+                                                     seq=self._seq)
+            self._in_grp += 1
+            if self._in_grp == self.group_steps:
+                self._flush()
+            return out, self._merged[slot][0], self._merged[slot][1]
         if candidates.dim() == 1:
-            sig = None
-            if self.overlap:
-                self._seq += 1
-                sig = self._signal
             out, recs, count = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
-                                                            verdicts=verdicts, into=into, signal=sig, seq=self._seq)
+                                                            verdicts=verdicts, into=into)
         else:
             out, recs, count = self.ev.evaluate_topk(candidates, k=self.k, index_base=index_base, out=out,
                                                      verdicts=verdicts, into=into)
-        recs, count = self.merge(recs, count, signalled=candidates.dim() == 1)
+        recs, count = self.merge(recs, count)
         return out, recs, count
 
-    def merge(self, recs: torch.Tensor, count: torch.Tensor, signalled: bool = False):
+    def _flush(self):
+        """Exchange the steps launched into the current group (side stream)."""
+        n, g, G, rows = self._in_grp, self._grp, self.group_steps, self.k + 1
+        if n == 0:
+            return
+        self.ev.wait_signal(self._signal, self._seq, stream=self._side)
+        gathered = self._gathered[g][: self.world * n * rows]
+        with torch.cuda.stream(self._side):
+            dist.all_gather_into_tensor(gathered, self._sendbuf[g * G: g * G + n].reshape(n * rows, 32),
+                                        group=self.group)
+            # rank r's block of step j starts at row (r * n + j) * rows: one merge launch for the group
+            check(self.ev._lib.ls_topk_merge_steps(ctypes.c_void_p(gathered.data_ptr()), self.world, n, self.k,
+                                                   ctypes.c_void_p(self._mrecs[g * G].data_ptr()),
+                                                   ctypes.c_void_p(self._mcount[g * G:].data_ptr()),
+                                                   ctypes.c_void_p(self._side.cuda_stream)))
+            done = torch.cuda.Event()
+            done.record(self._side)
+        self._free[g] = done
+        self._grp ^= 1
+        self._in_grp = 0
+
+    def merge(self, recs: torch.Tensor, count: torch.Tensor):
         """All-gather every rank's device top-k (k x 32 B + count) in ONE collective and merge on device."""
         if self.world == 1:
             return recs, count
-        slot = self._slot
+        slot = self._last
         send = self._sends[slot]
         if recs.data_ptr() != send.data_ptr():  # not produced in place by run()
             send[: self.k].copy_(recs)
             send[self.k, :4].view(torch.int32).copy_(count)
-            signalled = False
-        gathered = self._gathered[slot]
-        cur = torch.cuda.current_stream(self.ev.device)
+        gathered = self._gathered[0][: self.world * (self.k + 1)]
         if self._side is None:
             dist.all_gather_into_tensor(gathered, send, group=self.group)
             return self._merge_gathered(gathered, self._merged[slot])
-        if signalled and self.overlap:
-            self.ev.wait_signal(self._signal, self._seq, stream=self._side)
-        else:
-            ready = torch.cuda.Event()
-            ready.record(cur)
-            self._side.wait_event(ready)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.ev.device))
+        self._side.wait_event(ready)
         with torch.cuda.stream(self._side):
             dist.all_gather_into_tensor(gathered, send, group=self.group)
             res = self._merge_gathered(gathered, self._merged[slot])
-            done = torch.cuda.Event()
-            done.record(self._side)
-        self._free[slot] = done
-        self._slot = (slot + 1) % len(self._sends)
+        torch.cuda.current_stream(self.ev.device).wait_stream(self._side)  # planes: no pipelining
         return res
 
     def _merge_gathered(self, gathered: torch.Tensor, into):
@@ -161,10 +194,11 @@ class ShardedSweep:
 
     def last_local(self):
         """(records, count) this rank contributed to the most recent exchange."""
-        send = self._sends[(self._slot - 1) % len(self._sends)] if self.overlap else self._sends[0]
+        send = self._sends[self._last]
         return send[: self.k], send[self.k, :4].view(torch.int32)
 
     def wait(self) -> None:
-        """Make the caller's stream wait for every exchange issued so far."""
+        """Exchange what is still pending and make the caller's stream wait for every exchange."""
         if self._side is not None:
+            self._flush()
             torch.cuda.current_stream(self.ev.device).wait_stream(self._side)
