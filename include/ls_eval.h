@@ -151,6 +151,17 @@ int ls_ctx_destroy(ls_ctx* ctx);
 /* Size of the encodable space (product of head sizes); 0 if it overflows. */
 uint64_t ls_space_size(const ls_ctx* ctx);
 
+/* Arithmetic of the on-device sweeps (ls_sweep): LS_PREC_FP64 (default) is
+ * bit-exact; LS_PREC_FP32 is the fp32 fast mode — the plan walk on an fp32
+ * copy of the time tables with plain fp32 sums and division, raw throughput
+ * within 1e-5 relative of the reference's (measured ~2e-6 worst), every verdict
+ * reason exact (integer and memory gates in fp64; the SLO gate re-decided in
+ * fp64 within 1e-5 of the boundary). Elite order may differ from fp64 mode
+ * only among candidates whose raws agree to ~1e-5. Other entry points are
+ * always fp64. */
+enum { LS_PREC_FP64 = 0, LS_PREC_FP32 = 1 };
+int ls_set_precision(ls_ctx* ctx, int precision);
+
 /* Leave `sms` SMs free of the persistent evaluate kernels (default 0), so a
  * concurrent stream (e.g. the cross-rank elite all-gather + merge of the
  * previous step) runs beside them instead of delaying one of their CTAs. */

@@ -143,6 +143,7 @@ _SIGS = {
     "ls_evaluate_topk": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.POINTER(ResultSoA), ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ls_set_precision": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "ls_reserve_sms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "ls_stream_size": (ctypes.c_uint64, [ctypes.c_void_p, ctypes.c_int]),
     "ls_generate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,

@@ -148,6 +148,8 @@ struct ls_ctx {
   int device = 0;
   int num_sms = 148;
   uint64_t* d_tab = nullptr;
+  float* d_tabf = nullptr;   // fp32 copy of the tables (ls_set_precision LS_PREC_FP32)
+  std::atomic<int> precision{0};
   bool smem_gate = false;
   int64_t blocks_tma = 0, blocks_generic = 0;
   int tma_per_sm = 1;
@@ -488,11 +490,30 @@ int ls_ctx_destroy(ls_ctx* c) {
   if (c->one_stream) cudaStreamDestroy(c->one_stream);
   if (c->one) cudaFreeHost(c->one);
   cudaFree(c->d_tab);
+  cudaFree(c->d_tabf);
   delete c;
   return LS_OK;
 }
 
 uint64_t ls_space_size(const ls_ctx* c) { return c ? c->space_size : 0; }
+
+int ls_set_precision(ls_ctx* c, int precision) {
+  g_err.clear();
+  if (!c || (precision != LS_PREC_FP64 && precision != LS_PREC_FP32))
+    return fail(LS_ERR_INVALID_ARGUMENT, "precision must be LS_PREC_FP64 or LS_PREC_FP32");
+  if (precision == LS_PREC_FP32 && !c->d_tabf) {
+    DeviceGuard g(c->device);
+    const size_t bytes = ((size_t)c->L.words * 4 + 15) & ~size_t(15);
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->d_tabf, bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(fp32 tables)");
+    if ((e = cudaMemset(c->d_tabf, 0, bytes)) != cudaSuccess ||
+        (e = build_tables_f32(c->d_tab, c->L.words, c->d_tabf, 0)) != cudaSuccess ||
+        (e = cudaDeviceSynchronize()) != cudaSuccess)
+      return cuda_fail(e, "fp32 tables");
+  }
+  c->precision.store(precision);
+  return LS_OK;
+}
 
 int ls_reserve_sms(ls_ctx* c, int sms) {
   g_err.clear();
@@ -1267,7 +1288,12 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   }
   LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
   const GenMeta& gen = c->gen[mode];
-  lp.sweep_fits = sweep_smem_bytes(c->L, gen.axis_size / gen.lo_size, gen.lo_size) <= c->sweep_smem;
+  const bool f32 = c->precision.load() == LS_PREC_FP32;
+  lp.sweep_fits = sweep_smem_bytes(c->L, gen.axis_size / gen.lo_size, gen.lo_size, f32) <= c->sweep_smem;
+  if (f32) {
+    if (!lp.sweep_fits) return fail(LS_ERR_UNSUPPORTED, "fp32 sweep: tables do not fit in shared memory");
+    lp.tabf = c->d_tabf;
+  }
   if (lp.sweep_fits) lp.max_blocks = tma_grid_cap(c) / c->tma_per_sm;  // one sweep CTA per SM
   const int64_t grid = lp.sweep_fits ? sweep_grid(lp, n) : ws_grid(lp, n, mode);
   TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, start, topk_out, count_out);

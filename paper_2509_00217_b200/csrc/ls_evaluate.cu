@@ -326,11 +326,11 @@ inline size_t ws_dynamic_bytes(int A, int gate_words, bool smem_gate) {
 
 // fp64 pass over n <= 32 survivors (lane i takes entry i of keys/ys), with
 // verdict stores and the optional elite offer. Called by whole warps.
-template <bool NEU, bool FULL, bool TOPK, int MODE, bool SMEM_TAB>
+template <bool NEU, bool FULL, bool TOPK, int MODE, bool SMEM_TAB, bool F32 = false>
 __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, const TabLayout& L, const EvalMeta& M,
                                         const EvalArgs& a, const TopkArgs& tk, const uint64_t* keys,
                                         const uint32_t* ys, int n, RegList& wl, double& gfloor, double& gpend,
-                                        const PackMeta& pk) {
+                                        const PackMeta& pk, const float* Tf = nullptr) {
   const int lane = threadIdx.x & 31;
   int64_t idx = 0;
   Decoded c;
@@ -345,7 +345,7 @@ __device__ __forceinline__ void fp64_batch(const uint64_t* __restrict__ gtab, co
     } else {
       unpack_key(keys[lane], ys[lane], idx, c);
     }
-    full_path<NEU, !SMEM_TAB>(gtab, L, M, c, v);  // gtab: the shared-memory copy when SMEM_TAB
+    full_path<NEU, !SMEM_TAB, F32>(gtab, L, M, c, v, Tf);  // gtab: the shared-memory copy when SMEM_TAB
     if (a.reason) write_verdict<FULL>(a, idx, v);
   }
   if (TOPK) {  // fused elite: valid survivors offered to this warp's list
@@ -1087,12 +1087,16 @@ static_assert(kSwWarps * 32 * sizeof(Rec) + 512 * sizeof(int) + 64 * sizeof(Rec)
 // Shared-memory layout of sweep_kernel: workload table, the stream's two
 // axis tables, per-warp survivor queues.
 struct SwLayout {
-  uint32_t tab, gen_hi, gen_lo, qkey, qy, bytes;
+  uint32_t tab, tabf, gen_hi, gen_lo, qkey, qy, bytes;
 };
-__host__ __device__ inline SwLayout sw_layout(const TabLayout& L, uint32_t hi_size, uint32_t lo_size) {
+// f32: the fp32 fast mode also stages the fp32 copy of the tables
+__host__ __device__ inline uint32_t tabf_bytes(const TabLayout& L) { return ((uint32_t)L.words * 4u + 15u) & ~15u; }
+__host__ __device__ inline SwLayout sw_layout(const TabLayout& L, uint32_t hi_size, uint32_t lo_size,
+                                              bool f32 = false) {
   SwLayout o;
   o.tab = 0;
-  o.gen_hi = (uint32_t)L.words * 8u;
+  o.tabf = (uint32_t)L.words * 8u;
+  o.gen_hi = o.tabf + (f32 ? tabf_bytes(L) : 0u);
   o.gen_lo = o.gen_hi + 4u * hi_size;
   o.qkey = (o.gen_lo + 4u * lo_size + 15u) & ~15u;
   o.qy = o.qkey + 8u * kSwWarps * kSwQueue;
@@ -1136,15 +1140,16 @@ __device__ __forceinline__ void gen_candidate_s(const GenMeta& g, const uint32_t
   c.t = (int)q3;
 }
 
-template <bool NEU, int MODE>
+template <bool NEU, int MODE, bool F32>
 __global__ void __launch_bounds__(kSwThreads, 1)
     sweep_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const int64_t n,
-                 const TopkArgs tk, const GenMeta gm, const SwLayout SL) {
+                 const TopkArgs tk, const GenMeta gm, const SwLayout SL, const float* __restrict__ gtabf) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t tab_bar;
   __shared__ int list_count[kSwWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* T = reinterpret_cast<uint64_t*>(smem + SL.tab);
+  float* Tf = F32 ? reinterpret_cast<float*>(smem + SL.tabf) : nullptr;
   uint32_t* hi_s = reinterpret_cast<uint32_t*>(smem + SL.gen_hi);
   uint32_t* lo_s = reinterpret_cast<uint32_t*>(smem + SL.gen_lo);
   uint64_t* qkey = reinterpret_cast<uint64_t*>(smem + SL.qkey) + warp * kSwQueue;
@@ -1154,8 +1159,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const uint32_t bytes = (uint32_t)L.words * 8u;
-    mbar_expect_tx(&tab_bar, bytes);
+    mbar_expect_tx(&tab_bar, bytes + (F32 ? tabf_bytes(L) : 0u));
     bulk_g2s(T, gtab, bytes, &tab_bar);
+    if (F32) bulk_g2s(Tf, gtabf, tabf_bytes(L), &tab_bar);
   }
   if (threadIdx.x < kSwWarps) list_count[threadIdx.x] = 0;
   const uint32_t hi_size = (uint32_t)(gm.axis_size / gm.lo_size);
@@ -1237,8 +1243,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         if (qcount >= 32) {  // score the newest 32 in place
           __syncwarp();
           qcount -= 32;
-          fp64_batch<NEU, false, true, MODE, true>(T, L, M, a, tk, qkey + qcount, qy + qcount, 32, wl, gfloor, gpend,
-                                                  gm.pk);
+          fp64_batch<NEU, false, true, MODE, true, F32>(T, L, M, a, tk, qkey + qcount, qy + qcount, 32, wl, gfloor,
+                                                       gpend, gm.pk, Tf);
           __syncwarp();
         }
       }
@@ -1251,7 +1257,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   }
   if (qcount > 0) {
     __syncwarp();
-    fp64_batch<NEU, false, true, MODE, true>(T, L, M, a, tk, qkey, qy, qcount, wl, gfloor, gpend, gm.pk);
+    fp64_batch<NEU, false, true, MODE, true, F32>(T, L, M, a, tk, qkey, qy, qcount, wl, gfloor, gpend, gm.pk, Tf);
   }
   if (threadIdx.x == 0) LS_STAMP(2);
   bar_n<kSwWarps>();  // the merge region aliases the tables every warp reads until here
@@ -1261,9 +1267,13 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 template <bool NEU, int MODE>
 void launch_sweep_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, int64_t n,
                     const TopkArgs& tk, const GenMeta& gm, cudaStream_t s) {
-  const SwLayout SL = sw_layout(L, (uint32_t)(gm.axis_size / gm.lo_size), (uint32_t)gm.lo_size);
+  const bool f32 = lp.tabf != nullptr;
+  const SwLayout SL = sw_layout(L, (uint32_t)(gm.axis_size / gm.lo_size), (uint32_t)gm.lo_size, f32);
   const int64_t blocks = sweep_grid(lp, n);
-  sweep_kernel<NEU, MODE><<<(unsigned)blocks, kSwThreads, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL);
+  if (f32)  // plain fp32 sums: the NEU flag does not apply
+    sweep_kernel<false, MODE, true><<<(unsigned)blocks, kSwThreads, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL, lp.tabf);
+  else
+    sweep_kernel<NEU, MODE, false><<<(unsigned)blocks, kSwThreads, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL, nullptr);
 }
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
@@ -1497,23 +1507,27 @@ int64_t sweep_grid(const LaunchPlan& lp, int64_t n) {
   return blocks > lp.max_blocks ? lp.max_blocks : blocks;
 }
 
-size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size) {
-  return sw_layout(L, (uint32_t)hi_size, (uint32_t)lo_size).bytes;
+size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, bool f32) {
+  return sw_layout(L, (uint32_t)hi_size, (uint32_t)lo_size, f32).bytes;
 }
 
 // Opt every sweep kernel into the largest dynamic shared memory the device
 // allows beside its static shared memory; returns that dynamic budget.
 size_t prepare_sweep_kernels(size_t optin) {
   cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, sweep_kernel<true, GEN_ENUM_ADMISSIBLE>);
+  cudaFuncGetAttributes(&fa, sweep_kernel<true, GEN_ENUM_ADMISSIBLE, false>);
   const size_t budget = optin > fa.sharedSizeBytes + 1024 ? optin - fa.sharedSizeBytes - 1024 : 0;
   const int b = (int)budget;
-  cudaFuncSetAttribute(sweep_kernel<true, GEN_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  cudaFuncSetAttribute(sweep_kernel<true, GEN_ENUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  cudaFuncSetAttribute(sweep_kernel<true, GEN_ENUM_ADMISSIBLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  cudaFuncSetAttribute(sweep_kernel<false, GEN_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  cudaFuncSetAttribute(sweep_kernel<false, GEN_ENUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  cudaFuncSetAttribute(sweep_kernel<false, GEN_ENUM_ADMISSIBLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  auto set = [b](auto kern) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, b); };
+  set(sweep_kernel<true, GEN_UNIFORM, false>);
+  set(sweep_kernel<true, GEN_ENUM, false>);
+  set(sweep_kernel<true, GEN_ENUM_ADMISSIBLE, false>);
+  set(sweep_kernel<false, GEN_UNIFORM, false>);
+  set(sweep_kernel<false, GEN_ENUM, false>);
+  set(sweep_kernel<false, GEN_ENUM_ADMISSIBLE, false>);
+  set(sweep_kernel<false, GEN_UNIFORM, true>);  // fp32 fast mode: no compensation (NEU irrelevant)
+  set(sweep_kernel<false, GEN_ENUM, true>);
+  set(sweep_kernel<false, GEN_ENUM_ADMISSIBLE, true>);
   return cudaGetLastError() == cudaSuccess ? budget : 0;
 }
 
@@ -1588,9 +1602,10 @@ cudaError_t launch_sweep(const LaunchPlan& lp, bool neumaier, int mode, const ui
     if (mode == GEN_UNIFORM) launch_sweep_t<NEU, GEN_UNIFORM>(lp, tab, L, M, n, tk, gm, s);
     else if (mode == GEN_ENUM) launch_sweep_t<NEU, GEN_ENUM>(lp, tab, L, M, n, tk, gm, s);
     else launch_sweep_t<NEU, GEN_ENUM_ADMISSIBLE>(lp, tab, L, M, n, tk, gm, s);
+
 #endif
   };
-  if (neumaier) go(std::true_type{});
+  if (neumaier && !lp.tabf) go(std::true_type{});  // fp32 fast mode sums plainly: one instantiation
   else go(std::false_type{});
   return cudaGetLastError();
 }

@@ -12,6 +12,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ls_formulas.cuh"
 #include "ls_tables.cuh"
 
@@ -33,19 +35,19 @@ struct Verdict {
 // TwoSum computes the same exact error (both are exact for finite sums under
 // round-to-nearest), without the compare and selects. Adding 0.0 leaves both
 // f and c unchanged, so an absent term can be added as 0.0 (branch-free).
-template <bool NEU>
+template <bool NEU, typename R = double>
 struct PySum {
-  double f = 0.0, c = 0.0;
-  __device__ __forceinline__ void add(double x) {
-    const double t = f + x;
+  R f = R(0), c = R(0);
+  __device__ __forceinline__ void add(R x) {
+    const R t = f + x;
     if (NEU) {
-      const double xp = t - f, fp = t - xp;
+      const R xp = t - f, fp = t - xp;
       c += (f - fp) + (x - xp);
     }
     f = t;
   }
-  __device__ __forceinline__ double result() const {
-    if (NEU && c != 0.0 && isfinite(c)) return f + c;
+  __device__ __forceinline__ R result() const {
+    if (NEU && c != R(0) && isfinite(c)) return f + c;
     return f;
   }
 };
@@ -146,9 +148,21 @@ __device__ __forceinline__ uint32_t gate_rank(const uint32_t* C, const EvalMeta&
 }
 
 // fp64 pass for a candidate that passed gate(). T: the full table (global).
-template <bool NEU, bool LDG = true>
+//
+// F32 (the fp32 fast mode of ls_sweep, ls_set_precision): the same walk on the
+// fp32 copy of the time tables Tf (each entry the double correctly rounded),
+// plain fp32 sums (no compensation), fp32 division — raw within ~2e-6
+// relative of the fp64 value. The SLO gate is re-decided exactly in fp64 when
+// tpot lies within 1e-5 relative of slo_tpot, so every verdict reason is the
+// reference's; the integer gates and the memory gate run before, in fp64.
+template <bool NEU, bool LDG = true, bool F32 = false>
 __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
-                                          const Decoded& c, Verdict& v) {
+                                          const Decoded& c, Verdict& v, const float* __restrict__ Tf = nullptr) {
+  using R = typename std::conditional<F32, float, double>::type;
+  auto get = [&](int i) -> R {
+    if constexpr (F32) return Tf[i];
+    else return tget<LDG>(T, i);
+  };
   const int t = c.t, e = c.e, p = c.p, b = c.b;
   const uint32_t yc = canon_y(M, c.Y);
   const int ax_emb = cax(yc, LS_OP_EMBEDDING), ax_qkv = cax(yc, LS_OP_QKV_PROJ);
@@ -164,24 +178,24 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   const bool tp_gt1 = tpv > 1, ep_gt1 = epv > 1;
 
   // layer plan compute: qkv, kv, attn, out, router, ffn1, ffn2[, sh1, sh2]
-  PySum<NEU> lc;
-  lc.add(tget<LDG>(T, L.opt_qkv + ax_qkv * nt * nb + tb));
-  lc.add(tget<LDG>(T, L.opt_kv + a2 * nt * nb + tb));
-  lc.add(tget<LDG>(T, L.opt_attn + a2 * nt * nb + tb));
-  lc.add(tget<LDG>(T, L.opt_out + ax_out * nt * nb + tb));
-  lc.add(tget<LDG>(T, L.opt_router + b));
-  lc.add(tget<LDG>(T, L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
-  lc.add(tget<LDG>(T, L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
+  PySum<NEU && !F32, R> lc;
+  lc.add(get(L.opt_qkv + ax_qkv * nt * nb + tb));
+  lc.add(get(L.opt_kv + a2 * nt * nb + tb));
+  lc.add(get(L.opt_attn + a2 * nt * nb + tb));
+  lc.add(get(L.opt_out + ax_out * nt * nb + tb));
+  lc.add(get(L.opt_router + b));
+  lc.add(get(L.opt_ffn1 + ax_f1 * nt * ne * nb + teb));
+  lc.add(get(L.opt_ffn2 + ax_f2 * nt * ne * nb + teb));
   if (L.has_shared) {
-    lc.add(tget<LDG>(T, L.opt_sh1 + ax_s1 * nt * nb + tb));
-    lc.add(tget<LDG>(T, L.opt_sh2 + ax_s2 * nt * nb + tb));
+    lc.add(get(L.opt_sh1 + ax_s1 * nt * nb + tb));
+    lc.add(get(L.opt_sh2 + ax_s2 * nt * nb + tb));
   }
   // layer plan collectives in all_collectives() order (layout.py:270-275);
   // a collective that is not emitted is added as 0.0 (an exact no-op of the
   // sum), so the walk is branch-free: (f) ? time : 0.0 from an in-range slot
-  PySum<NEU> lm;
-#define LS_TP_COLL(cls, f) tget<LDG>(T, L.coll + ((cls) * 2 + ((f) - 1 + ((f) == 0))) * nt * nb + tb)
-#define LS_OPT(f, x) ((f) ? (x) : 0.0)
+  PySum<NEU && !F32, R> lm;
+#define LS_TP_COLL(cls, f) get(L.coll + ((cls) * 2 + ((f) - 1 + ((f) == 0))) * nt * nb + tb)
+#define LS_OPT(f, x) ((f) ? (x) : R(0))
   const int st_attn = a2 ? ST_S : ST_R;
   const int tpm = tp_gt1 ? 3 : 0;  // with tp == 1 no TP collective is emitted (fam & 0)
   int f;
@@ -191,10 +205,10 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));  // feed attn_out_proj
   f = fam(ax_out, ST_R) & tpm;
   lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));  // attention residual
-  const double a2a = ep_gt1 ? tget<LDG>(T, L.a2a + teb) : 0.0;
+  const R a2a = ep_gt1 ? get(L.a2a + teb) : R(0);
   lm.add(a2a);  // expert dispatch (0.0 when ep == 1)
   f = fam(ax_f1, req(ax_f2)) & tpm;
-  lm.add(LS_OPT(f, tget<LDG>(T, L.rtf + (f - 1 + (f == 0)) * nt * ne * nb + teb)));  // feed ffn2
+  lm.add(LS_OPT(f, get(L.rtf + (f - 1 + (f == 0)) * nt * ne * nb + teb)));  // feed ffn2
   if (L.has_shared) {
     f = fam(ax_s1, req(ax_s2)) & tpm;
     lm.add(LS_OPT(f, LS_TP_COLL(CLS_F, f)));  // feed sh2
@@ -209,31 +223,32 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
     f = fam(ax_f2, ST_R) & tpm;
     lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));
   }
-  const double layer_c = lc.result(), layer_m = lm.result();
+  const R layer_c = lc.result(), layer_m = lm.result();
 
   // pre plan (embedding) and post plan (final_norm, lm_head)
-  const double pre_c = 0.0 + tget<LDG>(T, L.opt_emb + ax_emb * nt * nb + tb);
+  const R pre_c = R(0) + get(L.opt_emb + ax_emb * nt * nb + tb);
   f = fam(ax_emb, ST_R) & tpm;
-  const double pre_m = 0.0 + LS_OPT(f, LS_TP_COLL(CLS_H, f));
+  const R pre_m = R(0) + LS_OPT(f, LS_TP_COLL(CLS_H, f));
   f = fam(ax_lmh, ST_R) & tpm;
-  const double post_m = 0.0 + LS_OPT(f, LS_TP_COLL(CLS_V, f));
+  const R post_m = R(0) + LS_OPT(f, LS_TP_COLL(CLS_V, f));
 #undef LS_TP_COLL
 #undef LS_OPT
-  PySum<NEU> po;
-  po.add(tget<LDG>(T, L.opt_norm + b));
-  po.add(tget<LDG>(T, L.opt_lmh + ax_lmh * nt * nb + tb));
-  const double post_c = po.result();
+  PySum<NEU && !F32, R> po;
+  po.add(get(L.opt_norm + b));
+  po.add(get(L.opt_lmh + ax_lmh * nt * nb + tb));
+  const R post_c = po.result();
 
   // totals and pipeline stages (simulator.py:286-323)
   const int64_t world = tpv * epv * ppv;
-  const double hop = ppv > 1 ? tget<LDG>(T, L.hop + (world <= M.node_size ? nb : 0) + b) : 0.0;
-  const double compute = (M.num_layers_d * layer_c + pre_c) + post_c;
-  const double comm = (M.num_layers_d * layer_m + pre_m) + post_m;
-  const double pipe = tget<LDG>(T, L.ppm1_d + p) * hop;
-  const double tpot = (compute + comm) + pipe;
-  const double body = tget<LDG>(T, L.lps_d + p) * (layer_c + layer_m);
-  const double c0 = body + (pre_c + pre_m);
-  double cmax;
+  const R hop = ppv > 1 ? get(L.hop + (world <= M.node_size ? nb : 0) + b) : R(0);
+  const R nl = (R)M.num_layers_d;
+  const R compute = (nl * layer_c + pre_c) + post_c;
+  const R comm = (nl * layer_m + pre_m) + post_m;
+  const R pipe = get(L.ppm1_d + p) * hop;
+  const R tpot = (compute + comm) + pipe;
+  const R body = get(L.lps_d + p) * (layer_c + layer_m);
+  const R c0 = body + (pre_c + pre_m);
+  R cmax;
   if (ppv == 1) {
     cmax = c0 + (post_c + post_m);
   } else {
@@ -245,14 +260,21 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
   v.comp = compute;
   v.comm = comm;
   v.pipe = pipe;
+  if (F32) {  // near the SLO boundary the fp32 tpot cannot decide gate 4: redo it in fp64
+    const R slo = (R)M.slo_tpot;
+    if (fabs(tpot - slo) <= (R)1e-5 * slo) {
+      full_path<NEU, LDG, false>(T, L, M, c, v);
+      return;
+    }
+  }
   // gate 4: tpot > slo_tpot (simulator.py:325)
-  if (tpot > M.slo_tpot) {
+  if ((double)tpot > M.slo_tpot) {
     v.reason = LS_REASON_SLO_VIOLATION;
     v.thr = 0.0;
     return;
   }
   v.reason = LS_REASON_NONE;
-  v.thr = (tget<LDG>(T, L.batch_d + b) / cmax) / (double)world;
+  v.thr = (double)((get(L.batch_d + b) / cmax) / (R)world);
 }
 
 }  // namespace ls

@@ -15,6 +15,7 @@
 namespace ls {
 
 __host__ __device__ inline double py_max(double a, double b) { return b > a ? b : a; }
+__host__ __device__ inline float py_max(float a, float b) { return b > a ? b : a; }
 __host__ __device__ inline double py_min(double a, double b) { return b < a ? b : a; }
 
 // op_time, simulator.py:100-104

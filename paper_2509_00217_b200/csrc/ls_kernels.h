@@ -24,6 +24,7 @@ struct LaunchPlan {
   int64_t max_blocks;
   bool sweep_fits = false;  // ls_sweep: sweep_kernel's tables fit in shared memory (else eval_ws_kernel)
   bool pdl = false;         // fused evaluate + elite: programmatic dependent launch
+  const float* tabf = nullptr;  // ls_sweep fp32 fast mode: the fp32 copy of the tables
 };
 
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
@@ -81,7 +82,8 @@ cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_
                         cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode);  // CTAs of one eval_ws_kernel launch
 int64_t sweep_grid(const LaunchPlan& lp, int64_t n);         // CTAs of one sweep_kernel launch (ls_sweep)
-size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size);
+size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, bool f32);
+cudaError_t build_tables_f32(const uint64_t* tab, int words, float* out, cudaStream_t s);
 size_t prepare_sweep_kernels(size_t optin);  // -> dynamic shared memory budget of sweep_kernel
 int fused_k_max();
 cudaError_t launch_evaluate_topk(const LaunchPlan& lp, bool neumaier, const uint64_t* tab, const TabLayout& L,

@@ -196,4 +196,18 @@ cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void tables_f32_kernel(const uint64_t* __restrict__ tab, int words, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < words) out[i] = (float)__longlong_as_double((long long)tab[i]);  // round to nearest
+}
+}  // namespace
+
+// fp32 copy of every table word read as a double (only the time segments are
+// read from it, by the fp32 fast mode of ls_sweep).
+cudaError_t build_tables_f32(const uint64_t* tab, int words, float* out, cudaStream_t s) {
+  tables_f32_kernel<<<(words + 255) / 256, 256, 0, s>>>(tab, words, out);
+  return cudaGetLastError();
+}
+
 }  // namespace ls

@@ -144,6 +144,15 @@ class Evaluator:
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(self._lib.ls_stream_wait_signal(ctypes.c_void_p(st.cuda_stream), _ptr(signal), int(seq)))
 
+    def set_precision(self, precision: str) -> None:
+        """"fp64" (default, bit-exact) or "fp32": the fp32 fast mode of the on-device
+        sweeps (``sweep`` / ``exhaustive_search`` / ``random_sweep``), raw within 1e-5
+        relative, reasons exact (ls_set_precision)."""
+        modes = {"fp64": 0, "fp32": 1}
+        if precision not in modes:
+            raise ValueError(f"precision must be 'fp64' or 'fp32', got {precision!r}")
+        check(self._lib.ls_set_precision(self._ctx, modes[precision]))
+
     def reserve_sms(self, sms: int) -> None:
         """Leave ``sms`` SMs free of the persistent evaluate kernels (ls_reserve_sms)."""
         check(self._lib.ls_reserve_sms(self._ctx, int(sms)))

@@ -19,8 +19,11 @@ ap.add_argument("--mode", type=int, default=3)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--k", type=int, default=8)
+ap.add_argument("--fp32", action="store_true", help="the fp32 fast mode (ls_set_precision)")
 args = ap.parse_args()
 ev = Evaluator(load_workload(args.config), device=0)
+if args.fp32:
+    ev.set_precision("fp32")
 n = args.n or (ev.stream_size(args.mode) if args.mode != 1 else 1 << 30)
 recs, count = ev.sweep(args.mode, n, k=args.k)  # warm (stream tables, scratch)
 torch.cuda.synchronize()
