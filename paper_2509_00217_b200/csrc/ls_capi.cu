@@ -927,9 +927,11 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
 // lists and counts. The sync words must be zero before the first call on a
 // buffer; each launch's last CTA leaves its half's words zero again, so a call
 // is one launch (no per-call memset).
-static size_t fused_half_bytes(const ls_ctx* c, int k) {
+// The half size does not depend on k: the second half's sync words sit at the
+// same offset for every call on a buffer, whatever k earlier calls used.
+static size_t fused_half_bytes(const ls_ctx* c, int /*k*/) {
   const size_t lists = (size_t)c->blocks_tma;
-  return (32 + lists * (size_t)k * sizeof(ls_elite_rec) + lists * 4 + 255) & ~size_t(255);
+  return (32 + lists * (size_t)fused_k_max() * sizeof(ls_elite_rec) + lists * 4 + 255) & ~size_t(255);
 }
 
 static uint8_t* fused_half(ls_ctx* c, void* scratch, int k) {

@@ -114,9 +114,9 @@ def test_sa_device_chain_budget_exhaustion():
 
 
 def test_fused_scratch_reuse_across_grids():
-    """One scratch buffer, calls whose CTA counts differ (n from 2^23 down to
-    a handful and back): the sync words the kernel leaves zeroed and the
-    fixed sync-word offset keep every call's elite exact."""
+    """One scratch buffer, calls whose CTA counts and k differ (n from 2^23 down
+    to a handful and back, k from 1 to 32): the sync words the kernel leaves
+    zeroed at fixed offsets keep every call's elite exact."""
     from oracle.cost_model import simulate_planes
     from paper_2509_00217_b200.evaluator import Evaluator
 
@@ -127,8 +127,8 @@ def test_fused_scratch_reuse_across_grids():
     want = simulate_planes(wl.desc(), big, fields=("throughput",))
     d = torch.from_numpy(big).cuda()
     words = ev.pack(d)
-    for n in (1 << 23, 5000, 1 << 21, 37, 1 << 23, 3 << 20):
-        _, recs, count = ev.evaluate_packed_topk(words[:n], k=8, verdicts=False)
+    for n, k in ((1 << 23, 8), (5000, 3), (1 << 21, 32), (37, 8), (1 << 23, 1), (3 << 20, 8), (1 << 20, 16)):
+        _, recs, count = ev.evaluate_packed_topk(words[:n], k=k, verdicts=False)
         got = [(e.raw, e.index) for e in ev.decode_records(recs, count)]
         thr = np.where(want["reason"][:n] == 0, want["throughput"][:n], -1.0)
         order = np.lexsort((np.arange(n), -thr))
@@ -140,4 +140,4 @@ def test_fused_scratch_reuse_across_grids():
             if key not in seen:
                 seen.add(key)
                 exp.append((raw, i))
-        assert got == exp[:8], n
+        assert got == exp[:k], (n, k)

@@ -121,6 +121,17 @@ def main():
                           "space": "admissible-axis" if admissible else "full", "n": rep.evaluated, "ms": rep.device_ms,
                           "evals_per_s": rep.evaluated / rep.device_ms * 1e3,
                           "best": None if b is None else {"vector": list(b.vector), "raw": b.raw, "index": b.index}})
+                if admissible:  # the fp32 fast mode of the same sweep (raw within 1e-5, reasons exact)
+                    ev.set_precision("fp32")
+                    exhaustive_search(ev, admissible_only=True)
+                    rep = exhaustive_search(ev, admissible_only=True)
+                    ev.set_precision("fp64")
+                    b = rep.best
+                    emit(fh, {"kind": "enumerate_fp32", "config": label, "workload": name, "slo_tpot": wl.slo_tpot,
+                              "space": "admissible-axis", "n": rep.evaluated, "ms": rep.device_ms,
+                              "evals_per_s": rep.evaluated / rep.device_ms * 1e3,
+                              "best": None if b is None else {"vector": list(b.vector), "raw": b.raw,
+                                                               "index": b.index}})
         torch.cuda.empty_cache()
 
     wl = load_workload("moe_1p6t_h100x2048")
@@ -135,6 +146,22 @@ def main():
             emit(fh, {"kind": "sizes", "config": "config 5", "workload": "moe_1p6t_h100x2048", "n": n, "ms": ms,
                       "evals_per_s": n / ms * 1e3, "reps": reps,
                       "l2": "resident" if n * 17 < 126e6 else "streamed from HBM"})
+            if n <= 10**6:  # one call on its own (launch + table staging + merges): the latency floor
+                words = uniform_words(ev, n)
+                out = ev._alloc(n, ("throughput",))
+                ev.evaluate_packed_topk(words, k=8, out=out)
+                lat = []
+                for _ in range(50):
+                    torch.cuda.synchronize(ev.device)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    ev.evaluate_packed_topk(words, k=8, out=out)
+                    b.record()
+                    torch.cuda.synchronize(ev.device)
+                    lat.append(a.elapsed_time(b))
+                emit(fh, {"kind": "latency", "config": "config 5", "workload": "moe_1p6t_h100x2048", "n": n,
+                          "ms_median": float(np.median(lat)), "note": "one fused call, synchronised, events around it"})
+                del words, out
             torch.cuda.empty_cache()
             n *= 10
 
