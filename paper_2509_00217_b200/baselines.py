@@ -32,7 +32,7 @@ from .report import SearchReport, build_report
 from .strategy import ActionSpaceSpec, canonical_fused_ops, megatron_fine_dims
 
 __all__ = ["NoValidConfiguration", "SaConfig", "uniform_vector", "mutate_vector", "acceptance_probability",
-           "cosine_decay", "random_walk", "simulated_annealing", "megatron_exhaustive", "SweepReport",
+           "cosine_decay", "random_walk", "simulated_annealing", "sa_draws", "megatron_exhaustive", "SweepReport",
            "exhaustive_search", "random_sweep"]
 
 
@@ -103,7 +103,27 @@ def simulated_annealing(env: SearchEnv, cfg: SaConfig, budget: int, seed: int) -
     steps = min(budget, env.budget_left)
     if steps < 1:
         raise BudgetExhausted(f"budget of {env.budget} evaluations spent")
-    space = env.space
+    init, coords, drawn, u, temperature, moves = sa_draws(env.space, cfg, budget, steps, rng)
+    rc = env.reward_cfg
+    vecs, raws, rewards, reasons, best = env.evaluator.sa_chain(
+        init, coords, drawn, u, temperature, moves, env.best_raw, rc.alpha, rc.beta, rc.invalid_penalty)
+    for i in range(steps):
+        env._append(EvalRecord(env.evals_used, tuple(int(x) for x in vecs[i]), float(raws[i]), float(rewards[i]),
+                               bool(reasons[i] == 0), REASON_NAMES[int(reasons[i])]))
+    env.best_raw = best
+    if steps < budget:  # the reference's next env.step would raise here
+        raise BudgetExhausted(f"budget of {env.budget} evaluations spent")
+    records = env.eval_log[first:first + budget]
+    return build_report("sa", seed, records, (), budget, time.perf_counter() - start)
+
+
+def sa_draws(space: ActionSpaceSpec, cfg: SaConfig, budget: int, steps: int, rng: np.random.Generator):
+    """The randomness of a simulated-annealing chain of ``steps`` evaluations, drawn
+    from ``rng`` exactly as the reference's loop draws it (baselines.py:131-139):
+    the first vector (``uniform_vector``), then per proposal ``mutate_vector``'s
+    ``choice`` + ``integers(k - 1)`` draws and the acceptance ``random()`` — none
+    depends on the chain's decisions. Returns (init, coords, drawn, u,
+    temperature, moves) for ``ls_sa_chain``."""
     init = uniform_vector(space, rng)
     mutable = [i for i, k in enumerate(space.head_sizes) if k > 1]
     moves = min(cfg.neighbor_moves, len(mutable)) if mutable else 0
@@ -120,17 +140,7 @@ def simulated_annealing(env: SearchEnv, cfg: SaConfig, budget: int, seed: int) -
                 coords[step - 1, j] = coord
                 drawn[step - 1, j] = int(rng.integers(space.head_sizes[coord] - 1))
         u[step - 1] = rng.random()
-    rc = env.reward_cfg
-    vecs, raws, rewards, reasons, best = env.evaluator.sa_chain(
-        init, coords, drawn, u, temperature, moves, env.best_raw, rc.alpha, rc.beta, rc.invalid_penalty)
-    for i in range(steps):
-        env._append(EvalRecord(env.evals_used, tuple(int(x) for x in vecs[i]), float(raws[i]), float(rewards[i]),
-                               bool(reasons[i] == 0), REASON_NAMES[int(reasons[i])]))
-    env.best_raw = best
-    if steps < budget:  # the reference's next env.step would raise here
-        raise BudgetExhausted(f"budget of {env.budget} evaluations spent")
-    records = env.eval_log[first:first + budget]
-    return build_report("sa", seed, records, (), budget, time.perf_counter() - start)
+    return init, coords, drawn, u, temperature, moves
 
 
 def _simulated_annealing_host(env: SearchEnv, cfg: SaConfig, budget: int, seed: int) -> SearchReport:
