@@ -149,6 +149,7 @@ struct ls_ctx {
   int num_sms = 148;
   uint64_t* d_tab = nullptr;
   float* d_tabf = nullptr;   // fp32 copy of the tables (ls_set_precision LS_PREC_FP32)
+  double2* d_memo = nullptr;  // layer-sum memo (ls_memo.cu), or null
   std::atomic<int> precision{0};
   bool smem_gate = false;
   int64_t blocks_tma = 0, blocks_generic = 0;
@@ -438,6 +439,23 @@ int ls_ctx_create(const ls_workload_desc* desc, int device, ls_ctx** out) {
     delete c;
     return cuda_fail(e, "build_tables");
   }
+  // the layer-sum memo when it stays small (12.6 MB for the default domains);
+  // LS_MEMO=0 disables it (the walk then sums per candidate)
+  {
+    const int64_t entries = memo_entries(c->L);
+    const char* v = getenv("LS_MEMO");
+    if ((!v || atoi(v) != 0) && entries * (int64_t)sizeof(double2) <= (int64_t(64) << 20)) {
+      if ((e = cudaMalloc(&c->d_memo, sizeof(double2) * (size_t)entries)) != cudaSuccess ||
+          (e = build_memo(c->desc.sum_mode == LS_SUM_NEUMAIER, c->d_tab, c->L, c->M, c->d_memo, 0)) != cudaSuccess ||
+          (e = cudaDeviceSynchronize()) != cudaSuccess) {
+        cudaFree(c->d_memo);
+        cudaFree(c->d_tab);
+        delete c;
+        return cuda_fail(e, "layer-sum memo");
+      }
+      c->M.memo = c->d_memo;
+    }
+  }
   // the workload's tables go to shared memory when they fit beside the ring
   // at the kernel's CTAs-per-SM; otherwise both passes read them through L1
   c->smem_gate = tma_smem_bytes(c->L, c->desc.vector_length, true) <= tma_smem_budget(prop);
@@ -491,6 +509,7 @@ int ls_ctx_destroy(ls_ctx* c) {
   if (c->one) cudaFreeHost(c->one);
   cudaFree(c->d_tab);
   cudaFree(c->d_tabf);
+  cudaFree(c->d_memo);
   delete c;
   return LS_OK;
 }

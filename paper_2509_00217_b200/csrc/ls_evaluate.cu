@@ -1338,6 +1338,11 @@ void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, 
   const size_t smem = ws_dynamic_bytes(M.A, stage_words(L), lp.smem_gate);
   const int64_t blocks = ws_grid(lp, a.n, MODE);
   auto kern = lp.smem_gate ? eval_ws_kernel<NEU, FULL, true, TOPK, MODE> : eval_ws_kernel<NEU, FULL, false, TOPK, MODE>;
+  // the streaming kernel walks the layer sums from its shared-memory table: its
+  // 4 fp64 warps are latency-bound, and dependent L2 reads of the memo slowed
+  // the HBM-bound step by 2%
+  EvalMeta Mw = M;
+  Mw.memo = nullptr;
   if (TOPK && (MODE == GEN_WORDS || MODE == GEN_PLANES) && lp.pdl) {
     // fused steps on one stream overlap: the next launch starts while this
     // one's last CTAs merge (eval_ws_kernel's griddepcontrol)
@@ -1351,9 +1356,9 @@ void launch_ws_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, tab, L, M, a, ntiles, tk, gm);
+    cudaLaunchKernelEx(&cfg, kern, tab, L, Mw, a, ntiles, tk, gm);
   } else {
-    kern<<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, M, a, ntiles, tk, gm);
+    kern<<<(unsigned)blocks, kThreads, smem, s>>>(tab, L, Mw, a, ntiles, tk, gm);
   }
 }
 

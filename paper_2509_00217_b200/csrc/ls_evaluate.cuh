@@ -148,35 +148,21 @@ __device__ __forceinline__ uint32_t gate_rank(const uint32_t* C, const EvalMeta&
 }
 
 // fp64 pass for a candidate that passed gate(). T: the full table (global).
-//
-// F32 (the fp32 fast mode of ls_sweep, ls_set_precision): the same walk on the
-// fp32 copy of the time tables Tf (each entry the double correctly rounded),
-// plain fp32 sums (no compensation), fp32 division — raw within ~2e-6
-// relative of the fp64 value. The SLO gate is re-decided exactly in fp64 when
-// tpot lies within 1e-5 relative of slo_tpot, so every verdict reason is the
-// reference's; the integer gates and the memory gate run before, in fp64.
-template <bool NEU, bool LDG = true, bool F32 = false>
-__device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
-                                          const Decoded& c, Verdict& v, const float* __restrict__ Tf = nullptr) {
-  using R = typename std::conditional<F32, float, double>::type;
+// The layer plan's two Python sums (simulator.py:224-236): compute over
+// qkv, kv, attn, out, router, ffn1, ffn2[, sh1, sh2] and the collectives in
+// all_collectives() order (layout.py:270-275) — functions of (t, e, b) and the
+// axes of qkv, attn (DIM1 or not), out, ffn1, ffn2, sh1, sh2 only.
+template <bool NEU, bool LDG, bool F32, typename R>
+__device__ __forceinline__ void layer_sums(const uint64_t* __restrict__ T, const float* __restrict__ Tf,
+                                           const TabLayout& L, int t, int e, int b, bool tp_gt1, bool ep_gt1,
+                                           int ax_qkv, int a2, int ax_out, int ax_f1, int ax_f2, int ax_s1,
+                                           int ax_s2, R& layer_c, R& layer_m) {
   auto get = [&](int i) -> R {
     if constexpr (F32) return Tf[i];
     else return tget<LDG>(T, i);
   };
-  const int t = c.t, e = c.e, p = c.p, b = c.b;
-  const uint32_t yc = canon_y(M, c.Y);
-  const int ax_emb = cax(yc, LS_OP_EMBEDDING), ax_qkv = cax(yc, LS_OP_QKV_PROJ);
-  const int ax_attn = cax(yc, LS_OP_ATTN_CORE), ax_out = cax(yc, LS_OP_ATTN_OUT_PROJ);
-  const int ax_f1 = cax(yc, LS_OP_EXPERT_FFN1), ax_f2 = cax(yc, LS_OP_EXPERT_FFN2);
-  const int ax_s1 = cax(yc, LS_OP_SHARED_FFN1), ax_s2 = cax(yc, LS_OP_SHARED_FFN2);
-  const int ax_lmh = cax(yc, LS_OP_LM_HEAD);
-  const int a2 = ax_attn == 2;
   const int nt = L.nt, ne = L.ne, nb = L.nb;
   const int tb = t * nb + b, teb = (t * ne + e) * nb + b;
-  const int64_t tpv = (int64_t)tword<LDG>(T, L.tpv + t), epv = (int64_t)tword<LDG>(T, L.epv + e);
-  const int64_t ppv = (int64_t)tword<LDG>(T, L.ppv + p);
-  const bool tp_gt1 = tpv > 1, ep_gt1 = epv > 1;
-
   // layer plan compute: qkv, kv, attn, out, router, ffn1, ffn2[, sh1, sh2]
   PySum<NEU && !F32, R> lc;
   lc.add(get(L.opt_qkv + ax_qkv * nt * nb + tb));
@@ -223,7 +209,66 @@ __device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const 
     f = fam(ax_f2, ST_R) & tpm;
     lm.add(LS_OPT(f, LS_TP_COLL(CLS_H, f)));
   }
-  const R layer_c = lc.result(), layer_m = lm.result();
+  layer_c = lc.result();
+  layer_m = lm.result();
+#undef LS_TP_COLL
+#undef LS_OPT
+}
+
+// Index of a layer-sum memo entry (EvalMeta::memo): (t, e, b) then the axes,
+// mixed radix; the shared-expert axes only when the model has one.
+__device__ __forceinline__ int64_t memo_key(const TabLayout& L, int t, int e, int b, int ax_qkv, int a2, int ax_out,
+                                            int ax_f1, int ax_f2, int ax_s1, int ax_s2) {
+  int64_t k = (((((int64_t)(t * L.ne + e) * L.nb + b) * 3 + ax_qkv) * 2 + a2) * 3 + ax_out) * 3 + ax_f1;
+  k = k * 3 + ax_f2;
+  if (L.has_shared) k = (k * 3 + ax_s1) * 3 + ax_s2;
+  return k;
+}
+
+//
+// F32 (the fp32 fast mode of ls_sweep, ls_set_precision): the same walk on the
+// fp32 copy of the time tables Tf (each entry the double correctly rounded),
+// plain fp32 sums (no compensation), fp32 division — raw within ~2e-6
+// relative of the fp64 value. The SLO gate is re-decided exactly in fp64 when
+// tpot lies within 1e-5 relative of slo_tpot, so every verdict reason is the
+// reference's; the integer gates and the memory gate run before, in fp64.
+template <bool NEU, bool LDG = true, bool F32 = false>
+__device__ __forceinline__ void full_path(const uint64_t* __restrict__ T, const TabLayout& L, const EvalMeta& M,
+                                          const Decoded& c, Verdict& v, const float* __restrict__ Tf = nullptr) {
+  using R = typename std::conditional<F32, float, double>::type;
+  auto get = [&](int i) -> R {
+    if constexpr (F32) return Tf[i];
+    else return tget<LDG>(T, i);
+  };
+  const int t = c.t, e = c.e, p = c.p, b = c.b;
+  const uint32_t yc = canon_y(M, c.Y);
+  const int ax_emb = cax(yc, LS_OP_EMBEDDING), ax_qkv = cax(yc, LS_OP_QKV_PROJ);
+  const int ax_attn = cax(yc, LS_OP_ATTN_CORE), ax_out = cax(yc, LS_OP_ATTN_OUT_PROJ);
+  const int ax_f1 = cax(yc, LS_OP_EXPERT_FFN1), ax_f2 = cax(yc, LS_OP_EXPERT_FFN2);
+  const int ax_s1 = cax(yc, LS_OP_SHARED_FFN1), ax_s2 = cax(yc, LS_OP_SHARED_FFN2);
+  const int ax_lmh = cax(yc, LS_OP_LM_HEAD);
+  const int a2 = ax_attn == 2;
+  const int nt = L.nt, nb = L.nb;
+  const int tb = t * nb + b;
+  const int64_t tpv = (int64_t)tword<LDG>(T, L.tpv + t), epv = (int64_t)tword<LDG>(T, L.epv + e);
+  const int64_t ppv = (int64_t)tword<LDG>(T, L.ppv + p);
+  const bool tp_gt1 = tpv > 1, ep_gt1 = epv > 1;
+
+  // layer sums: from the workload's memo table (exact values computed once
+  // by the same code, layer_sums) or walked here
+  R layer_c, layer_m;
+  if (M.memo) {  // (the fp32 fast mode rounds the exact sums to fp32)
+    const double2 lv = __ldg(M.memo + memo_key(L, t, e, b, ax_qkv, a2, ax_out, ax_f1, ax_f2, ax_s1, ax_s2));
+    layer_c = (R)lv.x;
+    layer_m = (R)lv.y;
+  } else {
+    layer_sums<NEU, LDG, F32, R>(T, Tf, L, t, e, b, tp_gt1, ep_gt1, ax_qkv, a2, ax_out, ax_f1, ax_f2, ax_s1, ax_s2,
+                                 layer_c, layer_m);
+  }
+#define LS_TP_COLL(cls, f) get(L.coll + ((cls) * 2 + ((f) - 1 + ((f) == 0))) * nt * nb + tb)
+#define LS_OPT(f, x) ((f) ? (x) : R(0))
+  const int tpm = tp_gt1 ? 3 : 0;  // with tp == 1 no TP collective is emitted (fam & 0)
+  int f;
 
   // pre plan (embedding) and post plan (final_norm, lm_head)
   const R pre_c = R(0) + get(L.opt_emb + ax_emb * nt * nb + tb);

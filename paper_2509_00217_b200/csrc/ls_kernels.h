@@ -28,6 +28,10 @@ struct LaunchPlan {
 };
 
 cudaError_t build_tables(const ls_workload_desc& d, const TabLayout& L, uint64_t* out, cudaStream_t stream);
+// Layer-sum memo (ls_memo.cu): entries and builder.
+int64_t memo_entries(const TabLayout& L);
+cudaError_t build_memo(bool neumaier, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, double2* memo,
+                       cudaStream_t s);
 
 // Fused evaluate + top-k by raw (eval_ws_kernel<..., TOPK>): every CTA emits
 // its elite list to part[blockIdx.x * k ..] / part_counts[blockIdx.x]; the

@@ -24,6 +24,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <vector_types.h>
+
 #include "../../include/ls_eval.h"
 
 namespace ls {
@@ -105,6 +107,10 @@ struct EvalMeta {
   uint8_t canon_shr[LS_NUM_OPS], canon_len[LS_NUM_OPS], canon_shl[LS_NUM_OPS];
   uint32_t canon_or;  // pinned ops' axes at their canonical fields
   int canon_ident;    // canon_y(Y) == Y (12 controlled ops, heads in canonical order)
+  int pad1_;
+  // layer-sum memo (ls_memo.cu): (layer compute, layer collectives) per
+  // memo_key(t, e, b, layer axes), or null (then walked per candidate)
+  const double2* memo;
 };
 
 __host__ __device__ inline int round2(int w) { return (w + 1) & ~1; }

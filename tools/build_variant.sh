@@ -7,7 +7,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 SRC=$ROOT/paper_2509_00217_b200/csrc
 OUT=/tmp/variant_$NAME; mkdir -p $OUT $ROOT/ab
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-O2 -Xptxas -v $DEFS"
-for f in ls_tables ls_evaluate ls_select ls_search ls_policy ls_capi; do
+for f in ls_tables ls_memo ls_evaluate ls_select ls_search ls_policy ls_capi; do
   nvcc $FLAGS -c -o $OUT/$f.o $SRC/$f.cu 2> $OUT/$f.ptxas &
 done
 wait
