@@ -1185,9 +1185,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   // counter (survivor-heavy chunks cost several times the others, so a static
   // deal leaves SMs idle at the end); the next claim is issued a chunk ahead
   const int64_t nwarps = (int64_t)gridDim.x * kSwWarps;
-  uint32_t claim = 0;
+  uint32_t claim = 0;  // lane 0: the claim in flight (read a whole chunk later)
   if (lane == 0) claim = atomicAdd(tk.tile_ctr, 1u);
-  int64_t nxt = nwarps + __shfl_sync(0xffffffffu, claim, 0);
   for (int64_t ch = (int64_t)blockIdx.x * kSwWarps + warp; ch < nchunks;) {
     const int64_t base = ch * kSwChunk;
     // enumeration: decode the lane's first position once, then step the
@@ -1249,11 +1248,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
       }
     }
-    ch = nxt;
-    if (ch < nchunks) {
-      if (lane == 0) claim = atomicAdd(tk.tile_ctr, 1u);
-      nxt = nwarps + __shfl_sync(0xffffffffu, claim, 0);
-    }
+    ch = nwarps + __shfl_sync(0xffffffffu, claim, 0);
+    if (ch < nchunks && lane == 0) claim = atomicAdd(tk.tile_ctr, 1u);
   }
   if (qcount > 0) {
     __syncwarp();

@@ -217,9 +217,10 @@ __device__ __forceinline__ void layer_sums(const uint64_t* __restrict__ T, const
 
 // Index of a layer-sum memo entry (EvalMeta::memo): (t, e, b) then the axes,
 // mixed radix; the shared-expert axes only when the model has one.
-__device__ __forceinline__ int64_t memo_key(const TabLayout& L, int t, int e, int b, int ax_qkv, int a2, int ax_out,
-                                            int ax_f1, int ax_f2, int ax_s1, int ax_s2) {
-  int64_t k = (((((int64_t)(t * L.ne + e) * L.nb + b) * 3 + ax_qkv) * 2 + a2) * 3 + ax_out) * 3 + ax_f1;
+// (32-bit: the memo is built only below 2^22 entries)
+__device__ __forceinline__ int memo_key(const TabLayout& L, int t, int e, int b, int ax_qkv, int a2, int ax_out,
+                                        int ax_f1, int ax_f2, int ax_s1, int ax_s2) {
+  int k = (((((t * L.ne + e) * L.nb + b) * 3 + ax_qkv) * 2 + a2) * 3 + ax_out) * 3 + ax_f1;
   k = k * 3 + ax_f2;
   if (L.has_shared) k = (k * 3 + ax_s1) * 3 + ax_s2;
   return k;
