@@ -363,13 +363,13 @@ class Evaluator:
                                            self._stream()))
         return out
 
-    def _fused_scratch(self, n: int, k: int) -> torch.Tensor:
+    def _fused_scratch(self, n: int, k: int, stream=None) -> torch.Tensor:
         """Scratch of the fused evaluate + elite kernels, one buffer per CUDA stream
         (calls on different streams may overlap and must not share the CTA lists
         and sync words). Zero-filled once: every call leaves its sync words zero.
         A buffer is only ever used on the stream it was allocated on."""
         nbytes = int(self._lib.ls_evaluate_topk_scratch_bytes(self._ctx, int(n), int(k)))
-        key = torch.cuda.current_stream(self.device).cuda_stream
+        key = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         buf = self._scratch.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.zeros(max(nbytes, 4096), dtype=torch.uint8, device=self.device)
@@ -380,9 +380,9 @@ class Evaluator:
         """(records, count) outputs: fresh tensors, or views of a caller's [(k + 1), 32]
         uint8 buffer (records in rows 0..k-1, the int32 count at the start of row k) —
         one contiguous message for the cross-rank all-gather."""
-        if into is None:
-            return (torch.empty((k, _REC_BYTES), dtype=torch.uint8, device=self.device),
-                    torch.empty(1, dtype=torch.int32, device=self.device))
+        if into is None:  # one allocation for both
+            into = torch.empty((k + 1, _REC_BYTES), dtype=torch.uint8, device=self.device)
+            return into[:k], into[k, :4].view(torch.int32)
         if into.shape != (k + 1, _REC_BYTES) or into.dtype != torch.uint8 or not into.is_contiguous():
             raise ValueError("into must be a contiguous [(k + 1), 32] uint8 tensor")
         return into[:k], into[k, :4].view(torch.int32)
@@ -399,17 +399,17 @@ class Evaluator:
             out = self._alloc(n, fields)
         soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if verdicts else None
         recs, count = self._elite_out(k, into)
-        scratch = self._fused_scratch(n, k)
+        st = torch.cuda.current_stream(self.device)
+        scratch = self._fused_scratch(n, k, st)
+        sp = ctypes.c_void_p(st.cuda_stream)
         if signal is not None:
             check(self._lib.ls_evaluate_packed_topk_signal(
                 self._ctx, ctypes.c_void_p(words.data_ptr()), n, ctypes.byref(soa) if soa is not None else None,
-                int(k), int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), _ptr(signal), int(seq),
-                self._stream()))
+                int(k), int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), _ptr(signal), int(seq), sp))
         else:
             check(self._lib.ls_evaluate_packed_topk(self._ctx, ctypes.c_void_p(words.data_ptr()), n,
                                                     ctypes.byref(soa) if soa is not None else None, int(k),
-                                                    int(index_base), _ptr(recs), _ptr(count), _ptr(scratch),
-                                                    self._stream()))
+                                                    int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), sp))
         return (out if verdicts else None), recs, count
 
     def evaluate_host_packed(self, words: np.ndarray, fields=("throughput",), out: dict | None = None) -> dict:
