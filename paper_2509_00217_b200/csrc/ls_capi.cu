@@ -520,6 +520,7 @@ int ls_set_precision(ls_ctx* c, int precision) {
   g_err.clear();
   if (!c || (precision != LS_PREC_FP64 && precision != LS_PREC_FP32))
     return fail(LS_ERR_INVALID_ARGUMENT, "precision must be LS_PREC_FP64 or LS_PREC_FP32");
+  std::lock_guard<std::mutex> lock(c->gen_mu);
   if (precision == LS_PREC_FP32 && !c->d_tabf) {
     DeviceGuard g(c->device);
     const size_t bytes = ((size_t)c->L.words * 4 + 15) & ~size_t(15);
@@ -949,7 +950,7 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
 // The half size does not depend on k: the second half's sync words sit at the
 // same offset for every call on a buffer, whatever k earlier calls used.
 static size_t fused_half_bytes(const ls_ctx* c, int /*k*/) {
-  const size_t lists = (size_t)c->blocks_tma;
+  const size_t lists = std::max<size_t>((size_t)c->blocks_tma, (size_t)c->num_sms * sweep_ctas_per_sm());
   return (32 + lists * (size_t)fused_k_max() * sizeof(ls_elite_rec) + lists * 4 + 255) & ~size_t(255);
 }
 
@@ -1315,7 +1316,7 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
     if (!lp.sweep_fits) return fail(LS_ERR_UNSUPPORTED, "fp32 sweep: tables do not fit in shared memory");
     lp.tabf = c->d_tabf;
   }
-  if (lp.sweep_fits) lp.max_blocks = tma_grid_cap(c) / c->tma_per_sm;  // one sweep CTA per SM
+  if (lp.sweep_fits) lp.max_blocks = tma_grid_cap(c) / c->tma_per_sm * sweep_ctas_per_sm();
   const int64_t grid = lp.sweep_fits ? sweep_grid(lp, n) : ws_grid(lp, n, mode);
   TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, start, topk_out, count_out);
   cudaError_t e;

@@ -1077,6 +1077,9 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 #ifndef LS_SWEEP_WARPS
 #define LS_SWEEP_WARPS 24
 #endif
+#ifndef LS_SWEEP_CTAS
+#define LS_SWEEP_CTAS 1  // CTAs per SM (each stages its own tables)
+#endif
 constexpr int kSwWarps = LS_SWEEP_WARPS;
 constexpr int kSwThreads = 32 * kSwWarps;
 constexpr int kSwChunk = 256;  // consecutive stream positions per warp chunk
@@ -1141,7 +1144,7 @@ __device__ __forceinline__ void gen_candidate_s(const GenMeta& g, const uint32_t
 }
 
 template <bool NEU, int MODE, bool F32>
-__global__ void __launch_bounds__(kSwThreads, 1)
+__global__ void __launch_bounds__(kSwThreads, LS_SWEEP_CTAS)
     sweep_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const int64_t n,
                  const TopkArgs tk, const GenMeta gm, const SwLayout SL, const float* __restrict__ gtabf) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1499,6 +1502,8 @@ int generic_blocks_per_sm() {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_generic_kernel<true>, kGenericThreads, 0);
   return nb;
 }
+
+int sweep_ctas_per_sm() { return LS_SWEEP_CTAS; }
 
 int64_t sweep_grid(const LaunchPlan& lp, int64_t n) {
   const int64_t chunks = (n + kSwChunk - 1) / kSwChunk;

@@ -86,6 +86,7 @@ cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_
                         cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode);  // CTAs of one eval_ws_kernel launch
 int64_t sweep_grid(const LaunchPlan& lp, int64_t n);         // CTAs of one sweep_kernel launch (ls_sweep)
+int sweep_ctas_per_sm();
 size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, bool f32);
 cudaError_t build_tables_f32(const uint64_t* tab, int words, float* out, cudaStream_t s);
 size_t prepare_sweep_kernels(size_t optin);  // -> dynamic shared memory budget of sweep_kernel
