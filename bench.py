@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=CONFIG)
-    ap.add_argument("--n", type=int, default=1 << 27, help="candidates per GPU per step")
+    ap.add_argument("--candidates-per-gpu", "--n", dest="n", type=int, default=1 << 27,
+                    help="candidates per GPU per step (use the long name under torchrun: --n is ambiguous there)")
     ap.add_argument("--e2e-n", type=int, default=1 << 26, help="candidates per GPU per e2e step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
