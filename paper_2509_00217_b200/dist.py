@@ -116,6 +116,9 @@ class ShardedSweep:
         """
         if self.world == 1:
             if candidates.dim() == 1:
+                if out is not None and verdicts:  # repeated steps over the same buffers: a prepared launch
+                    recs, count = self._plan_for(candidates, index_base, out, None, None)()
+                    return out, recs, count
                 return self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
                                                     verdicts=verdicts)
             return self.ev.evaluate_topk(candidates, k=self.k, index_base=index_base, out=out, verdicts=verdicts)
@@ -127,9 +130,12 @@ class ShardedSweep:
         self._last = slot
         if candidates.dim() == 1 and self.overlap:
             self._seq += 1
-            out, _, _ = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
-                                                     verdicts=verdicts, into=into, signal=self._signal,
-                                                     seq=self._seq)
+            if out is not None and verdicts:
+                self._plan_for(candidates, index_base, out, into, self._signal)(self._seq)
+            else:
+                out, _, _ = self.ev.evaluate_packed_topk(candidates, k=self.k, index_base=index_base, out=out,
+                                                         verdicts=verdicts, into=into, signal=self._signal,
+                                                         seq=self._seq)
             self._in_grp += 1
             if self._in_grp == self.group_steps:
                 self._flush()
@@ -142,6 +148,21 @@ class ShardedSweep:
                                                      verdicts=verdicts, into=into)
         recs, count = self.merge(recs, count)
         return out, recs, count
+
+    def _plan_for(self, words, index_base, out, into, signal):
+        """The prepared fused launch for these buffers (one per send slot), rebuilt when they change."""
+        plans = self.__dict__.setdefault("_plans", {})
+        slot_key = None if into is None else into.data_ptr()
+        p = plans.get(slot_key)
+        st = torch.cuda.current_stream(self.ev.device).cuda_stream
+        recs_ptr = into.data_ptr() if into is not None else (p.recs.data_ptr() if p is not None else None)
+        key = (words.data_ptr(), words.shape[0], self.k, index_base, recs_ptr,
+               (out.reason.data_ptr(), out.throughput.data_ptr() if out.throughput is not None else 0), st,
+               None if signal is None else signal.data_ptr())
+        if p is None or p.key != key:
+            p = self.ev.fused_plan(words, k=self.k, out=out, into=into, index_base=index_base, signal=signal)
+            plans[slot_key] = p
+        return p
 
     def _flush(self):
         """Exchange the steps launched into the current group (side stream)."""

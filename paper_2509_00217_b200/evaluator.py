@@ -412,6 +412,15 @@ class Evaluator:
                                                     int(index_base), _ptr(recs), _ptr(count), _ptr(scratch), sp))
         return (out if verdicts else None), recs, count
 
+    def fused_plan(self, words: torch.Tensor, k: int = 3, out: BatchResult | None = None,
+                   into: torch.Tensor | None = None, index_base: int = 0,
+                   signal: torch.Tensor | None = None) -> "FusedPlan":
+        """A prepared ``evaluate_packed_topk`` over fixed buffers on the current stream:
+        each call of the plan enqueues the fused launch with arguments marshalled
+        once (the per-call host cost of the small-batch regime). With ``signal``,
+        ``plan(seq)`` is ``evaluate_packed_topk(..., signal=signal, seq=seq)``."""
+        return FusedPlan(self, words, k, out, into, index_base, signal)
+
     def evaluate_host_packed(self, words: np.ndarray, fields=("throughput",), out: dict | None = None) -> dict:
         """Score host-resident packed words (pinned for full PCIe speed); numpy results."""
         arr = np.ascontiguousarray(words)
@@ -523,3 +532,39 @@ def pinned_results(n: int, fields=("throughput",)) -> dict:
     for f in fields:
         out[f] = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
     return out
+
+
+class FusedPlan:
+    """``Evaluator.fused_plan``: one fused evaluate + elite launch over fixed device
+    buffers (candidate words, verdicts, elite records) on the stream current at
+    creation. Calling it enqueues the launch and returns (records, count)."""
+
+    def __init__(self, ev: Evaluator, words: torch.Tensor, k: int, out: BatchResult | None, into, index_base: int,
+                 signal: torch.Tensor | None = None):
+        n = ev._check_words(words)
+        self.ev, self.words, self.out = ev, words, out
+        self.recs, self.count = ev._elite_out(k, into)
+        st = torch.cuda.current_stream(ev.device)
+        self.scratch = ev._fused_scratch(n, k, st)
+        self._soa = ResultSoA(_ptr(out.reason), *(_ptr(getattr(out, f)) for f in FIELDS)) if out is not None else None
+        self.key = (words.data_ptr(), n, k, index_base, self.recs.data_ptr(),
+                    None if out is None else (out.reason.data_ptr(), out.throughput.data_ptr() if out.throughput
+                                              is not None else 0), st.cuda_stream,
+                    None if signal is None else signal.data_ptr())
+        self.signal = signal
+        head = (ev._ctx, ctypes.c_void_p(words.data_ptr()), ctypes.c_int64(n),
+                ctypes.byref(self._soa) if self._soa is not None else None, ctypes.c_int(k),
+                ctypes.c_int64(index_base), _ptr(self.recs), _ptr(self.count), _ptr(self.scratch))
+        self._stream = ctypes.c_void_p(st.cuda_stream)
+        if signal is None:
+            self._fn = ev._lib.ls_evaluate_packed_topk
+            self._args = head + (self._stream,)
+        else:
+            self._fn = ev._lib.ls_evaluate_packed_topk_signal
+            self._head = head + (_ptr(signal),)
+
+    def __call__(self, seq: int | None = None):
+        rc = self._fn(*self._args) if self.signal is None else self._fn(*self._head, seq, self._stream)
+        if rc:
+            check(rc)
+        return self.recs, self.count
