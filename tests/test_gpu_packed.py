@@ -122,3 +122,36 @@ def test_pack_vectorised_path_and_tail(n, ev_factory):
     planes = torch.from_numpy(big).cuda()[:, :n]
     dev = ev.pack(planes).cpu().numpy().view(np.uint64)
     np.testing.assert_array_equal(dev, pack_vectors(vecs, wl.space))
+
+
+@pytest.mark.parametrize("fields", ["all", ("throughput",)])
+def test_fused_back_to_back_verdicts_and_elites(fields):
+    """Consecutive fused launches on one stream (programmatic dependent launch,
+    dynamic tile claims, the ragged tail tile claimed by any CTA) over planes and
+    packed words, with one or all six verdict fields: every verdict bit equals
+    the oracle's and every elite equals the standalone top-k of the batch."""
+    from oracle.cost_model import simulate_planes
+    from paper_2509_00217_b200.evaluator import Evaluator
+
+    wl, _, _ = load_eval("moe_1p6t_2048")
+    ev = Evaluator(wl, device=0)
+    rng = np.random.default_rng(41)
+    for n in (2047, 2049, 5 * 2048 + 77, 1 << 20, (1 << 22) + 4093):
+        planes_np = np.stack([rng.integers(0, k, size=n, dtype=np.uint8) for k in ev.head_sizes])
+        want = simulate_planes(wl.desc(), planes_np)
+        planes = torch.from_numpy(planes_np).cuda()
+        words = ev.pack(planes)
+        runs = []
+        for _ in range(3):  # back to back, no sync in between
+            runs.append(ev.evaluate_topk(planes, k=8, index_base=11, fields=fields))
+            runs.append(ev.evaluate_packed_topk(words, k=8, index_base=11, fields=fields))
+        torch.cuda.synchronize()
+        _, r0, c0 = ev.evaluate_topk(planes, k=8, index_base=11, verdicts=False)
+        ref_elite = ev.decode_records(r0, c0)
+        for out, recs, count in runs:
+            got = out.numpy()
+            assert np.array_equal(got["reason"], want["reason"]), n
+            for f in got:
+                if f != "reason":
+                    assert np.array_equal(np.asarray(got[f]).view(np.uint64), want[f].view(np.uint64)), (n, f)
+            assert ev.decode_records(recs, count) == ref_elite, n
