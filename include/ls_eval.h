@@ -273,7 +273,8 @@ uint64_t ls_stream_size(ls_ctx* ctx, int mode);
 int ls_generate(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, uint8_t* planes,
                 int64_t plane_stride, void* stream);
 /* Evaluate stream positions [start, start + n) and reduce them to the top-k
- * by raw throughput over distinct vectors (index = stream position). k <= 32;
+ * by raw throughput over distinct vectors (index = stream position). k <= 32,
+ * n <= 2^40 per call (split larger enumerations, e.g. baselines._sweep);
  * scratch as for ls_evaluate_topk_scratch_bytes(ctx, n, k). */
 int ls_sweep(ls_ctx* ctx, int mode, uint64_t seed, int64_t start, int64_t n, int k, ls_elite_rec* topk_out,
              int32_t* count_out, void* scratch, void* stream);

@@ -1298,6 +1298,8 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   g_err.clear();
   if (!c || n < 0 || k < 1 || k > fused_k_max() || !topk_out || !count_out || !scratch)
     return fail(LS_ERR_INVALID_ARGUMENT, "bad sweep arguments (k must be in [1, 32])");
+  if (n > (int64_t(1) << 40))  // the launch's 32-bit chunk / tile claim counters
+    return fail(LS_ERR_INVALID_ARGUMENT, "a sweep launch covers at most 2^40 stream positions: split it");
   if (c->blocks_tma == 0) return fail(LS_ERR_UNSUPPORTED, "sweeps need vectors of up to 16 heads");
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
