@@ -15,9 +15,10 @@ from pathlib import Path
 from .workload import WorkloadDesc
 
 __all__ = ["NativeUnavailable", "NativeError", "lib", "lib_path", "ResultSoA", "EliteRec", "check",
-           "LS_OK", "REASON_DECODE_ERROR", "KEY_RAW", "KEY_REWARD"]
+           "LS_OK", "LS_ERR_UNSUPPORTED", "REASON_DECODE_ERROR", "KEY_RAW", "KEY_REWARD"]
 
 LS_OK = 0
+LS_ERR_UNSUPPORTED = 4
 REASON_DECODE_ERROR = 255
 KEY_RAW = 0
 KEY_REWARD = 1

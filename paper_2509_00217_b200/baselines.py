@@ -194,6 +194,8 @@ class SweepReport:
 def _sweep(ev: Evaluator, mode: int, n: int, start: int, seed: int, k: int, chunk: int) -> SweepReport:
     import torch
 
+    if n <= 0:  # nothing to evaluate: an empty elite
+        return SweepReport(mode, 0, (), 0.0)
     recs, counts = [], []
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(torch.cuda.current_stream(ev.device))

@@ -485,8 +485,15 @@ class Evaluator:
     # -- on-device candidate streams ----------------------------------------
 
     def stream_size(self, mode: int) -> int:
-        """Length of an enumeration stream (GEN_ENUM / GEN_ENUM_ADMISSIBLE)."""
-        return int(self._lib.ls_stream_size(self._ctx, int(mode)))
+        """Length of an enumeration stream (GEN_ENUM / GEN_ENUM_ADMISSIBLE). Raises
+        NativeError when the library cannot enumerate it (a space beyond exact 64-bit
+        indexing, vectors of more than 16 heads) — 0 is never a valid size."""
+        size = int(self._lib.ls_stream_size(self._ctx, int(mode)))
+        if size == 0:
+            msg = self._lib.ls_last_error().decode("utf-8", "replace")
+            raise _native.NativeError(_native.LS_ERR_UNSUPPORTED,
+                                      msg or "stream size unavailable (uniform streams are unbounded)")
+        return size
 
     def generate(self, mode: int, n: int, start: int = 0, seed: int = 0) -> torch.Tensor:
         """Stream positions [start, start + n) as [A, N] uint8 planes on the device."""

@@ -105,3 +105,19 @@ def test_llama8b_exhaustive_equals_oracle(make_ev):
     best = int(np.argmax(thr))
     assert got[0].index == best and got[0].raw == res["throughput"][best]
     assert got[0].vector == tuple(int(x) for x in planes[:, best])
+
+
+def test_stream_size_errors_and_empty_sweep():
+    """a stream the library cannot enumerate raises instead of reporting
+    0, and an empty sweep returns an empty elite."""
+    from paper_2509_00217_b200._native import NativeError
+    from paper_2509_00217_b200.baselines import random_sweep
+    from paper_2509_00217_b200.evaluator import Evaluator
+    from paper_2509_00217_b200.generator import GEN_UNIFORM
+
+    wl, _, _ = load_eval("tiny")
+    ev = Evaluator(wl, device=0)
+    with pytest.raises(NativeError):
+        ev.stream_size(GEN_UNIFORM)  # unbounded: no size
+    rep = random_sweep(ev, 0)
+    assert rep.evaluated == 0 and rep.elites == () and rep.best is None
