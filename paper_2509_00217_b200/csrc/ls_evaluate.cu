@@ -56,17 +56,21 @@ __device__ __forceinline__ void diag_stamp(int slot) {
 #ifndef LS_GATE_WARPS
 #define LS_GATE_WARPS 16
 #endif
+// 16 + 3 + the producer = 20 warps, 5 per SM sub-partition: the 64K-register
+// file then allows 96 registers per thread (21 warps capped it at 80, and the
+// hot loops rematerialised values to fit); 3 fp64 warps keep up with the
+// survivors of a uniform batch.
 #ifndef LS_FP_WARPS
-#define LS_FP_WARPS 4
+#define LS_FP_WARPS 3
 #endif
 #ifndef LS_RING_KB
-#define LS_RING_KB 80
+#define LS_RING_KB 96
 #endif
 #ifndef LS_MIN_BLOCKS
 #define LS_MIN_BLOCKS 1
 #endif
 #ifndef LS_CLAIM_GROUP
-#define LS_CLAIM_GROUP 4  // tiles per dynamic claim of the fused kernels
+#define LS_CLAIM_GROUP 2  // tiles per dynamic claim of the fused kernels
 #endif
 #ifndef LS_BACKOFF_MAX
 #define LS_BACKOFF_MAX 512
