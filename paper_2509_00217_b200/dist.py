@@ -10,8 +10,8 @@ communication. Only two small exchanges cross ranks:
   on device with ``ls_topk_merge``; contiguous ranges keep "earliest global
   index wins" consistent, and the merge rule is exact for any arrival order.
   With ``overlap=True`` the all-gather and the merge run on a side stream
-  while the next batch is evaluated (the evaluate kernels leave one SM free
-  for them, ``ls_reserve_sms``), so the exchange is off the critical path;
+  while the next batch is evaluated, so the exchange is off the critical
+  path;
 * reward shaping across ranks (``SearchEnv.step`` semantics, env.py:159-164):
   each rank needs the best valid raw of all EARLIER ranks as its starting
   baseline — one all-gather of one float per rank.
@@ -65,14 +65,18 @@ class ShardedSweep:
 
     launches_per_merge = 2  # without grouping: the NCCL all-gather kernel + ls_topk_merge (per step)
 
-    def __init__(self, evaluator, k: int = 8, group=None, overlap: bool = False, group_steps: int = 4):
+    def __init__(self, evaluator, k: int = 8, group=None, overlap: bool = False, group_steps: int = 4,
+                 reserve_sms: int = 0):
         """``overlap``: run the exchanges on a side stream so the caller's stream goes
         straight on to the next batch; ``wait()`` joins it. With packed words the
         exchange is batched: every ``group_steps`` steps the side stream waits ONCE
         for the last launch's completion signal (ls_stream_wait_signal), all-gathers
         the group's per-rank lists in one collective and merges each step's — a wait
         on the side stream costs ~15 us of the next fused launch's overlap, so it is
-        paid once per group. The global elite of a step is ready at ``wait()``."""
+        paid once per group. The global elite of a step is ready at ``wait()``.
+        ``reserve_sms``: SMs the fused launches leave free for the side stream's
+        kernels (ls_reserve_sms); 0 measured fastest (NCCL's kernel starts as the
+        fused CTAs exit at a step boundary; one reserved SM cost 0.3 %)."""
         self.ev = evaluator
         self.k = int(k)
         self.group = group
@@ -99,8 +103,8 @@ class ShardedSweep:
         self._seq = 0
         self._signal = torch.zeros(1, dtype=torch.int32, device=dev)  # last fused launch whose elite is written
         self._side = torch.cuda.Stream(dev) if self.overlap else None
-        if self.overlap:
-            evaluator.reserve_sms(1)
+        if self.overlap and reserve_sms:
+            evaluator.reserve_sms(int(reserve_sms))
 
     @property
     def _send(self) -> torch.Tensor:
