@@ -949,9 +949,16 @@ int ls_topk(ls_ctx* c, const uint8_t* planes, int64_t plane_stride, const uint8_
 // is one launch (no per-call memset).
 // The half size does not depend on k: the second half's sync words sit at the
 // same offset for every call on a buffer, whatever k earlier calls used.
+// Sync words at the head of each fused scratch half: the floor and the done
+// counter share a line; the tile-claim counter has its own 128-byte line (the
+// floor's atomics, frequent while the elite lists fill, would queue the
+// claims behind them); the CTA lists start after them.
+constexpr size_t kSyncBytes = 256;
+constexpr size_t kClaimOffset = 128;
+
 static size_t fused_half_bytes(const ls_ctx* c, int /*k*/) {
   const size_t lists = std::max<size_t>((size_t)c->blocks_tma, (size_t)c->num_sms * sweep_ctas_per_sm());
-  return (32 + lists * (size_t)fused_k_max() * sizeof(ls_elite_rec) + lists * 4 + 255) & ~size_t(255);
+  return (kSyncBytes + lists * (size_t)fused_k_max() * sizeof(ls_elite_rec) + lists * 4 + 255) & ~size_t(255);
 }
 
 static uint8_t* fused_half(ls_ctx* c, void* scratch, int k) {
@@ -969,8 +976,8 @@ static TopkArgs fused_topk_args(void* half, int64_t grid, int k, int64_t index_b
   tk.index_base = index_base;
   tk.floor = static_cast<unsigned long long*>(half);
   tk.done = reinterpret_cast<unsigned int*>(tk.floor + 1);
-  tk.tile_ctr = tk.done + 1;
-  tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(half) + 32);
+  tk.tile_ctr = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(half) + kClaimOffset);
+  tk.part = reinterpret_cast<ls_elite_rec*>(static_cast<uint8_t*>(half) + kSyncBytes);
   tk.part_counts = reinterpret_cast<int32_t*>(tk.part + grid * k);
   tk.out = out;
   tk.count_out = count_out;
@@ -1096,8 +1103,9 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
   if (k > 64) return fail(LS_ERR_INVALID_ARGUMENT, "k must be <= 64");
   e = launch_topk(c->TM, planes, plane_stride, a.reason, a.thr, a.thr, n, k, index_base, topk_out, count_out, scratch,
                   c->num_sms, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 32, s);  // the fused path's sync words, zero again
-  if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(scratch) + fused_half_bytes(c, k), 0, 32, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, kSyncBytes, s);  // the fused path's sync words, zero again
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(static_cast<uint8_t*>(scratch) + fused_half_bytes(c, k), 0, kSyncBytes, s);
   return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk launch");
 }
 

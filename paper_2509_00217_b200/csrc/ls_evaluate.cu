@@ -69,6 +69,9 @@ __device__ __forceinline__ void diag_stamp(int slot) {
 #ifndef LS_MIN_BLOCKS
 #define LS_MIN_BLOCKS 1
 #endif
+#ifndef LS_LATE_CTAS
+#define LS_LATE_CTAS 1  // CTAs (highest indices) without a static first tile group
+#endif
 #ifndef LS_CLAIM_GROUP
 #define LS_CLAIM_GROUP 2  // tiles per dynamic claim of the fused kernels
 #endif
@@ -713,13 +716,19 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
       // counter (tk.tile_ctr: a CTA that starts late — e.g. behind the
       // previous launch's final merge under PDL — simply claims fewer) or,
       // without one, every gridDim.x-th tile. Stage tile -1 ends the stream.
-      // Claims are groups of G consecutive tiles (G = 4 with the counter, so
-      // one atomic round trip covers several microseconds of streaming), and
-      // the next group's claim is issued when the current group starts.
+      // Claims are groups of G consecutive tiles (G = 2 with the counter, so
+      // one atomic round trip hides behind ~1.7 µs of streaming), and the next
+      // group's claim is issued when the current group starts.
       const int64_t last = a.n > ntiles * kTile ? ntiles : ntiles - 1;
+      // The last LS_LATE_CTAS CTAs claim even their first group: under PDL the
+      // highest block indices are dispatched last, onto the SMs the previous
+      // launch frees last (its final merge), and a static group there would
+      // finish last in a short launch.
       const int G = tk.tile_ctr ? LS_CLAIM_GROUP : 1;
-      int64_t grp = blockIdx.x;
-      int64_t nxt = tk.tile_ctr ? (int64_t)gridDim.x + atomicAdd(tk.tile_ctr, 1u) : grp + gridDim.x;
+      const int64_t nstat = !tk.tile_ctr ? (int64_t)gridDim.x
+                                         : gridDim.x > LS_LATE_CTAS ? (int64_t)gridDim.x - LS_LATE_CTAS : 0;
+      int64_t grp = blockIdx.x < nstat ? (int64_t)blockIdx.x : nstat + atomicAdd(tk.tile_ctr, 1u);
+      int64_t nxt = tk.tile_ctr ? nstat + atomicAdd(tk.tile_ctr, 1u) : grp + gridDim.x;
       int j = 0;
       for (int i = 0; MODE == GEN_PLANES || MODE == GEN_WORDS; ++i) {
         const int s = i % NST, k = i / NST;
@@ -742,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
         if (++j == G || tile == last) {  // next group (its claim was issued a group ago)
           j = 0;
           grp = nxt;
-          nxt = tk.tile_ctr ? (int64_t)gridDim.x + atomicAdd(tk.tile_ctr, 1u) : grp + gridDim.x;
+          nxt = tk.tile_ctr ? nstat + atomicAdd(tk.tile_ctr, 1u) : grp + gridDim.x;
         }
       }
     }
