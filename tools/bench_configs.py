@@ -178,8 +178,9 @@ def main():
                   "budget": 4000, "wall_s": wall, "best_raw": rep.best_raw, "best_vector": list(rep.best_vector),
                   "reference_wall_s": None if ref is None else ref["wall_s"],
                   "reference_best_raw": None if ref is None else ref["best_raw"],
-                  "same_best_as_reference": None if ref is None else (
-                      rep.best_raw == ref["best_raw"] and list(rep.best_vector) == ref["best_vector"])})
+                  "same_best_raw_as_reference": None if ref is None else rep.best_raw == ref["best_raw"],
+                  "same_best_vector_as_reference": None if ref is None else (
+                      list(rep.best_vector) == ref["best_vector"])})
     fh.close()
 
 
