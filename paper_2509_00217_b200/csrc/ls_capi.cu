@@ -1321,13 +1321,13 @@ int ls_sweep(ls_ctx* c, int mode, uint64_t seed, int64_t start, int64_t n, int k
   LaunchPlan lp{true, c->smem_gate, tma_grid_cap(c)};
   const GenMeta& gen = c->gen[mode];
   const bool f32 = c->precision.load() == LS_PREC_FP32;
-  lp.sweep_fits = sweep_smem_bytes(c->L, gen.axis_size / gen.lo_size, gen.lo_size, f32) <= c->sweep_smem;
+  lp.sweep_fits = sweep_smem_bytes(c->L, gen.axis_size / gen.lo_size, gen.lo_size, mode, f32) <= c->sweep_smem;
   if (f32) {
     if (!lp.sweep_fits) return fail(LS_ERR_UNSUPPORTED, "fp32 sweep: tables do not fit in shared memory");
     lp.tabf = c->d_tabf;
   }
   if (lp.sweep_fits) lp.max_blocks = tma_grid_cap(c) / c->tma_per_sm * sweep_ctas_per_sm();
-  const int64_t grid = lp.sweep_fits ? sweep_grid(lp, n) : ws_grid(lp, n, mode);
+  const int64_t grid = lp.sweep_fits ? sweep_grid(lp, n, mode) : ws_grid(lp, n, mode);
   TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, start, topk_out, count_out);
   cudaError_t e;
   if ((e = launch_sweep(lp, c->desc.sum_mode == LS_SUM_NEUMAIER, mode, c->d_tab, c->L, c->M, n, tk, gm, s)) !=

@@ -1086,19 +1086,33 @@ __global__ void __launch_bounds__(kThreads, LS_MIN_BLOCKS)
 // shared-memory queue and scores 32 queued survivors at once in place
 // (full_path from the shared-memory table), offering the valid ones to its
 // register elite list. No ring, no mailboxes, no idle roles; one CTA of
-// kSwWarps warps per SM.
+// sw_warps<MODE>() warps per SM.
 #ifndef LS_SWEEP_WARPS
-#define LS_SWEEP_WARPS 24
+#define LS_SWEEP_WARPS 24  // admissible enumeration: survivor-heavy, registers matter
+#endif
+#ifndef LS_SWEEP_WARPS_SPARSE
+#define LS_SWEEP_WARPS_SPARSE 32  // uniform / full enumeration: most candidates fail the gates
 #endif
 #ifndef LS_SWEEP_CTAS
 #define LS_SWEEP_CTAS 1  // CTAs per SM (each stages its own tables)
 #endif
-constexpr int kSwWarps = LS_SWEEP_WARPS;
-constexpr int kSwThreads = 32 * kSwWarps;
+// Warps per sweep CTA by stream: 24 (80 registers) for the admissible
+// enumeration, where ~60 % of positions take the fp64 walk; 32 (64 registers)
+// for the uniform stream and the full enumeration, where most positions fail
+// the gates and more warps hide more latency (1.2T: admissible 0.482 vs 0.503
+// ms, full 5.95 vs 6.27 ms, uniform 2^30 8.17 vs 8.25 ms).
+template <int MODE>
+__host__ __device__ constexpr int sw_warps() {
+  return MODE == GEN_ENUM_ADMISSIBLE ? LS_SWEEP_WARPS : LS_SWEEP_WARPS_SPARSE;
+}
+constexpr int kSwWarpsMax = LS_SWEEP_WARPS > LS_SWEEP_WARPS_SPARSE ? LS_SWEEP_WARPS : LS_SWEEP_WARPS_SPARSE;
+inline int sw_warps_of(int mode) {
+  return mode == GEN_ENUM_ADMISSIBLE ? sw_warps<GEN_ENUM_ADMISSIBLE>() : sw_warps<GEN_ENUM>();
+}
 constexpr int kSwChunk = 256;  // consecutive stream positions per warp chunk
 constexpr int kSwQueue = 64;   // survivor queue per warp (< 32 left over + 32 new)
 constexpr uint32_t kSwMergeBytes = 64 * 1024;  // shared memory the end-of-kernel merges use (aliases the tables)
-static_assert(kSwWarps * 32 * sizeof(Rec) + 512 * sizeof(int) + 64 * sizeof(Rec) <= kSwMergeBytes, "merge region");
+static_assert(kSwWarpsMax * 32 * sizeof(Rec) + 512 * sizeof(int) + 64 * sizeof(Rec) <= kSwMergeBytes, "merge region");
 
 // Shared-memory layout of sweep_kernel: workload table, the stream's two
 // axis tables, per-warp survivor queues.
@@ -1107,7 +1121,7 @@ struct SwLayout {
 };
 // f32: the fp32 fast mode also stages the fp32 copy of the tables
 __host__ __device__ inline uint32_t tabf_bytes(const TabLayout& L) { return ((uint32_t)L.words * 4u + 15u) & ~15u; }
-__host__ __device__ inline SwLayout sw_layout(const TabLayout& L, uint32_t hi_size, uint32_t lo_size,
+__host__ __device__ inline SwLayout sw_layout(const TabLayout& L, uint32_t hi_size, uint32_t lo_size, int nw,
                                               bool f32 = false) {
   SwLayout o;
   o.tab = 0;
@@ -1115,8 +1129,8 @@ __host__ __device__ inline SwLayout sw_layout(const TabLayout& L, uint32_t hi_si
   o.gen_hi = o.tabf + (f32 ? tabf_bytes(L) : 0u);
   o.gen_lo = o.gen_hi + 4u * hi_size;
   o.qkey = (o.gen_lo + 4u * lo_size + 15u) & ~15u;
-  o.qy = o.qkey + 8u * kSwWarps * kSwQueue;
-  o.bytes = o.qy + 4u * kSwWarps * kSwQueue;
+  o.qy = o.qkey + 8u * (uint32_t)nw * kSwQueue;
+  o.bytes = o.qy + 4u * (uint32_t)nw * kSwQueue;
   if (o.bytes < kSwMergeBytes) o.bytes = kSwMergeBytes;
   return o;
 }
@@ -1157,9 +1171,11 @@ __device__ __forceinline__ void gen_candidate_s(const GenMeta& g, const uint32_t
 }
 
 template <bool NEU, int MODE, bool F32>
-__global__ void __launch_bounds__(kSwThreads, LS_SWEEP_CTAS)
+__global__ void __launch_bounds__(32 * sw_warps<MODE>(), LS_SWEEP_CTAS)
     sweep_kernel(const uint64_t* __restrict__ gtab, const TabLayout L, const EvalMeta M, const int64_t n,
                  const TopkArgs tk, const GenMeta gm, const SwLayout SL, const float* __restrict__ gtabf) {
+  constexpr int kSwWarps = sw_warps<MODE>();
+  constexpr int kSwThreads = 32 * kSwWarps;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t tab_bar;
   __shared__ int list_count[kSwWarps];
@@ -1280,12 +1296,13 @@ template <bool NEU, int MODE>
 void launch_sweep_t(const LaunchPlan& lp, const uint64_t* tab, const TabLayout& L, const EvalMeta& M, int64_t n,
                     const TopkArgs& tk, const GenMeta& gm, cudaStream_t s) {
   const bool f32 = lp.tabf != nullptr;
-  const SwLayout SL = sw_layout(L, (uint32_t)(gm.axis_size / gm.lo_size), (uint32_t)gm.lo_size, f32);
-  const int64_t blocks = sweep_grid(lp, n);
+  constexpr int NT = 32 * sw_warps<MODE>();
+  const SwLayout SL = sw_layout(L, (uint32_t)(gm.axis_size / gm.lo_size), (uint32_t)gm.lo_size, sw_warps<MODE>(), f32);
+  const int64_t blocks = sweep_grid(lp, n, MODE);
   if (f32)  // plain fp32 sums: the NEU flag does not apply
-    sweep_kernel<false, MODE, true><<<(unsigned)blocks, kSwThreads, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL, lp.tabf);
+    sweep_kernel<false, MODE, true><<<(unsigned)blocks, NT, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL, lp.tabf);
   else
-    sweep_kernel<NEU, MODE, false><<<(unsigned)blocks, kSwThreads, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL, nullptr);
+    sweep_kernel<NEU, MODE, false><<<(unsigned)blocks, NT, SL.bytes, s>>>(tab, L, M, n, tk, gm, SL, nullptr);
 }
 
 // One candidate per thread, any alignment, any A <= LS_MAX_HEADS.
@@ -1518,24 +1535,31 @@ int generic_blocks_per_sm() {
 
 int sweep_ctas_per_sm() { return LS_SWEEP_CTAS; }
 
-int64_t sweep_grid(const LaunchPlan& lp, int64_t n) {
+int64_t sweep_grid(const LaunchPlan& lp, int64_t n, int mode) {
   const int64_t chunks = (n + kSwChunk - 1) / kSwChunk;
-  int64_t blocks = (chunks + kSwWarps - 1) / kSwWarps;
+  const int nw = sw_warps_of(mode);
+  int64_t blocks = (chunks + nw - 1) / nw;
   if (blocks < 1) blocks = 1;
   // one CTA per SM: the cap counts the eval_ws_kernel's CTAs per SM, the same or more
   return blocks > lp.max_blocks ? lp.max_blocks : blocks;
 }
 
-size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, bool f32) {
-  return sw_layout(L, (uint32_t)hi_size, (uint32_t)lo_size, f32).bytes;
+size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, int mode, bool f32) {
+  return sw_layout(L, (uint32_t)hi_size, (uint32_t)lo_size, sw_warps_of(mode), f32).bytes;
 }
 
 // Opt every sweep kernel into the largest dynamic shared memory the device
 // allows beside its static shared memory; returns that dynamic budget.
 size_t prepare_sweep_kernels(size_t optin) {
-  cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, sweep_kernel<true, GEN_ENUM_ADMISSIBLE, false>);
-  const size_t budget = optin > fa.sharedSizeBytes + 1024 ? optin - fa.sharedSizeBytes - 1024 : 0;
+  size_t st = 0;  // the largest static shared memory of the instances (their warp counts differ)
+  auto stat = [&st](auto kern) {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.sharedSizeBytes > st) st = fa.sharedSizeBytes;
+  };
+  stat(sweep_kernel<true, GEN_ENUM_ADMISSIBLE, false>);
+  stat(sweep_kernel<true, GEN_ENUM, false>);
+  stat(sweep_kernel<true, GEN_UNIFORM, false>);
+  const size_t budget = optin > st + 1024 ? optin - st - 1024 : 0;
   const int b = (int)budget;
   auto set = [b](auto kern) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, b); };
   set(sweep_kernel<true, GEN_UNIFORM, false>);

@@ -85,9 +85,9 @@ cudaError_t launch_generate(int mode, const GenMeta& gm, int64_t n, int A, uint8
 cudaError_t launch_pack(const PackMeta& pk, int A, const uint8_t* planes, int64_t stride, int64_t n, uint64_t* words,
                         cudaStream_t s);
 int64_t ws_grid(const LaunchPlan& lp, int64_t n, int mode);  // CTAs of one eval_ws_kernel launch
-int64_t sweep_grid(const LaunchPlan& lp, int64_t n);         // CTAs of one sweep_kernel launch (ls_sweep)
+int64_t sweep_grid(const LaunchPlan& lp, int64_t n, int mode);         // CTAs of one sweep_kernel launch (ls_sweep)
 int sweep_ctas_per_sm();
-size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, bool f32);
+size_t sweep_smem_bytes(const TabLayout& L, uint64_t hi_size, uint64_t lo_size, int mode, bool f32);
 cudaError_t build_tables_f32(const uint64_t* tab, int words, float* out, cudaStream_t s);
 size_t prepare_sweep_kernels(size_t optin);  // -> dynamic shared memory budget of sweep_kernel
 int fused_k_max();
