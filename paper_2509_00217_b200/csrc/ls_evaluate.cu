@@ -1241,7 +1241,16 @@ __global__ void __launch_bounds__(32 * sw_warps<MODE>(), LS_SWEEP_CTAS)
       const int64_t i = base + j * 32 + lane;
       const bool in = i < n;
       if (MODE == GEN_UNIFORM) {
-        gen_candidate_s<MODE>(gm, hi_s, lo_s, (uint64_t)(gm.start + (in ? i : n - 1)), c);
+        if (coarse) {  // the coarse rank indexes the gate words directly: (t, e, p, b) only for survivors
+          const uint64_t gi = (uint64_t)(gm.start + (in ? i : n - 1));
+          const uint64_t r1 = splitmix64(gm.seed ^ (2 * gi)), r2 = splitmix64(gm.seed ^ (2 * gi + 1));
+          crank = __umul64hi(r1, gm.coarse_size);
+          const uint64_t axis = __umul64hi(r2, gm.axis_size);
+          const uint64_t hi = divq(axis, gm.m_lo, gm.lo_size);
+          c.Y = hi_s[hi] | lo_s[axis - hi * gm.lo_size];
+        } else {
+          gen_candidate_s<MODE>(gm, hi_s, lo_s, (uint64_t)(gm.start + (in ? i : n - 1)), c);
+        }
       } else {
         if (j > 0 && in) {  // advance by 32 positions (past-the-end lanes keep their last candidate)
           alo += 32;
@@ -1257,7 +1266,7 @@ __global__ void __launch_bounds__(32 * sw_warps<MODE>(), LS_SWEEP_CTAS)
       }
       uint32_t reason;
       if (coarse) {
-        reason = MODE == GEN_UNIFORM ? gate_coarse(Cg, L, M, c) : gate_rank(Cg, M, (uint32_t)crank, c.Y);
+        reason = gate_rank(Cg, M, (uint32_t)crank, c.Y);
       } else {
         double m;
         reason = gate(T, L, M, c, m);
@@ -1266,6 +1275,7 @@ __global__ void __launch_bounds__(32 * sw_warps<MODE>(), LS_SWEEP_CTAS)
       const uint32_t b = __ballot_sync(0xffffffffu, sv);
       if (b) {
         if (sv) {
+          if (MODE == GEN_UNIFORM && coarse) rank_split_g(gm, crank, c);
           const int pos = qcount + __popc(b & lt);
           qkey[pos] = pack_key(i, c);
           qy[pos] = c.Y;
