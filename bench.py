@@ -434,7 +434,12 @@ def run_ours(args, rank, world, local_rank):
                       throughput=torch.empty(n, dtype=torch.float64, device=dev))
     # N > 1: each step's elite all-gather + merge runs on a side stream beside the
     # next step's evaluate (which leaves one SM free for it)
-    sweep = ShardedSweep(ev, k=ELITE_K, overlap=world > 1, group_steps=int(os.environ.get("LS_XCHG_GROUP", "4")))
+    # N > 1: the elite exchange — "nccl" (grouped all-gather on a side stream; measured faster at
+    # 20 steps) or "p2p" (the fused launch writes its block into every rank's ring over NVLink,
+    # one merge launch per lap of 16 steps)
+    xchg = os.environ.get("LS_XCHG", "nccl")
+    sweep = ShardedSweep(ev, k=ELITE_K, overlap=world > 1, group_steps=int(os.environ.get("LS_XCHG_GROUP", "4")),
+                         transport=xchg if world > 1 else "nccl")
     if args.diag_reserve is not None:
         ev.reserve_sms(args.diag_reserve)
     if args.diag_no_exchange:  # diagnostics: each rank's fused launches alone (no elite exchange)
@@ -448,7 +453,11 @@ def run_ours(args, rank, world, local_rank):
         _, recs, count = sweep.run(cands, index_base=base, out=out)
         # our kernels per step: the fused evaluate (its last CTA merges the CTA lists);
         # N > 1: + per group of steps one NCCL all-gather and one merge launch (side stream)
-        return recs, count, 1 + ((2 / sweep.group_steps) if world > 1 else 0)
+        if world == 1:
+            return recs, count, 1
+        if sweep.transport == "p2p":  # + one merge launch per lap (and one in wait())
+            return recs, count, 1 + 1 / sweep._lap
+        return recs, count, 1 + 2 / sweep.group_steps
 
     for _ in range(args.warmup):
         step()
@@ -470,6 +479,8 @@ def run_ours(args, rank, world, local_rank):
     t_end.record(stream)
     clocks.poll_until(t_end)
     torch.cuda.synchronize(dev)
+    sweep.check()  # a p2p merge that timed out waiting for a peer fails the run
+    sweep.close()  # p2p: unmap the peers' rings (collective)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()

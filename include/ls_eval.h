@@ -447,6 +447,30 @@ int ls_evaluate_packed_topk_signal(ls_ctx* ctx, const uint64_t* words, int64_t n
                                    uint32_t* signal, uint32_t seq, void* stream);
 int ls_stream_wait_signal(void* stream, const uint32_t* signal, uint32_t seq);
 
+/* Multi-GPU elite exchange over peer memory (replaces the NCCL all-gather of
+ * the per-rank top-k blocks, reference: the driver loop that compares every
+ * worker's best). Each rank owns a ring of exchange blocks
+ * [world][slots][k + 1][32 B] in its own HBM and maps its peers' rings with
+ * CUDA IPC; for step t the fused launch's last CTA writes its elite block
+ * (k records, then a count | seq << 32 word at row k, release-stored after a
+ * system-scope fence) into slot t of every rank's ring — sinks is a DEVICE
+ * array of nsinks destination pointers, seq != 0 the step's sequence number.
+ * ls_topk_merge_steps_wait merges `steps` consecutive slots of the local ring
+ * (rank r's block of step j at blocks + (r * rank_stride + j) * (k + 1)
+ * records) after waiting, on the device, until each block carries seq0 + j;
+ * a block that does not arrive within ~10 s sets *err (device int) to 1. */
+#define LS_IPC_HANDLE_BYTES 64
+int ls_evaluate_packed_topk_sinks(ls_ctx* ctx, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
+                                  int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                                  void* const* sinks, int nsinks, uint32_t seq, void* stream);
+int ls_topk_merge_steps_wait(const void* blocks, int world, int steps, int rank_stride, int k, uint32_t seq0,
+                             ls_elite_rec* out, int32_t* counts_out, int32_t* err, void* stream);
+int ls_ipc_alloc(size_t bytes, void** dptr_out); /* zeroed device memory of its own allocation (the ring) */
+int ls_ipc_free(void* dptr);
+int ls_ipc_handle(const void* dptr, void* handle_out); /* dptr: a base returned by ls_ipc_alloc */
+int ls_ipc_open(const void* handle, void** dptr_out);
+int ls_ipc_close(void* dptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -992,7 +992,8 @@ size_t ls_evaluate_topk_scratch_bytes(const ls_ctx* c, int64_t n, int k) {
 static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
                               int64_t plane_stride, const ls_result_soa* out, int k, int64_t index_base,
                               ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream,
-                              uint32_t* signal = nullptr, uint32_t seq = 0);
+                              uint32_t* signal = nullptr, uint32_t seq = 0, uint8_t* const* sinks = nullptr,
+                              int nsinks = 0);
 
 int ls_evaluate_topk(ls_ctx* c, const uint8_t* planes, int64_t n, int64_t plane_stride, const ls_result_soa* out,
                      int k, int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
@@ -1013,6 +1014,71 @@ int ls_evaluate_packed_topk_signal(ls_ctx* c, const uint64_t* words, int64_t n, 
     return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_packed_topk_signal arguments");
   return evaluate_topk_impl(c, nullptr, words, n, n, out, k, index_base, topk_out, count_out, scratch, stream, signal,
                             seq);
+}
+
+int ls_evaluate_packed_topk_sinks(ls_ctx* c, const uint64_t* words, int64_t n, const ls_result_soa* out, int k,
+                                  int64_t index_base, ls_elite_rec* topk_out, int32_t* count_out, void* scratch,
+                                  void* const* sinks, int nsinks, uint32_t seq, void* stream) {
+  g_err.clear();
+  if (!c || n < 1 || k < 1 || k > fused_k_max() || !topk_out || !count_out || !scratch || !words || !sinks ||
+      nsinks < 1 || nsinks > 32 || seq == 0)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad evaluate_packed_topk_sinks arguments");
+  return evaluate_topk_impl(c, nullptr, words, n, n, out, k, index_base, topk_out, count_out, scratch, stream,
+                            nullptr, seq, reinterpret_cast<uint8_t* const*>(sinks), nsinks);
+}
+
+int ls_topk_merge_steps_wait(const void* blocks, int world, int steps, int rank_stride, int k, uint32_t seq0,
+                             ls_elite_rec* out, int32_t* counts_out, int32_t* err, void* stream) {
+  g_err.clear();
+  if (!blocks || world < 1 || world > 1024 || steps < 1 || rank_stride < steps || k < 1 || k > 32 || !out ||
+      !counts_out || seq0 == 0)
+    return fail(LS_ERR_INVALID_ARGUMENT, "bad topk_merge_steps_wait arguments");
+  cudaError_t e = launch_topk_merge_steps(static_cast<const ls_elite_rec*>(blocks), world, steps, k, out, counts_out,
+                                          static_cast<cudaStream_t>(stream), rank_stride, seq0, err);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "topk_merge_steps_wait launch");
+}
+
+int ls_ipc_alloc(size_t bytes, void** dptr_out) {
+  g_err.clear();
+  if (!bytes || !dptr_out) return fail(LS_ERR_INVALID_ARGUMENT, "bad ipc_alloc arguments");
+  cudaError_t e = cudaMalloc(dptr_out, bytes);  // its own allocation: an IPC handle maps exactly this base
+  if (e == cudaSuccess) e = cudaMemset(*dptr_out, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "ipc_alloc");
+}
+
+int ls_ipc_free(void* dptr) {
+  g_err.clear();
+  if (!dptr) return fail(LS_ERR_INVALID_ARGUMENT, "null ipc_free argument");
+  cudaError_t e = cudaFree(dptr);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "ipc_free");
+}
+
+int ls_ipc_handle(const void* dptr, void* handle_out) {
+  g_err.clear();
+  if (!dptr || !handle_out) return fail(LS_ERR_INVALID_ARGUMENT, "null ipc_handle argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == LS_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  return LS_OK;
+}
+
+int ls_ipc_open(const void* handle, void** dptr_out) {
+  g_err.clear();
+  if (!handle || !dptr_out) return fail(LS_ERR_INVALID_ARGUMENT, "null ipc_open argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+int ls_ipc_close(void* dptr) {
+  g_err.clear();
+  if (!dptr) return fail(LS_ERR_INVALID_ARGUMENT, "null ipc_close argument");
+  cudaError_t e = cudaIpcCloseMemHandle(dptr);
+  return e == cudaSuccess ? LS_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
 // cuStreamWaitValue32 from the driver (resolved once through the runtime: no -lcuda)
@@ -1055,7 +1121,7 @@ int ls_evaluate_packed_topk(ls_ctx* c, const uint64_t* words, int64_t n, const l
 static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* words, int64_t n,
                               int64_t plane_stride, const ls_result_soa* out, int k, int64_t index_base,
                               ls_elite_rec* topk_out, int32_t* count_out, void* scratch, void* stream,
-                              uint32_t* signal, uint32_t seq) {
+                              uint32_t* signal, uint32_t seq, uint8_t* const* sinks, int nsinks) {
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   EvalArgs a{};
@@ -1081,7 +1147,10 @@ static int evaluate_topk_impl(ls_ctx* c, const uint8_t* planes, const uint64_t* 
     TopkArgs tk = fused_topk_args(fused_half(c, scratch, k), grid, k, index_base, topk_out, count_out);
     tk.signal = signal;
     tk.seq = seq;
+    tk.sinks = sinks;
+    tk.nsinks = nsinks;
     if (n == 0) {
+      if (nsinks > 0) return fail(LS_ERR_INVALID_ARGUMENT, "an empty batch has no elite to send to sinks");
       cudaMemsetAsync(count_out, 0, sizeof(int32_t), s);
       if (signal) cudaMemcpyAsync(signal, &seq, sizeof(seq), cudaMemcpyHostToDevice, s);
       return LS_OK;

@@ -595,6 +595,33 @@ __device__ __forceinline__ void final_merge(RegList& wl, uint8_t* smem, int* cnt
 }
 
 
+// The final elite block to every sink (the multi-GPU exchange over peer
+// memory: each rank's ring slot for this step, peers' rings mapped by CUDA
+// IPC): lane j copies record j, then — after a system-scope fence — lane r
+// publishes sink r's count | seq << 32 word with a release store, so a reader
+// that acquires the word sees the records. Called by warp 0 of the last CTA.
+__device__ __noinline__ void sink_copy(const TopkArgs tk) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  __threadfence();
+  const int cnt = __ldcg(tk.count_out);
+  for (int r = 0; r < tk.nsinks; ++r) {
+    uint8_t* dst = tk.sinks[r];
+    if (lane < cnt) {
+      const int4* src = reinterpret_cast<const int4*>(tk.out + lane);
+      int4* d = reinterpret_cast<int4*>(dst + 32 * lane);
+      d[0] = __ldcg(src);
+      d[1] = __ldcg(src + 1);
+    }
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane < tk.nsinks) {
+    const unsigned long long w = (unsigned long long)(uint32_t)cnt | ((unsigned long long)tk.seq << 32);
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(tk.sinks[lane] + 32 * tk.k), "l"(w) : "memory");
+  }
+}
+
 // End of a fused evaluate + elite kernel (all NW work warps call it): every
 // warp's list to shared memory, warp 0 merges them into this CTA's list and
 // publishes it; the last CTA to finish merges every CTA's list into tk.out
@@ -628,6 +655,7 @@ __device__ __forceinline__ void elite_epilogue(RegList& wl, uint8_t* region, int
     if (warp == 0 && (threadIdx.x & 31) == 0) LS_STAMP(6);
     __threadfence();
     final_merge<NW, REGION>(wl, region, list_count, warp, tk);
+    if (tk.nsinks > 0 && warp == 0) sink_copy(tk);
     if (warp == 0 && (threadIdx.x & 31) == 0) {
       LS_STAMP(7);
       // every other CTA is past its last floor read and done increment:

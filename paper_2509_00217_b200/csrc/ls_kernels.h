@@ -46,6 +46,8 @@ struct TopkArgs {
   unsigned int* tile_ctr;     // dynamic tile claims after each CTA's first (zero before launch), or null
   uint32_t* signal;           // optional: the last CTA stores seq here (release) once out / count_out are written
   uint32_t seq;
+  uint8_t* const* sinks;      // optional (device array): the last CTA copies the elite block (k records + a
+  int nsinks;                 // count | seq << 32 word at row k) to each sink, peers' memory included
   ls_elite_rec* out;          // final top-k and its count
   int32_t* count_out;
 };
@@ -124,7 +126,8 @@ cudaError_t launch_topk(const TopkMeta& tm, const uint8_t* planes, int64_t strid
                         const double* thr, const double* key, int64_t n, int k, int64_t index_base,
                         ls_elite_rec* out, int32_t* count_out, void* scratch, int num_sms, cudaStream_t s);
 cudaError_t launch_topk_merge_steps(const ls_elite_rec* blocks, int world, int steps, int k, ls_elite_rec* out,
-                                    int32_t* counts_out, cudaStream_t s);
+                                    int32_t* counts_out, cudaStream_t s, int rank_stride = 0, uint32_t seq0 = 0,
+                                    int32_t* err = nullptr);
 cudaError_t launch_topk_merge(const ls_elite_rec* recs, const int32_t* counts, int m, int k_in, int k,
                               const unsigned long long* floor,
                               ls_elite_rec* out, int32_t* count_out, cudaStream_t s);

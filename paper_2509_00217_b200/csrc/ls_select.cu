@@ -329,13 +329,32 @@ __global__ void __launch_bounds__(kMergeThreads) topk_merge_fast_kernel(const ls
                                                                         const unsigned long long* floor,
                                                                         ls_elite_rec* __restrict__ out,
                                                                         int32_t* __restrict__ count_out,
-                                                                        int64_t step_stride = 0) {
+                                                                        int64_t step_stride = 0, uint32_t seq0 = 0,
+                                                                        int32_t* err = nullptr) {
   __shared__ Rec slots[kMergeWarps][32];
   __shared__ int s_counts[ROWS ? 1024 : 1];
   if (ROWS) {
     recs += (int64_t)blockIdx.x * step_stride;
     out += (int64_t)blockIdx.x * k;
     count_out += blockIdx.x;
+    if (seq0) {  // peer-memory exchange: wait until every rank's block of this step carries its seq
+      const uint32_t want = seq0 + blockIdx.x;
+      for (int l = threadIdx.x; l < m; l += kMergeThreads) {
+        const unsigned long long* w = reinterpret_cast<const unsigned long long*>(recs + (int64_t)l * k_in + k);
+        const long long t0 = clock64();
+        for (;;) {
+          unsigned long long v;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+          if ((uint32_t)(v >> 32) == want) break;
+          if (clock64() - t0 > 20000000000ll) {  // ~10 s: a rank stopped producing
+            if (err) atomicExch(err, 1);
+            break;
+          }
+          __nanosleep(200);
+        }
+      }
+      __syncthreads();
+    }
     for (int l = threadIdx.x; l < m; l += kMergeThreads)
       s_counts[l] = *reinterpret_cast<const int32_t*>(recs + (int64_t)l * k_in + k);
     __syncthreads();
@@ -517,10 +536,12 @@ cudaError_t launch_valid_compact(const uint8_t* reason, const double* thr, int64
 }
 
 cudaError_t launch_topk_merge_steps(const ls_elite_rec* blocks, int world, int steps, int k, ls_elite_rec* out,
-                                    int32_t* counts_out, cudaStream_t s) {
-  // rank r's block of step j: blocks + (r * steps + j) * (k + 1) records
-  topk_merge_fast_kernel<true><<<steps, kMergeThreads, 0, s>>>(blocks, nullptr, world, steps * (k + 1), k, nullptr, out,
-                                                              counts_out, (int64_t)(k + 1));
+                                    int32_t* counts_out, cudaStream_t s, int rank_stride, uint32_t seq0,
+                                    int32_t* err) {
+  // rank r's block of step j: blocks + (r * rank_stride + j) * (k + 1) records (rank_stride 0: = steps)
+  const int rs = rank_stride > 0 ? rank_stride : steps;
+  topk_merge_fast_kernel<true><<<steps, kMergeThreads, 0, s>>>(blocks, nullptr, world, rs * (k + 1), k, nullptr, out,
+                                                              counts_out, (int64_t)(k + 1), seq0, err);
   return cudaGetLastError();
 }
 

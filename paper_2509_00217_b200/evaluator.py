@@ -414,12 +414,12 @@ class Evaluator:
 
     def fused_plan(self, words: torch.Tensor, k: int = 3, out: BatchResult | None = None,
                    into: torch.Tensor | None = None, index_base: int = 0,
-                   signal: torch.Tensor | None = None) -> "FusedPlan":
+                   signal: torch.Tensor | None = None, sinks: torch.Tensor | None = None) -> "FusedPlan":
         """A prepared ``evaluate_packed_topk`` over fixed buffers on the current stream:
         each call of the plan enqueues the fused launch with arguments marshalled
         once (the per-call host cost of the small-batch regime). With ``signal``,
         ``plan(seq)`` is ``evaluate_packed_topk(..., signal=signal, seq=seq)``."""
-        return FusedPlan(self, words, k, out, into, index_base, signal)
+        return FusedPlan(self, words, k, out, into, index_base, signal, sinks)
 
     def evaluate_host_packed(self, words: np.ndarray, fields=("throughput",), out: dict | None = None) -> dict:
         """Score host-resident packed words (pinned for full PCIe speed); numpy results."""
@@ -547,7 +547,7 @@ class FusedPlan:
     creation. Calling it enqueues the launch and returns (records, count)."""
 
     def __init__(self, ev: Evaluator, words: torch.Tensor, k: int, out: BatchResult | None, into, index_base: int,
-                 signal: torch.Tensor | None = None):
+                 signal: torch.Tensor | None = None, sinks: torch.Tensor | None = None):
         n = ev._check_words(words)
         self.ev, self.words, self.out = ev, words, out
         self.recs, self.count = ev._elite_out(k, into)
@@ -563,7 +563,11 @@ class FusedPlan:
                 ctypes.byref(self._soa) if self._soa is not None else None, ctypes.c_int(k),
                 ctypes.c_int64(index_base), _ptr(self.recs), _ptr(self.count), _ptr(self.scratch))
         self._stream = ctypes.c_void_p(st.cuda_stream)
-        if signal is None:
+        self.sinks = sinks
+        if sinks is not None:  # the elite block also goes to these device pointers (peer-memory exchange)
+            self._fn = ev._lib.ls_evaluate_packed_topk_sinks
+            self._head = head + (_ptr(sinks), int(sinks.numel()))
+        elif signal is None:
             self._fn = ev._lib.ls_evaluate_packed_topk
             self._args = head + (self._stream,)
         else:
@@ -571,7 +575,10 @@ class FusedPlan:
             self._head = head + (_ptr(signal),)
 
     def __call__(self, seq: int | None = None):
-        rc = self._fn(*self._args) if self.signal is None else self._fn(*self._head, seq, self._stream)
+        if self.signal is None and self.sinks is None:
+            rc = self._fn(*self._args)
+        else:
+            rc = self._fn(*self._head, seq, self._stream)
         if rc:
             check(rc)
         return self.recs, self.count
