@@ -18,6 +18,42 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _run_two(target, args, attempts=3):
+    """Run target(rank, 2, port, *args, q) on two spawned ranks and return rank 0's
+    result; a rank that dies early (e.g. the rendezvous port was taken between
+    _free_port and the bind) restarts the pair on a fresh port."""
+    import queue
+    import time
+
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    for attempt in range(attempts):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=target, args=(r, 2, port, *args[:-1], q, *args[-1])) for r in range(2)]
+        for p in procs:
+            p.start()
+        t0, res = time.time(), None
+        while res is None and time.time() - t0 < 300:
+            try:
+                res = q.get(timeout=1)
+            except queue.Empty:
+                if any(p.exitcode not in (None, 0) for p in procs):
+                    break
+        if res is None:
+            for p in procs:
+                p.terminate()
+                p.join(timeout=30)
+            if attempt + 1 < attempts:
+                continue
+            raise AssertionError("the two-rank run failed")
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+        return res
+
+
 def _worker(rank, world, port, n, k, q, packed=False, overlap=False):
     import torch.distributed as dist
 
@@ -61,19 +97,7 @@ def _worker(rank, world, port, n, k, q, packed=False, overlap=False):
 @pytest.mark.parametrize("packed", [False, True])
 @pytest.mark.parametrize("k", [3, 8])
 def test_two_gpu_elite_equals_single_gpu(k, packed, overlap):
-    import torch.multiprocessing as mp
-
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    n = 5_000_003
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, k, q, packed, overlap)) for r in range(2)]
-    for p in procs:
-        p.start()
-    merged, single = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    merged, single = _run_two(_worker, (5_000_003, k, (packed, overlap)))
     assert merged == single and len(merged) == k
 
 
@@ -126,19 +150,7 @@ def test_two_gpu_p2p_exchange_equals_single_gpu(k, steps, lap):
     """The peer-memory exchange (the fused launch writes its elite into every rank's
     ring over NVLink, laps merged after a device-side wait on the blocks' sequence
     words): every step's merged elite equals the single-GPU elite of the batch."""
-    import torch.multiprocessing as mp
-
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    n = 3_000_017
-    procs = [ctx.Process(target=_worker_p2p, args=(r, 2, port, n, k, q, steps, lap)) for r in range(2)]
-    for p in procs:
-        p.start()
-    merged, single = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    merged, single = _run_two(_worker_p2p, (3_000_017, k, (steps, lap)))
     assert len(single) == k
     for m in merged:
         assert m == single
